@@ -1,0 +1,389 @@
+"""Benchmark: flex_conv forward + backward points/sec on B200 (BASELINE.json metric).
+
+Workload (config C4 shape, with the backward the metric names): one flex-conv layer on a
+single synthetic uniform-random cloud of N = 7,000,000 points, K = 8 (kNN, self
+included), 64 -> 64 channels, Dp = 3, fp32 I/O.  A step = forward (out) + full backward
+(d_features, d_theta, d_theta_b, d_locations) -- the reference harness's fwd and
+bwd-with-locations pair (harness.py:520-527).  Neighbourhood (kNN) and reverse CSR are
+built once before timing (as harness.py:516-517 does) and reported separately.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--mode M]
+
+N > 1 (torchrun, one rank per GPU): weak scaling -- each rank runs its own 7M-point cloud
+and the theta/theta_b gradients are all-reduced over NCCL every step (the data-parallel
+training collective); value = all points / max-over-ranks time.
+--impl reference: the reference's own CPU kernels (oracle/_ref, built from
+/root/reference by oracle/build_ref.sh; else the C restatement in oracle/) on the host
+cores, rank 0 only, a bounded sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "flex_conv fwd+bwd points/sec (1M-7M pts, K=8, 64->64)"
+UNIT = "points/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=7_000_000)
+    ap.add_argument("--k", type=int, default=8)
+    ap.add_argument("--c", type=int, default=64)
+    ap.add_argument("--mode", default="auto")
+    ap.add_argument("--cpu-sample", type=int, default=131072)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops", 1590.0)), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def algo_bytes_per_point(c_in, c_out, d, k, s=4):
+    """compulsory bytes per point (fp32 I/O, int32 indices)."""
+    fwd = s * c_in + 4 * d + 4 * k + s * c_out
+    bwd = s * c_out + s * c_in + 4 * d + 4 * k + (4 + 4 * k) + s * c_in + 4 * d
+    return fwd, bwd
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ CPU reference / baseline
+def cpu_kernels():
+    """The reference's own compiled kernels (oracle/_ref) if built, else the C restatement."""
+    from oracle import oracle
+
+    nat = oracle.ref_native()
+    if nat is not None:
+        return "reference", nat
+    oracle.build()
+    return "port", None
+
+
+def cpu_sample(n_sample, k, c, seed=4):
+    """A bounded sample of the workload: an n_sample-point cloud of the same construction."""
+    import torch
+
+    from paper_1803_07289_b200 import _ops
+    from paper_1803_07289_b200.core import synthetic_layer
+
+    loc, feat, th, tb, up = synthetic_layer(seed, 0, n_sample, 3, c, c)
+    pts = torch.from_numpy(loc).cuda()
+    nbr = _ops.knn(pts, 1, n_sample, k).to(torch.int64).cpu().numpy()
+    return loc, feat, th, tb, up, nbr
+
+
+def time_cpu_step(kind, nat, sample):
+    """One fwd + bwd(with locations) of the reference kernels on the sample; seconds."""
+    from oracle import oracle
+
+    loc, feat, th, tb, up, nbr = sample
+    nthreads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    if kind == "reference":
+        out = np.empty((feat.shape[0], th.shape[0]))
+        nat.flex_conv_forward(feat, loc, nbr, th, tb, out, nthreads)
+        t1 = time.perf_counter()
+        bufs = [np.zeros_like(feat), np.zeros_like(loc), np.zeros_like(th), np.zeros_like(tb)]
+        nat.flex_conv_backward(up, feat, loc, nbr, th, tb, bufs[0], bufs[1], bufs[2], bufs[3], True)
+    else:
+        oracle.conv_forward(feat, loc, nbr, th, tb, num_threads=nthreads)
+        t1 = time.perf_counter()
+        oracle.conv_backward(up, feat, loc, nbr, th, tb, True)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1
+
+
+# ------------------------------------------------------------------ distributed
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1803_07289_b200 import _lib, _ops
+
+    n, k, c, d = args.n, args.k, args.c, 3
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    # positions on the 2^-24 lattice (exact in fp32), spatially ordered once
+    pos = torch.floor(torch.rand(n, d, generator=gen, device=dev, dtype=torch.float64) * 2 ** 24) / 2 ** 24
+    pos = pos.to(torch.float32)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    order = _ops.spatial_order(pos)
+    pos = pos[order.long()].contiguous()
+    torch.cuda.synchronize()
+    sort_ms = (time.perf_counter() - t0) * 1e3
+    feat = torch.randn(n, c, generator=gen, device=dev)
+    g = torch.randn(n, c, generator=gen, device=dev)
+    theta = 0.1 * torch.randn(c, c, d, generator=gen, device=dev)
+    theta_b = 0.1 * torch.randn(c, c, generator=gen, device=dev)
+
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    nbr = _ops.knn(pos, 1, n, k)
+    e1.record()
+    torch.cuda.synchronize()
+    knn_ms = e0.elapsed_time(e1)
+    e0.record()
+    csr = _ops.csr_build(nbr, 1, n)
+    e1.record()
+    torch.cuda.synchronize()
+    csr_ms = e0.elapsed_time(e1)
+
+    def step(phase_events=None):
+        if phase_events:
+            phase_events[0].record()
+        _ops.conv_forward(feat, pos, nbr, theta, theta_b, 1, n, args.mode)
+        if phase_events:
+            phase_events[1].record()
+        _, dth, dtb, _ = _ops.conv_backward(g, feat, pos, nbr, csr, theta, theta_b, 1, n,
+                                            need=(True, True, True, True), mode=args.mode)
+        if phase_events:
+            phase_events[2].record()
+        if world > 1:
+            flat = torch.cat([dth.reshape(-1), dtb.reshape(-1)])
+            dist.all_reduce(flat)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    launches0 = _lib.launch_count()
+    phases = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        for s in range(args.steps):
+            step(phases[s])
+        stop.record()
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    ms_total = start.elapsed_time(stop)
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    fwd_ms = statistics.median(p[0].elapsed_time(p[1]) for p in phases)
+    bwd_ms = statistics.median(p[1].elapsed_time(p[2]) for p in phases)
+    value = world * n / (ms_step / 1e3)
+
+    # ---------------- e2e: host buffers through the C ABI, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, torch, _ops, feat, pos, nbr, g, theta, theta_b, n, k, world, dist)
+
+    hbm, bf16, src = peaks()
+    fwd_b, bwd_b = algo_bytes_per_point(c, c, d, k)
+    # dominant kernel = the larger phase; achieved = algorithmic bytes / its device time
+    if bwd_ms >= fwd_ms:
+        dom, dom_ms, dom_b = "conv_backward", bwd_ms, bwd_b
+    else:
+        dom, dom_ms, dom_b = "conv_forward", fwd_ms, fwd_b
+    achieved = dom_b * n / (dom_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": src,
+                "algorithmic_bytes_per_point": dom_b,
+                "phases": {"forward": {"ms": round(fwd_ms, 4), "bytes_per_point": fwd_b,
+                                       "GBps": round(fwd_b * n / fwd_ms / 1e6, 1)},
+                           "backward": {"ms": round(bwd_ms, 4), "bytes_per_point": bwd_b,
+                                        "GBps": round(bwd_b * n / bwd_ms / 1e6, 1)}}}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        kind, nat = cpu_kernels()
+        sample = cpu_sample(args.cpu_sample, k, c)
+        tf, tb_ = time_cpu_step(kind, nat, sample)
+        cpu = {"value": round(args.cpu_sample / (tf + tb_), 1), "unit": UNIT, "cores": os.cpu_count(),
+               "kind": kind,
+               "sample": f"{args.cpu_sample}-point cloud, K={k}, {c}->{c}, fwd {tf:.2f}s on "
+                         f"{os.cpu_count()} threads + bwd {tb_:.2f}s (single-threaded by reference design, "
+                         f"_native.pyx:77-78), fp64"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"flex_conv fwd+bwd (with d_locations), one {n}-point uniform cloud "
+                                   f"per GPU, K={k}, {c}->{c}, Dp=3",
+                       "points_per_gpu": n, "k": k, "c_in": c, "c_out": c, "dp": d, "mode": args.mode,
+                       "parallelism": f"dp{world}" if world > 1 else "single",
+                       "l2": "inputs (>= 1.8 GB) exceed the 126 MB L2; no flush needed",
+                       "setup_ms": {"spatial_order": round(sort_ms, 2), "knn": round(knn_ms, 3),
+                                    "reverse_csr": round(csr_ms, 3)}},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, torch, _ops, feat, pos, nbr, g, theta, theta_b, n, k, world, dist):
+    """Same metric through the C ABI with pinned HOST buffers: every step copies the inputs
+    H2D, rebuilds the reverse neighbourhood, runs fwd + bwd and copies the results D2H."""
+    dev = feat.device
+    host_in = [t.cpu().pin_memory() for t in (feat, pos, nbr, g, theta, theta_b)]
+    outs_shape = [(n, theta.shape[0]), (n, feat.shape[1]), tuple(theta.shape), tuple(theta_b.shape), (n, 3)]
+    host_out = [torch.empty(s, dtype=torch.float32).pin_memory() for s in outs_shape]
+    h2d = sum(t.numel() * t.element_size() for t in host_in)
+    d2h = sum(t.numel() * t.element_size() for t in host_out)
+    steps = max(1, min(args.steps, 5))
+
+    def one():
+        f, p, nb, gg, th, tb = (t.to(dev, non_blocking=True) for t in host_in)
+        csr = _ops.csr_build(nb, 1, n)
+        out = _ops.conv_forward(f, p, nb, th, tb, 1, n, args.mode)
+        df, dth, dtb, dl = _ops.conv_backward(gg, f, p, nb, csr, th, tb, 1, n, mode=args.mode)
+        for h, dv in zip(host_out, (out, df, dth, dtb, dl)):
+            h.copy_(dv, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        one()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": round(world * n / (ms / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3), "steps": steps,
+            "path": "C ABI (fc_csr_build + fc_conv_forward + fc_conv_backward), pinned host fp32 buffers"}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU kernels on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    kind, nat = cpu_kernels()
+    n_sample = min(args.cpu_sample, 65536)
+    sample = cpu_sample(n_sample, args.k, args.c)
+    for _ in range(args.warmup):
+        time_cpu_step(kind, nat, sample)
+    t0 = time.perf_counter()
+    fw = bw = 0.0
+    for _ in range(args.steps):
+        a, b = time_cpu_step(kind, nat, sample)
+        fw += a
+        bw += b
+    total = time.perf_counter() - t0
+    ms_step = total / args.steps * 1e3
+    value = n_sample / (total / args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"flex_conv fwd+bwd (with d_locations), K={args.k}, {args.c}->{args.c}, Dp=3; "
+                               f"each step a {n_sample}-point sample of the {args.n}-point workload",
+                   "points_per_step": n_sample, "parallelism": "cpu"},
+        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
+                         "sample": f"{n_sample}-point cloud per step; fwd on {os.cpu_count()} threads "
+                                   f"({fw / args.steps:.2f}s), bwd single-threaded by reference design "
+                                   f"({bw / args.steps:.2f}s)"},
+        "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,172 @@
+/*
+ * flexconv_b200.h -- C ABI of the B200-native flex-convolution hot path.
+ *
+ * The drop-in boundary: plain pointers, sizes and a cudaStream_t (passed as void*),
+ * int status codes, caller-allocated outputs, no torch types.  Each entry point names
+ * the reference interface it replaces.  The reference's kernel slot is the module ABI
+ * shared by flexconv._native and flexconv._reference (identical signatures,
+ * /root/reference/pkg/src/flexconv/_reference.py:3-4) selected by backend.active()
+ * (/root/reference/pkg/src/flexconv/backend.py:34-36); its callers are the flexops /
+ * neighborhood wrappers.  INTEGRATION.md shows the binding a maintainer would add.
+ *
+ * Conventions (all entry points)
+ *  - Device pointers.  Point-major layouts: features [B*N, C], locations [B*N, d],
+ *    neighbours [B*N, k] int32 with CLOUD-LOCAL indices (row i of cloud b lists
+ *    indices in [0, N)); B clouds of N points stacked along the point axis.
+ *    The reference has no batch axis: B = 1 reproduces it exactly.
+ *  - theta [c_out, c_in, d], theta_b [c_out, c_in] -- the reference's FlexConvParams
+ *    shapes (flexops.py:22-51).  Offsets are centre - neighbour (l_i - l_j,
+ *    _native.pyx:55).
+ *  - dtype: FC_F32 or FC_F64 for every floating tensor of the call.  FC_F64 runs
+ *    the reference's arithmetic (fp64, same operation order; forward and pooling
+ *    are bitwise identical to _native).
+ *  - Outputs are OVERWRITTEN (the reference zero-fills then accumulates,
+ *    flexops.py:123-126 -- same result).  Nullable outputs are skipped.
+ *  - Work is enqueued on `stream` (cudaStream_t; NULL = legacy default stream);
+ *    no entry point synchronises the host except fc_knn's grid path (reads a
+ *    48-byte bounding box) and the *_check helpers documented as such.
+ *  - Return FC_OK or an FC_ERR_* code; fc_last_error() holds the message (thread-local).
+ */
+#ifndef FLEXCONV_B200_H
+#define FLEXCONV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FC_ABI_VERSION 1
+
+/* Status codes map 1:1 onto the reference's EngineError kinds (errors.py:8-35). */
+enum {
+    FC_OK = 0,
+    FC_ERR_SHAPE = 1,      /* ShapeMismatchError  */
+    FC_ERR_INDEX = 2,      /* IndexOutOfRangeError */
+    FC_ERR_NONFINITE = 3,  /* NonFiniteError       */
+    FC_ERR_EMPTY = 4,      /* EmptyInputError      */
+    FC_ERR_CONFIG = 5,     /* ConfigInvalidError   */
+    FC_ERR_CUDA = 6,       /* CUDA runtime failure */
+    FC_ERR_UNSUPPORTED = 7 /* shape not covered by the requested engine */
+};
+
+enum { FC_F32 = 0, FC_F64 = 1 };
+
+/* Contraction engine for FC_F32 (ignored for FC_F64, which is always SIMT fp64). */
+enum {
+    FC_MODE_AUTO = 0,      /* tensor-core 3xTF32 where the shape is covered, else SIMT */
+    FC_MODE_SIMT = 1,      /* CUDA-core fp32 FMA                                       */
+    FC_MODE_TC_TF32X3 = 2, /* tcgen05 kind::tf32, 3-pass hi/lo split, fp32 accumulate  */
+    FC_MODE_TC_BF16 = 3    /* tcgen05 kind::f16 bf16 operands, fp32 accumulate (1e-2)  */
+};
+
+/* kNN algorithm selector. */
+enum { FC_KNN_AUTO = 0, FC_KNN_BRUTE = 1, FC_KNN_GRID = 2 };
+
+int fc_abi_version(void);
+const char *fc_last_error(void);
+/* Number of kernel launches this library has issued (process-wide counter). */
+uint64_t fc_launch_count(void);
+
+/* ---- flex_conv -------------------------------------------------------------------
+ * Replaces _native.flex_conv_forward(features, locations, neighbors, theta, theta_b,
+ * out, num_threads) (_native.pyx:25-28), called by flexops.flex_conv_forward
+ * (flexops.py:97-110).  out [B*N, c_out]. */
+int fc_conv_forward(int dtype, int mode, int64_t batch, int64_t n, int c_in, int d, int k,
+                    int c_out, const void *features, const void *locations,
+                    const int32_t *neighbors, const void *theta, const void *theta_b,
+                    void *out, void *stream);
+
+/* Replaces _native.flex_conv_backward(upstream, features, locations, neighbors, theta,
+ * theta_b, d_features, d_locations, d_theta, d_theta_b, with_locations)
+ * (_native.pyx:69-74), called by flexops.flex_conv_backward (flexops.py:113-132).
+ * rev_offsets/rev_entries: the reverse neighbourhood from fc_csr_build (needed when
+ * d_features or d_locations is requested).  d_locations == NULL <=> with_locations=False.
+ * Deterministic: no floating-point atomics; bitwise reproducible run to run. */
+int fc_conv_backward(int dtype, int mode, int64_t batch, int64_t n, int c_in, int d, int k,
+                     int c_out, const void *upstream, const void *features,
+                     const void *locations, const int32_t *neighbors,
+                     const int32_t *rev_offsets, const int32_t *rev_entries,
+                     const void *theta, const void *theta_b, void *d_features,
+                     void *d_locations, void *d_theta, void *d_theta_b, void *stream);
+
+/* ---- flex_deconv (transposed flex_conv) --------------------------------------------
+ * No reference function (the reference drops it); defined as the adjoint
+ * y = A(theta)^T x of flex_conv with the SAME theta shapes.  Exact reference equivalent:
+ * flex_conv_backward(upstream=x, ...).d_features (_native.pyx:106-120).
+ * x [B*N, c_out] -> y [B*N, c_in].  Needs the reverse neighbourhood. */
+int fc_deconv_forward(int dtype, int mode, int64_t batch, int64_t n, int c_in, int d, int k,
+                      int c_out, const void *x, const void *locations,
+                      const int32_t *rev_offsets, const int32_t *rev_entries,
+                      const void *theta, const void *theta_b, void *y, void *stream);
+
+/* ---- reverse neighbourhood ---------------------------------------------------------
+ * Bucket g = b*N + neighbors[e] collects the forward slots e = p*k + s, ascending
+ * (the fixed i-order of the reference's serial scatter, _native.pyx:93-127).
+ * offsets [B*N + 1], entries [B*N*k].  Validates indices (FC_ERR_INDEX). */
+int fc_csr_build(int64_t batch, int64_t n, int k, const int32_t *neighbors,
+                 int32_t *offsets, int32_t *entries, void *stream);
+
+/* ---- flex_pool (neighbourhood max-pool) --------------------------------------------
+ * Replaces _native.max_pool_forward (_native.pyx:130-155) behind flexops.flex_max_pool
+ * (flexops.py:135-151).  argmax [B*N, c] holds the winning CLOUD-LOCAL index; ties go to
+ * the lowest index (_native.pyx:151). */
+int fc_pool_forward(int dtype, int64_t batch, int64_t n, int c, int k, const void *features,
+                    const int32_t *neighbors, void *out, int32_t *argmax, void *stream);
+
+/* Pool backward through the reverse neighbourhood (argmax always lies in N(i)):
+ * d_f[j,c] = sum over i in R(j), ascending, of [argmax[i,c]==j] * g[i,c] -- the same
+ * additions in the same order as _native.max_pool_backward (_native.pyx:158-168). */
+int fc_pool_backward(int dtype, int64_t batch, int64_t n, int c, int k, const void *upstream,
+                     const int32_t *argmax, const int32_t *rev_offsets,
+                     const int32_t *rev_entries, void *d_features, void *stream);
+
+/* Record-only pool backward, the exact flexops.flex_max_pool_backward(upstream, record, n)
+ * contract (flexops.py:154-165): record [n_up, c] indexes rows [0, n_rows).
+ * fc_record_csr_build groups slots e = i*c + ch by (record[e], ch): offsets
+ * [n_rows*c + 1], entries [n_up*c]; fc_pool_backward_record then sums in ascending i. */
+int fc_record_csr_build(int64_t n_up, int64_t n_rows, int c, const int32_t *record,
+                        int32_t *offsets, int32_t *entries, void *stream);
+int fc_pool_backward_record(int dtype, int64_t n_up, int64_t n_rows, int c,
+                            const void *upstream, const int32_t *offsets,
+                            const int32_t *entries, void *d_features, void *stream);
+
+/* ---- kNN neighbourhood builder ------------------------------------------------------
+ * Exact self-kNN: row i = [i, the k-1 nearest other points ordered by (d^2, index)],
+ * d^2 evaluated in fp64 left-to-right over the d coordinates without FMA -- the
+ * contract of knn_query / knn_brute_force (neighborhood.py:149-187, _native.pyx:171-255).
+ * points [B*N, d] (dtype), out [B*N, k] int32 cloud-local.  algo: FC_KNN_*.
+ * The grid path (d <= 3) reads each cloud's bounding box to the host once. */
+int fc_knn(int dtype, int64_t batch, int64_t n, int d, int k, const void *points,
+           int32_t *out, int algo, void *stream);
+
+/* Cell-ordered (spatially coherent) permutation of one cloud: order[q] = point index.
+ * Permutation equivariance (tests/test_flexops.py:263-276) makes any relabelling legal. */
+int fc_spatial_order(int dtype, int64_t n, int d, const void *points, int32_t *order,
+                     void *stream);
+
+/* ---- row movement used by the pooling stage (flexops.py:168-203) --------------------- */
+/* out[r] = in[sel[r]] -- downsample_gather (flexops.py:168-175). */
+int fc_gather_rows(int dtype, int64_t rows_out, int c, const void *in, const int32_t *sel,
+                   void *out, void *stream);
+/* out = 0; out[sel[r]] = in[r], last writer wins on duplicate targets -- scatter_to_fine
+ * (flexops.py:178-190). */
+int fc_scatter_rows(int dtype, int64_t rows_in, int64_t rows_out, int c, const void *in,
+                    const int32_t *sel, void *out, void *stream);
+
+/* ---- index plumbing --------------------------------------------------------------------
+ * int64 -> int32 narrowing with a device-side range check: *bad (device int32) receives
+ * the number of entries outside [0, hi) (the reference's idx.min()/max() scan,
+ * flexops.py:92-93).  fc_check_indices does the same on an int32 table.  If `row_len` > 0
+ * the bound is per cloud: entry e belongs to cloud e / (n_per_cloud*row_len). */
+int fc_indices_to_i32(const int64_t *in, int32_t *out, int64_t count, int64_t hi,
+                      int32_t *bad, void *stream);
+int fc_check_indices(const int32_t *idx, int64_t count, int64_t hi, int32_t *bad,
+                     void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLEXCONV_B200_H */

@@ -1,0 +1,203 @@
+"""Device-level operator layer: torch CUDA tensors in the point-major layout, one C-ABI
+call per operator (include/flexconv_b200.h).  torch supplies allocation and the current
+stream only; every byte of arithmetic runs in libflexconv_b200.so.
+
+Shapes (T = B*N points, B clouds of N points stacked along the point axis):
+  features [T, C], locations [T, d], neighbours [T, K] int32 (cloud-local indices),
+  theta [C_out, C_in, d], theta_b [C_out, C_in], reverse CSR (offsets [T+1], entries [T*K]).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .errors import ShapeMismatchError, UnsupportedError
+
+MODES = {"auto": _lib.MODE_AUTO, "simt": _lib.MODE_SIMT, "tf32x3": _lib.MODE_TC_TF32X3,
+         "bf16": _lib.MODE_TC_BF16}
+
+
+def _mode(mode) -> int:
+    if isinstance(mode, int):
+        return mode
+    try:
+        return MODES[mode]
+    except KeyError as exc:
+        raise UnsupportedError(f"unknown engine {mode!r}; choose from {sorted(MODES)}") from exc
+
+
+def _dtype(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return _lib.FC_F32
+    if t.dtype == torch.float64:
+        return _lib.FC_F64
+    raise UnsupportedError(f"floating tensors must be float32 or float64, got {t.dtype}")
+
+
+def _p(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(t: torch.Tensor):
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _need(t: torch.Tensor, name: str, dtype=None, device=None):
+    if not t.is_cuda:
+        raise UnsupportedError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if dtype is not None and t.dtype != dtype:
+        raise ShapeMismatchError(f"{name} must be {dtype}, got {t.dtype}")
+    if device is not None and t.device != device:
+        raise ShapeMismatchError(f"{name} is on {t.device}, expected {device}")
+    return t.contiguous()
+
+
+def csr_build(nbr: torch.Tensor, batch: int, n: int):
+    """Reverse neighbourhood (stable counting sort): offsets [B*N+1], entries [B*N*K]."""
+    nbr = _need(nbr, "neighbors", torch.int32)
+    k = nbr.shape[-1]
+    off = torch.empty(batch * n + 1, dtype=torch.int32, device=nbr.device)
+    ent = torch.empty(batch * n * k, dtype=torch.int32, device=nbr.device)
+    _lib.call("fc_csr_build", batch, n, k, _p(nbr), _p(off), _p(ent), _stream(nbr))
+    return off, ent
+
+
+def conv_forward(feat, loc, nbr, theta, theta_b, batch, n, mode="auto"):
+    feat = _need(feat, "features")
+    dt, dev = feat.dtype, feat.device
+    loc = _need(loc, "locations", dt, dev)
+    nbr = _need(nbr, "neighbors", torch.int32, dev)
+    theta = _need(theta, "theta", dt, dev)
+    theta_b = _need(theta_b, "theta_b", dt, dev)
+    c_out, c_in, d = theta.shape
+    k = nbr.shape[-1]
+    out = torch.empty(batch * n, c_out, dtype=dt, device=dev)
+    _lib.call("fc_conv_forward", _dtype(feat), _mode(mode), batch, n, c_in, d, k, c_out, _p(feat), _p(loc),
+              _p(nbr), _p(theta), _p(theta_b), _p(out), _stream(feat))
+    return out
+
+
+def conv_backward(g, feat, loc, nbr, csr, theta, theta_b, batch, n, need=(True, True, True, True),
+                  mode="auto"):
+    """Returns (d_features, d_theta, d_theta_b, d_locations); entries not in `need` are None."""
+    feat = _need(feat, "features")
+    dt, dev = feat.dtype, feat.device
+    g = _need(g, "upstream", dt, dev)
+    loc = _need(loc, "locations", dt, dev)
+    nbr = _need(nbr, "neighbors", torch.int32, dev)
+    theta = _need(theta, "theta", dt, dev)
+    theta_b = _need(theta_b, "theta_b", dt, dev)
+    c_out, c_in, d = theta.shape
+    k = nbr.shape[-1]
+    want_df, want_dth, want_dtb, want_dl = need
+    df = torch.empty(batch * n, c_in, dtype=dt, device=dev) if want_df else None
+    dl = torch.empty(batch * n, d, dtype=dt, device=dev) if want_dl else None
+    dth = torch.empty(c_out, c_in, d, dtype=dt, device=dev) if want_dth else None
+    dtb = torch.empty(c_out, c_in, dtype=dt, device=dev) if want_dtb else None
+    off, ent = csr if csr is not None else (None, None)
+    _lib.call("fc_conv_backward", _dtype(feat), _mode(mode), batch, n, c_in, d, k, c_out, _p(g), _p(feat),
+              _p(loc), _p(nbr), _p(off), _p(ent), _p(theta), _p(theta_b), _p(df), _p(dl), _p(dth), _p(dtb),
+              _stream(feat))
+    return df, dth, dtb, dl
+
+
+def deconv_forward(x, loc, csr, theta, theta_b, batch, n, k, mode="auto"):
+    """y = A(theta)^T x: x [T, C_out] -> y [T, C_in]."""
+    x = _need(x, "x")
+    dt, dev = x.dtype, x.device
+    loc = _need(loc, "locations", dt, dev)
+    theta = _need(theta, "theta", dt, dev)
+    theta_b = _need(theta_b, "theta_b", dt, dev)
+    c_out, c_in, d = theta.shape
+    off, ent = csr
+    y = torch.empty(batch * n, c_in, dtype=dt, device=dev)
+    _lib.call("fc_deconv_forward", _dtype(x), _mode(mode), batch, n, c_in, d, k, c_out, _p(x), _p(loc),
+              _p(off), _p(ent), _p(theta), _p(theta_b), _p(y), _stream(x))
+    return y
+
+
+def pool_forward(feat, nbr, batch, n):
+    feat = _need(feat, "features")
+    nbr = _need(nbr, "neighbors", torch.int32, feat.device)
+    c = feat.shape[-1]
+    k = nbr.shape[-1]
+    out = torch.empty_like(feat)
+    am = torch.empty(feat.shape, dtype=torch.int32, device=feat.device)
+    _lib.call("fc_pool_forward", _dtype(feat), batch, n, c, k, _p(feat), _p(nbr), _p(out), _p(am),
+              _stream(feat))
+    return out, am
+
+
+def pool_backward(g, argmax, csr, batch, n, k):
+    g = _need(g, "upstream")
+    argmax = _need(argmax, "argmax", torch.int32, g.device)
+    c = g.shape[-1]
+    df = torch.empty_like(g)
+    off, ent = csr
+    _lib.call("fc_pool_backward", _dtype(g), batch, n, c, k, _p(g), _p(argmax), _p(off), _p(ent), _p(df),
+              _stream(g))
+    return df
+
+
+def pool_backward_record(g, record, n_rows):
+    g = _need(g, "upstream")
+    record = _need(record, "record", torch.int32, g.device)
+    n_up, c = g.shape
+    off = torch.empty(n_rows * c + 1, dtype=torch.int32, device=g.device)
+    ent = torch.empty(max(n_up * c, 1), dtype=torch.int32, device=g.device)
+    _lib.call("fc_record_csr_build", n_up, n_rows, c, _p(record), _p(off), _p(ent), _stream(g))
+    df = torch.empty(n_rows, c, dtype=g.dtype, device=g.device)
+    _lib.call("fc_pool_backward_record", _dtype(g), n_up, n_rows, c, _p(g), _p(off), _p(ent), _p(df), _stream(g))
+    return df
+
+
+def knn(points, batch, n, k, algo=_lib.KNN_AUTO):
+    points = _need(points, "points")
+    d = points.shape[-1]
+    out = torch.empty(batch * n, k, dtype=torch.int32, device=points.device)
+    _lib.call("fc_knn", _dtype(points), batch, n, d, k, _p(points), _p(out), int(algo), _stream(points))
+    return out
+
+
+def spatial_order(points):
+    points = _need(points, "points")
+    n, d = points.shape
+    order = torch.empty(n, dtype=torch.int32, device=points.device)
+    _lib.call("fc_spatial_order", _dtype(points), n, d, _p(points), _p(order), _stream(points))
+    return order
+
+
+def gather_rows(x, sel):
+    x = _need(x, "features")
+    sel = _need(sel, "selection", torch.int32, x.device)
+    out = torch.empty(sel.numel(), x.shape[1], dtype=x.dtype, device=x.device)
+    _lib.call("fc_gather_rows", _dtype(x), sel.numel(), x.shape[1], _p(x), _p(sel), _p(out), _stream(x))
+    return out
+
+
+def scatter_rows(x, sel, rows_out):
+    x = _need(x, "features")
+    sel = _need(sel, "selection", torch.int32, x.device)
+    out = torch.empty(rows_out, x.shape[1], dtype=x.dtype, device=x.device)
+    _lib.call("fc_scatter_rows", _dtype(x), x.shape[0], rows_out, x.shape[1], _p(x), _p(sel), _p(out),
+              _stream(x))
+    return out
+
+
+def narrow_indices(idx64, hi):
+    """int64 -> int32 with the reference's [0, hi) range check; returns (idx32, bad_count)."""
+    idx64 = _need(idx64, "indices", torch.int64)
+    out = torch.empty(idx64.shape, dtype=torch.int32, device=idx64.device)
+    bad = torch.zeros(1, dtype=torch.int32, device=idx64.device)
+    _lib.call("fc_indices_to_i32", _p(idx64), _p(out), idx64.numel(), int(hi), _p(bad), _stream(idx64))
+    return out, bad
+
+
+def check_indices(idx32, hi):
+    idx32 = _need(idx32, "indices", torch.int32)
+    bad = torch.zeros(1, dtype=torch.int32, device=idx32.device)
+    _lib.call("fc_check_indices", _p(idx32), idx32.numel(), int(hi), _p(bad), _stream(idx32))
+    return bad

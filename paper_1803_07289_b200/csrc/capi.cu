@@ -1,0 +1,368 @@
+// capi.cu -- the extern "C" boundary (include/flexconv_b200.h): argument validation,
+// dtype/engine dispatch, stream-ordered scratch, error reporting, launch accounting.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+
+#include "fc_common.cuh"
+
+namespace fc {
+
+static thread_local char g_err[512] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+int set_error(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int check_launch(const char *what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(FC_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return FC_OK;
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// Stream-ordered scratch from the device's default memory pool (kept resident: the
+// release threshold is raised once so repeated calls do not return memory to the OS).
+void *scratch_alloc(size_t bytes, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        configured = true;
+    }
+    void *p = nullptr;
+    if (bytes == 0) bytes = 16;
+    if (cudaMallocAsync(&p, bytes, st) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+void scratch_free(void *p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
+
+// conv_simt.cu
+template <typename T>
+void launch_pack(int cin, int d, int cout, const T *theta, const T *theta_b, T *wt, T *wr, cudaStream_t st);
+template <typename T>
+int launch_gmc(bool reverse, int64_t total, int64_t n, int d, int gc, int k, int cout, const T *rows,
+               const T *loc, const int32_t *nbr, Csr csr, const T *w, T *out, const T *feat,
+               const T *theta, const T *centre, T *dloc, cudaStream_t st);
+template <typename T>
+int launch_dloc_centre(int64_t total, int64_t n, int d, int cin, int k, int cout, const T *feat,
+                       const int32_t *nbr, const T *g, const T *theta, T *centre, cudaStream_t st);
+template <typename T>
+int launch_dtheta(int64_t total, int64_t n, int d, int cin, int k, int cout, const T *feat,
+                  const T *loc, const int32_t *nbr, const T *g, T *d_theta, T *d_theta_b, cudaStream_t st);
+// conv_tc.cu
+int tc_conv_forward_supported(int mode, int c_in, int d, int k, int c_out);
+int tc_conv_forward(int mode, int64_t total, int64_t n, int c_in, int d, int k, int c_out,
+                    const float *feat, const float *loc, const int32_t *nbr, const float *theta,
+                    const float *theta_b, float *out, cudaStream_t st);
+int tc_reverse_supported(int mode, int gc, int d, int cout);
+int tc_reverse_gmc(int mode, int64_t total, int64_t n, int gc, int d, int k, int cout,
+                   const float *rows, const float *loc, Csr csr, const float *theta,
+                   const float *theta_b, float *out, cudaStream_t st);
+// pool_csr.cu
+template <typename T>
+int launch_pool_fwd(int64_t total, int64_t n, int c, int k, const T *feat, const int32_t *nbr, T *out,
+                    int32_t *argmax, cudaStream_t st);
+template <typename T>
+int launch_pool_bwd(int64_t total, int64_t n, int c, int k, const T *g, const int32_t *argmax, Csr csr,
+                    T *df, cudaStream_t st);
+template <typename T>
+int launch_pool_bwd_record(int64_t n_rows, int c, const T *g, const int32_t *off, const int32_t *ent,
+                           T *df, cudaStream_t st);
+template <typename T>
+int launch_gather_rows(int64_t rows_out, int c, const T *in, const int32_t *sel, T *out, cudaStream_t st);
+template <typename T>
+int launch_scatter_rows(int64_t rows_in, int64_t rows_out, int c, const T *in, const int32_t *sel, T *out,
+                        cudaStream_t st);
+int launch_narrow_indices(const int64_t *in, int32_t *out, int64_t count, int64_t hi, int32_t *bad,
+                          cudaStream_t st);
+int launch_check_indices(const int32_t *in, int64_t count, int64_t hi, int32_t *bad, cudaStream_t st);
+// knn.cu
+template <typename PT>
+int launch_knn(int64_t batch, int64_t n, int d, int k, const PT *pts, int32_t *out, int algo, cudaStream_t st);
+template <typename PT>
+int launch_spatial_order(int64_t n, int d, const PT *pts, int32_t *order, cudaStream_t st);
+
+}  // namespace fc
+
+using namespace fc;
+
+#define ST(s) (reinterpret_cast<cudaStream_t>(s))
+
+static int check_dtype(int dtype) {
+    if (dtype != FC_F32 && dtype != FC_F64) return set_error(FC_ERR_CONFIG, "unknown dtype %d", dtype);
+    return FC_OK;
+}
+
+static int check_conv_shape(int64_t batch, int64_t n, int c_in, int d, int k, int c_out) {
+    if (batch < 1 || n < 1) return set_error(FC_ERR_EMPTY, "empty input (batch=%lld, n=%lld)", (long long)batch, (long long)n);
+    if (c_in < 1 || c_out < 1) return set_error(FC_ERR_SHAPE, "channel counts must be >= 1 (c_in=%d, c_out=%d)", c_in, c_out);
+    if (d < 1 || d > kMaxDp) return set_error(FC_ERR_UNSUPPORTED, "spatial dimension d=%d outside [1, %d]", d, kMaxDp);
+    if (k < 1) return set_error(FC_ERR_SHAPE, "neighbourhood size k must be >= 1 (got %d)", k);
+    if (batch * n * (int64_t)k >= (int64_t)INT32_MAX) return set_error(FC_ERR_UNSUPPORTED, "B*N*k exceeds the int32 slot space");
+    return FC_OK;
+}
+
+extern "C" {
+
+int fc_abi_version(void) { return FC_ABI_VERSION; }
+const char *fc_last_error(void) { return g_err; }
+uint64_t fc_launch_count(void) { return g_launches.load(); }
+
+int fc_conv_forward(int dtype, int mode, int64_t batch, int64_t n, int c_in, int d, int k, int c_out,
+                    const void *features, const void *locations, const int32_t *neighbors,
+                    const void *theta, const void *theta_b, void *out, void *stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (int rc = check_conv_shape(batch, n, c_in, d, k, c_out)) return rc;
+    cudaStream_t st = ST(stream);
+    const int64_t total = batch * n;
+    if (dtype == FC_F32 && mode != FC_MODE_SIMT) {
+        if (tc_conv_forward_supported(mode, c_in, d, k, c_out))
+            return tc_conv_forward(mode, total, n, c_in, d, k, c_out, (const float *)features,
+                                   (const float *)locations, neighbors, (const float *)theta,
+                                   (const float *)theta_b, (float *)out, st);
+        if (mode != FC_MODE_AUTO)
+            return set_error(FC_ERR_UNSUPPORTED, "tensor-core engine %d does not cover c_in=%d d=%d c_out=%d", mode, c_in, d, c_out);
+    }
+    auto run = [&](auto tag) -> int {
+        using T = decltype(tag);
+        const size_t wbytes = (size_t)c_out * c_in * (d + 1) * sizeof(T);
+        T *wt = (T *)scratch_alloc(wbytes, st);
+        if (!wt) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+        launch_pack<T>(c_in, d, c_out, (const T *)theta, (const T *)theta_b, wt, nullptr, st);
+        int rc = launch_gmc<T>(false, total, n, d, c_in, k, c_out, (const T *)features, (const T *)locations,
+                               neighbors, Csr{nullptr, nullptr}, wt, (T *)out, nullptr, nullptr, nullptr, nullptr, st);
+        scratch_free(wt, st);
+        return rc;
+    };
+    return dtype == FC_F32 ? run(float{}) : run(double{});
+}
+
+int fc_conv_backward(int dtype, int mode, int64_t batch, int64_t n, int c_in, int d, int k, int c_out,
+                     const void *upstream, const void *features, const void *locations,
+                     const int32_t *neighbors, const int32_t *rev_offsets, const int32_t *rev_entries,
+                     const void *theta, const void *theta_b, void *d_features, void *d_locations,
+                     void *d_theta, void *d_theta_b, void *stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (int rc = check_conv_shape(batch, n, c_in, d, k, c_out)) return rc;
+    if ((d_features || d_locations) && (!rev_offsets || !rev_entries))
+        return set_error(FC_ERR_CONFIG, "d_features/d_locations need the reverse neighbourhood (fc_csr_build)");
+    cudaStream_t st = ST(stream);
+    const int64_t total = batch * n;
+    auto run = [&](auto tag) -> int {
+        using T = decltype(tag);
+        const T *g = (const T *)upstream;
+        const T *f = (const T *)features;
+        const T *l = (const T *)locations;
+        const T *th = (const T *)theta;
+        int rc = FC_OK;
+        if (d_theta || d_theta_b) {
+            rc = launch_dtheta<T>(total, n, d, c_in, k, c_out, f, l, neighbors, g, (T *)d_theta, (T *)d_theta_b, st);
+            if (rc) return rc;
+        }
+        if (d_features || d_locations) {
+            T *centre = nullptr;
+            if (d_locations) {
+                centre = (T *)scratch_alloc(sizeof(T) * total * d, st);
+                if (!centre) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+                rc = launch_dloc_centre<T>(total, n, d, c_in, k, c_out, f, neighbors, g, th, centre, st);
+                if (rc) return rc;
+            }
+            T *df = (T *)d_features;
+            T *df_scratch = nullptr;
+            if (!df) df = df_scratch = (T *)scratch_alloc(sizeof(T) * total * c_in, st);
+            const bool tc = dtype == FC_F32 && mode != FC_MODE_SIMT && !d_locations &&
+                            tc_reverse_supported(mode, c_out, d, c_in);
+            if (tc) {
+                rc = tc_reverse_gmc(mode, total, n, c_out, d, k, c_in, (const float *)g, (const float *)l,
+                                    Csr{rev_offsets, rev_entries}, (const float *)th, (const float *)theta_b,
+                                    (float *)df, st);
+            } else {
+                T *wr = (T *)scratch_alloc((size_t)c_out * c_in * (d + 1) * sizeof(T), st);
+                launch_pack<T>(c_in, d, c_out, th, (const T *)theta_b, nullptr, wr, st);
+                rc = launch_gmc<T>(true, total, n, d, c_out, k, c_in, g, l, neighbors, Csr{rev_offsets, rev_entries},
+                                   wr, df, f, th, centre, (T *)d_locations, st);
+                scratch_free(wr, st);
+            }
+            scratch_free(df_scratch, st);
+            scratch_free(centre, st);
+        }
+        return rc;
+    };
+    return dtype == FC_F32 ? run(float{}) : run(double{});
+}
+
+int fc_deconv_forward(int dtype, int mode, int64_t batch, int64_t n, int c_in, int d, int k, int c_out,
+                      const void *x, const void *locations, const int32_t *rev_offsets,
+                      const int32_t *rev_entries, const void *theta, const void *theta_b, void *y,
+                      void *stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (int rc = check_conv_shape(batch, n, c_in, d, k, c_out)) return rc;
+    if (!rev_offsets || !rev_entries) return set_error(FC_ERR_CONFIG, "flex_deconv needs the reverse neighbourhood");
+    cudaStream_t st = ST(stream);
+    const int64_t total = batch * n;
+    if (dtype == FC_F32 && mode != FC_MODE_SIMT) {
+        if (tc_reverse_supported(mode, c_out, d, c_in))
+            return tc_reverse_gmc(mode, total, n, c_out, d, k, c_in, (const float *)x, (const float *)locations,
+                                  Csr{rev_offsets, rev_entries}, (const float *)theta, (const float *)theta_b,
+                                  (float *)y, st);
+        if (mode != FC_MODE_AUTO)
+            return set_error(FC_ERR_UNSUPPORTED, "tensor-core engine %d does not cover this deconv shape", mode);
+    }
+    auto run = [&](auto tag) -> int {
+        using T = decltype(tag);
+        T *wr = (T *)scratch_alloc((size_t)c_out * c_in * (d + 1) * sizeof(T), st);
+        if (!wr) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+        launch_pack<T>(c_in, d, c_out, (const T *)theta, (const T *)theta_b, nullptr, wr, st);
+        int rc = launch_gmc<T>(true, total, n, d, c_out, k, c_in, (const T *)x, (const T *)locations, nullptr,
+                               Csr{rev_offsets, rev_entries}, wr, (T *)y, nullptr, nullptr, nullptr, nullptr, st);
+        scratch_free(wr, st);
+        return rc;
+    };
+    return dtype == FC_F32 ? run(float{}) : run(double{});
+}
+
+int fc_csr_build(int64_t batch, int64_t n, int k, const int32_t *neighbors, int32_t *offsets,
+                 int32_t *entries, void *stream) {
+    if (batch < 1 || n < 1 || k < 1) return set_error(FC_ERR_EMPTY, "empty neighbourhood");
+    if (batch * n * (int64_t)k >= (int64_t)INT32_MAX) return set_error(FC_ERR_UNSUPPORTED, "B*N*k exceeds int32");
+    cudaStream_t st = ST(stream);
+    int32_t *bad = (int32_t *)scratch_alloc(sizeof(int32_t), st);
+    cudaMemsetAsync(bad, 0, sizeof(int32_t), st);
+    int rc = build_csr(neighbors, batch * n * k, BucketFn{0, n, k}, batch * n, offsets, entries, bad, st);
+    int32_t bad_h = 0;
+    cudaMemcpyAsync(&bad_h, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    scratch_free(bad, st);
+    cudaStreamSynchronize(st);
+    if (rc) return rc;
+    if (int rc2 = check_launch("fc_csr_build")) return rc2;
+    if (bad_h) return set_error(FC_ERR_INDEX, "neighbor index out of [0, n) (%d entries)", bad_h);
+    return FC_OK;
+}
+
+int fc_pool_forward(int dtype, int64_t batch, int64_t n, int c, int k, const void *features,
+                    const int32_t *neighbors, void *out, int32_t *argmax, void *stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (batch < 1 || n < 1) return set_error(FC_ERR_EMPTY, "empty input");
+    if (c < 1 || k < 1) return set_error(FC_ERR_SHAPE, "c and k must be >= 1");
+    cudaStream_t st = ST(stream);
+    if (dtype == FC_F32)
+        return launch_pool_fwd<float>(batch * n, n, c, k, (const float *)features, neighbors, (float *)out, argmax, st);
+    return launch_pool_fwd<double>(batch * n, n, c, k, (const double *)features, neighbors, (double *)out, argmax, st);
+}
+
+int fc_pool_backward(int dtype, int64_t batch, int64_t n, int c, int k, const void *upstream,
+                     const int32_t *argmax, const int32_t *rev_offsets, const int32_t *rev_entries,
+                     void *d_features, void *stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (batch < 1 || n < 1) return set_error(FC_ERR_EMPTY, "empty input");
+    if (!rev_offsets || !rev_entries) return set_error(FC_ERR_CONFIG, "pool backward needs the reverse neighbourhood");
+    cudaStream_t st = ST(stream);
+    Csr csr{rev_offsets, rev_entries};
+    if (dtype == FC_F32)
+        return launch_pool_bwd<float>(batch * n, n, c, k, (const float *)upstream, argmax, csr, (float *)d_features, st);
+    return launch_pool_bwd<double>(batch * n, n, c, k, (const double *)upstream, argmax, csr, (double *)d_features, st);
+}
+
+int fc_record_csr_build(int64_t n_up, int64_t n_rows, int c, const int32_t *record, int32_t *offsets,
+                        int32_t *entries, void *stream) {
+    if (n_rows < 1 || c < 1) return set_error(FC_ERR_EMPTY, "empty record");
+    if (n_up * (int64_t)c >= (int64_t)INT32_MAX || n_rows * (int64_t)c >= (int64_t)INT32_MAX)
+        return set_error(FC_ERR_UNSUPPORTED, "record too large for int32 slots");
+    cudaStream_t st = ST(stream);
+    int32_t *bad = (int32_t *)scratch_alloc(sizeof(int32_t), st);
+    cudaMemsetAsync(bad, 0, sizeof(int32_t), st);
+    int rc = build_csr(record, n_up * c, BucketFn{1, n_rows, c}, n_rows * c, offsets, entries, bad, st);
+    int32_t bad_h = 0;
+    cudaMemcpyAsync(&bad_h, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    scratch_free(bad, st);
+    cudaStreamSynchronize(st);
+    if (rc) return rc;
+    if (bad_h) return set_error(FC_ERR_INDEX, "corrupt pool record: winner index out of range");
+    return check_launch("fc_record_csr_build");
+}
+
+int fc_pool_backward_record(int dtype, int64_t n_up, int64_t n_rows, int c, const void *upstream,
+                            const int32_t *offsets, const int32_t *entries, void *d_features, void *stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    (void)n_up;
+    cudaStream_t st = ST(stream);
+    if (dtype == FC_F32)
+        return launch_pool_bwd_record<float>(n_rows, c, (const float *)upstream, offsets, entries, (float *)d_features, st);
+    return launch_pool_bwd_record<double>(n_rows, c, (const double *)upstream, offsets, entries, (double *)d_features, st);
+}
+
+__global__ static void self_rows_kernel(int64_t total, int64_t n, int32_t *out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int32_t)(i % n);
+}
+
+int fc_knn(int dtype, int64_t batch, int64_t n, int d, int k, const void *points, int32_t *out, int algo,
+           void *stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (batch < 1 || n < 1) return set_error(FC_ERR_EMPTY, "no points to index");
+    if (d < 1 || d > kMaxDp) return set_error(FC_ERR_UNSUPPORTED, "kNN supports 1 <= d <= %d", kMaxDp);
+    if (k < 1 || k > n) return set_error(FC_ERR_CONFIG, "k must satisfy 1 <= k <= %lld, got %d", (long long)n, k);
+    if (n >= (int64_t)INT32_MAX) return set_error(FC_ERR_UNSUPPORTED, "cloud too large for int32 indices");
+    cudaStream_t st = ST(stream);
+    if (k == 1) {
+        self_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(batch * n, 256), 4096), 256, 0, st>>>(batch * n, n, out);
+        count_launch();
+        return check_launch("self_rows_kernel");
+    }
+    if (dtype == FC_F32) return launch_knn<float>(batch, n, d, k, (const float *)points, out, algo, st);
+    return launch_knn<double>(batch, n, d, k, (const double *)points, out, algo, st);
+}
+
+int fc_spatial_order(int dtype, int64_t n, int d, const void *points, int32_t *order, void *stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (n < 1) return set_error(FC_ERR_EMPTY, "no points");
+    cudaStream_t st = ST(stream);
+    if (dtype == FC_F32) return launch_spatial_order<float>(n, d, (const float *)points, order, st);
+    return launch_spatial_order<double>(n, d, (const double *)points, order, st);
+}
+
+int fc_gather_rows(int dtype, int64_t rows_out, int c, const void *in, const int32_t *sel, void *out, void *stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (rows_out == 0) return FC_OK;
+    cudaStream_t st = ST(stream);
+    if (dtype == FC_F32) return launch_gather_rows<float>(rows_out, c, (const float *)in, sel, (float *)out, st);
+    return launch_gather_rows<double>(rows_out, c, (const double *)in, sel, (double *)out, st);
+}
+
+int fc_scatter_rows(int dtype, int64_t rows_in, int64_t rows_out, int c, const void *in, const int32_t *sel,
+                    void *out, void *stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (rows_out == 0) return FC_OK;
+    cudaStream_t st = ST(stream);
+    if (dtype == FC_F32) return launch_scatter_rows<float>(rows_in, rows_out, c, (const float *)in, sel, (float *)out, st);
+    return launch_scatter_rows<double>(rows_in, rows_out, c, (const double *)in, sel, (double *)out, st);
+}
+
+int fc_indices_to_i32(const int64_t *in, int32_t *out, int64_t count, int64_t hi, int32_t *bad, void *stream) {
+    if (count == 0) return FC_OK;
+    return launch_narrow_indices(in, out, count, hi, bad, ST(stream));
+}
+
+int fc_check_indices(const int32_t *idx, int64_t count, int64_t hi, int32_t *bad, void *stream) {
+    if (count == 0) return FC_OK;
+    return launch_check_indices(idx, count, hi, bad, ST(stream));
+}
+
+}  // extern "C"

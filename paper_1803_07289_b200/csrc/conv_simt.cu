@@ -1,0 +1,441 @@
+// conv_simt.cu -- CUDA-core flex-convolution kernels (fp32 FMA and fp64 reference order).
+//
+// One "gather -> moments -> contraction" kernel serves three operators:
+//   forward      : X_i = sum_{s} (l_i - l_j, 1) (x) f_j  over j = nbr[i, s]       (_native.pyx:47-59)
+//                  out_i = [theta; theta_b] . X_i                                  (_native.pyx:60-66)
+//   d_features / : Y_j = sum_{(i,s) in R(j)} (l_i - l_j, 1) (x) g_i  (reverse CSR)
+//   flex_deconv    d_f_j = [theta; theta_b]^T . Y_j  -- the same sum as the reference's
+//                  per-(i,s) scatter of W_i (_native.pyx:106-120), regrouped per target j.
+// Every warp owns whole points (no cross-warp dependencies, no atomics): results are
+// deterministic and independent of the launch configuration.
+#include "fc_common.cuh"
+
+namespace fc {
+
+// wt[(c*(D+1)+t)*cout + cp] = theta[cp,c,t] (t < D) | theta_b[cp,c] (t == D)   forward packing
+// wr[(cp*(D+1)+t)*cin + c]  = same value                                       adjoint packing
+template <typename T>
+__global__ void pack_weights_kernel(int cin, int d, int cout, const T *__restrict__ theta,
+                                    const T *__restrict__ theta_b, T *__restrict__ wt,
+                                    T *__restrict__ wr) {
+    const int64_t total = (int64_t)cout * cin * (d + 1);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int t = (int)(q % (d + 1));
+        const int64_t r = q / (d + 1);
+        const int c = (int)(r % cin);
+        const int cp = (int)(r / cin);
+        const T v = (t < d) ? theta[((int64_t)cp * cin + c) * d + t] : theta_b[(int64_t)cp * cin + c];
+        if (wt) wt[((int64_t)c * (d + 1) + t) * cout + cp] = v;
+        if (wr) wr[((int64_t)cp * (d + 1) + t) * cin + c] = v;
+    }
+}
+
+// Moments of one centre point, computed by one warp (lanes over channels), written
+// c-major into xs[c*(DP+1) + t].  Per (c,t) the neighbour terms are added in slot
+// order, exactly the reference's accumulation order (_native.pyx:52-59).
+//   REVERSE = false: neighbours j = base + nbr[p*k + s], offset = l_p - l_j
+//   REVERSE = true : (i, s) from the reverse CSR of p, i = e / k, offset = l_i - l_p
+template <typename T, int DP, bool REVERSE>
+__device__ __forceinline__ void warp_moments(const T *__restrict__ rows, int gc,
+                                             const T *__restrict__ loc,
+                                             const int32_t *__restrict__ nbr, int k, Csr csr,
+                                             int64_t p, int64_t base, T *__restrict__ xs,
+                                             int lane) {
+    T lp[DP];
+#pragma unroll
+    for (int t = 0; t < DP; ++t) lp[t] = loc[p * DP + t];
+    int64_t q0 = 0, q1 = k;
+    if (REVERSE) {
+        q0 = csr.off[p];
+        q1 = csr.off[p + 1];
+    }
+    for (int c0 = 0; c0 < gc; c0 += 32) {
+        const int c = c0 + lane;
+        const bool ok = c < gc;
+        T acc[DP + 1];
+#pragma unroll
+        for (int t = 0; t <= DP; ++t) acc[t] = T(0);
+        for (int64_t q = q0; q < q1; ++q) {
+            int64_t j;
+            if (REVERSE)
+                j = (int64_t)csr.ent[q] / k;
+            else
+                j = base + nbr[p * k + q];
+            T o[DP];
+#pragma unroll
+            for (int t = 0; t < DP; ++t)
+                o[t] = REVERSE ? Ar<T>::sub(loc[j * DP + t], lp[t]) : Ar<T>::sub(lp[t], loc[j * DP + t]);
+            const T v = ok ? rows[j * gc + c] : T(0);
+#pragma unroll
+            for (int t = 0; t < DP; ++t) acc[t] = Ar<T>::madd(acc[t], v, o[t]);
+            acc[DP] = Ar<T>::add(acc[DP], v);
+        }
+        if (ok) {
+#pragma unroll
+            for (int t = 0; t <= DP; ++t) xs[c * (DP + 1) + t] = acc[t];
+        }
+    }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Gather-moment-contract.  Each warp processes PPW points at a time (persistent loop).
+//   out[p, cp] = sum_{c, t} w[(c*(DP+1)+t)*cout + cp] * M_p[c, t]   (c-major, t fastest =
+//   the reference's contraction order, _native.pyx:60-66).
+// Optional (REVERSE, dloc != nullptr): neighbour role of the location gradient,
+//   dloc[j,t] = centre[j,t] - sum_c f[j,c] sum_cp theta[cp,c,t] * Y_j[cp, DP]
+// (the -dt terms of _native.pyx:121-127 regrouped per j; `feat` rows have `cout` channels).
+template <typename T, int DP, bool REVERSE, int PPW>
+__global__ void __launch_bounds__(256)
+    gmc_kernel(int64_t total, int64_t n, int gc, int k, int cout, const T *__restrict__ rows,
+               const T *__restrict__ loc, const int32_t *__restrict__ nbr, Csr csr,
+               const T *__restrict__ w, T *__restrict__ out, const T *__restrict__ feat,
+               const T *__restrict__ theta, const T *__restrict__ centre, T *__restrict__ dloc) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ktot = gc * (DP + 1);
+    T *xs = reinterpret_cast<T *>(smem_raw) + (int64_t)warp * PPW * ktot;
+    const int64_t nwarps = (int64_t)gridDim.x * 8;
+    for (int64_t g0 = ((int64_t)blockIdx.x * 8 + warp) * PPW; g0 < total; g0 += nwarps * PPW) {
+#pragma unroll
+        for (int q = 0; q < PPW; ++q) {
+            const int64_t p = g0 + q;
+            if (p < total)
+                warp_moments<T, DP, REVERSE>(rows, gc, loc, nbr, k, csr, p, (p / n) * n,
+                                             xs + q * ktot, lane);
+        }
+        __syncwarp();
+        for (int cp0 = 0; cp0 < cout; cp0 += 32) {
+            const int cp = cp0 + lane;
+            if (cp < cout) {
+                T acc[PPW];
+#pragma unroll
+                for (int q = 0; q < PPW; ++q) acc[q] = T(0);
+                for (int kk = 0; kk < ktot; ++kk) {
+                    const T wv = w[(int64_t)kk * cout + cp];
+#pragma unroll
+                    for (int q = 0; q < PPW; ++q) acc[q] = Ar<T>::madd(acc[q], wv, xs[q * ktot + kk]);
+                }
+#pragma unroll
+                for (int q = 0; q < PPW; ++q)
+                    if (g0 + q < total) out[(g0 + q) * cout + cp] = acc[q];
+            }
+        }
+        if (REVERSE && dloc != nullptr) {
+            // theta is the conv's [gc (= conv c_out), cout (= conv c_in), DP] tensor.
+#pragma unroll
+            for (int q = 0; q < PPW; ++q) {
+                const int64_t p = g0 + q;
+                if (p >= total) break;
+                T part[DP];
+#pragma unroll
+                for (int t = 0; t < DP; ++t) part[t] = T(0);
+                for (int c0 = 0; c0 < cout; c0 += 32) {
+                    const int c = c0 + lane;
+                    if (c < cout) {
+                        T z[DP];
+#pragma unroll
+                        for (int t = 0; t < DP; ++t) z[t] = T(0);
+                        for (int cp = 0; cp < gc; ++cp) {
+                            const T yb = xs[q * ktot + cp * (DP + 1) + DP];
+#pragma unroll
+                            for (int t = 0; t < DP; ++t)
+                                z[t] = Ar<T>::madd(z[t], theta[((int64_t)cp * cout + c) * DP + t], yb);
+                        }
+                        const T fv = feat[p * cout + c];
+#pragma unroll
+                        for (int t = 0; t < DP; ++t) part[t] = Ar<T>::madd(part[t], fv, z[t]);
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < DP; ++t) {
+                    const T s = warp_sum(part[t]);
+                    if (lane == 0) dloc[p * DP + t] = Ar<T>::sub(centre[p * DP + t], s);
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// Centre role of the location gradient:
+//   centre[i,t] = sum_c (sum_s f[j_s, c]) * (sum_cp theta[cp,c,t] g[i,cp])
+// (the +dt terms of _native.pyx:121-127 summed over s: sum_s f_j . W_i[:,t] = X_i[:,D] . W_i[:,t]).
+template <typename T, int DP>
+__global__ void __launch_bounds__(256)
+    dloc_centre_kernel(int64_t total, int64_t n, int cin, int k, int cout,
+                       const T *__restrict__ feat, const int32_t *__restrict__ nbr,
+                       const T *__restrict__ g, const T *__restrict__ theta,
+                       T *__restrict__ centre) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T *gs = reinterpret_cast<T *>(smem_raw) + (int64_t)warp * cout;
+    const int64_t nwarps = (int64_t)gridDim.x * 8;
+    for (int64_t p = (int64_t)blockIdx.x * 8 + warp; p < total; p += nwarps) {
+        const int64_t base = (p / n) * n;
+        for (int cp = lane; cp < cout; cp += 32) gs[cp] = g[p * cout + cp];
+        __syncwarp();
+        T part[DP];
+#pragma unroll
+        for (int t = 0; t < DP; ++t) part[t] = T(0);
+        for (int c0 = 0; c0 < cin; c0 += 32) {
+            const int c = c0 + lane;
+            if (c < cin) {
+                T xb = T(0);
+                for (int s = 0; s < k; ++s) xb = Ar<T>::add(xb, feat[(base + nbr[p * k + s]) * cin + c]);
+                T z[DP];
+#pragma unroll
+                for (int t = 0; t < DP; ++t) z[t] = T(0);
+                for (int cp = 0; cp < cout; ++cp) {
+                    const T gv = gs[cp];
+#pragma unroll
+                    for (int t = 0; t < DP; ++t)
+                        z[t] = Ar<T>::madd(z[t], theta[((int64_t)cp * cin + c) * DP + t], gv);
+                }
+#pragma unroll
+                for (int t = 0; t < DP; ++t) part[t] = Ar<T>::madd(part[t], xb, z[t]);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < DP; ++t) {
+            const T s = warp_sum(part[t]);
+            if (lane == 0) centre[p * DP + t] = s;
+        }
+        __syncwarp();
+    }
+}
+
+// d_theta partials: block (chunk, slice) accumulates, over its contiguous point chunk
+// in ascending order, the entries e = slice*256*RPT + tid + 256*r of
+//   P[cp, c, t] = sum_i g[i, cp] * X_i[c, t]        (_native.pyx:106-112)
+// then writes them to partial[chunk][e]; dtheta_reduce sums chunks in fixed order.
+template <typename T, int DP, int RPT>
+__global__ void __launch_bounds__(256)
+    dtheta_partial_kernel(int64_t total, int64_t n, int cin, int k, int cout,
+                          const T *__restrict__ feat, const T *__restrict__ loc,
+                          const int32_t *__restrict__ nbr, const T *__restrict__ g,
+                          T *__restrict__ partial, int64_t chunk_pts, int tile) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ktot = cin * (DP + 1);
+    const int64_t E = (int64_t)cout * ktot;
+    T *xs = reinterpret_cast<T *>(smem_raw);
+    T *gs = xs + (int64_t)tile * ktot;
+    const int64_t p_begin = (int64_t)blockIdx.x * chunk_pts;
+    const int64_t p_end = min(total, p_begin + chunk_pts);
+    const int64_t e0 = (int64_t)blockIdx.y * 256 * RPT + threadIdx.x;
+    int cps[RPT], kks[RPT];
+    T acc[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        const int64_t e = e0 + 256 * r;
+        cps[r] = (int)(e / ktot);
+        kks[r] = (int)(e % ktot);
+        acc[r] = T(0);
+    }
+    const int ppw = tile / 8;
+    for (int64_t t0 = p_begin; t0 < p_end; t0 += tile) {
+        for (int q = 0; q < ppw; ++q) {
+            const int pl = warp * ppw + q;
+            const int64_t p = t0 + pl;
+            if (p < p_end) {
+                warp_moments<T, DP, false>(feat, cin, loc, nbr, k, Csr{nullptr, nullptr}, p,
+                                           (p / n) * n, xs + (int64_t)pl * ktot, lane);
+                for (int cp = lane; cp < cout; cp += 32) gs[(int64_t)pl * cout + cp] = g[p * cout + cp];
+            }
+        }
+        __syncthreads();
+        const int np = (int)min((int64_t)tile, p_end - t0);
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+            if (e0 + 256 * r < E) {
+                T a = acc[r];
+                for (int pl = 0; pl < np; ++pl)
+                    a = Ar<T>::madd(a, gs[(int64_t)pl * cout + cps[r]], xs[(int64_t)pl * ktot + kks[r]]);
+                acc[r] = a;
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        const int64_t e = e0 + 256 * r;
+        if (e < E) partial[(int64_t)blockIdx.x * E + e] = acc[r];
+    }
+}
+
+// Fixed-order (ascending chunk) reduction of the d_theta partials, accumulated in fp64.
+template <typename T>
+__global__ void dtheta_reduce_kernel(int chunks, int cin, int d, int cout,
+                                     const T *__restrict__ partial, T *__restrict__ d_theta,
+                                     T *__restrict__ d_theta_b) {
+    const int64_t E = (int64_t)cout * cin * (d + 1);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int ch = 0; ch < chunks; ++ch) s = __dadd_rn(s, (double)partial[(int64_t)ch * E + e]);
+        const int cp = (int)(e / (cin * (d + 1)));
+        const int kk = (int)(e % (cin * (d + 1)));
+        const int c = kk / (d + 1), t = kk % (d + 1);
+        if (t < d) {
+            if (d_theta) d_theta[((int64_t)cp * cin + c) * d + t] = (T)s;
+        } else if (d_theta_b) {
+            d_theta_b[(int64_t)cp * cin + c] = (T)s;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// host-side launchers
+// ------------------------------------------------------------------------------------
+
+template <typename F>
+static void set_smem(F *kernel, size_t bytes) {
+    if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+static int grid_for(int64_t work_items, int per_block) {
+    int64_t g = ceil_div(work_items, per_block);
+    const int64_t cap = (int64_t)num_sms() * 8;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+template <typename T>
+void launch_pack(int cin, int d, int cout, const T *theta, const T *theta_b, T *wt, T *wr,
+                 cudaStream_t st) {
+    const int64_t total = (int64_t)cout * cin * (d + 1);
+    pack_weights_kernel<T><<<grid_for(total, 256), 256, 0, st>>>(cin, d, cout, theta, theta_b, wt, wr);
+    count_launch();
+}
+
+template <typename T, int DP, bool REV>
+static int launch_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, const T *rows,
+                         const T *loc, const int32_t *nbr, Csr csr, const T *w, T *out,
+                         const T *feat, const T *theta, const T *centre, T *dloc, cudaStream_t st) {
+    const int ktot = gc * (DP + 1);
+    const size_t per_point = (size_t)ktot * sizeof(T);
+    int ppw = 4;
+    while (ppw > 1 && per_point * ppw * 8 > 96 * 1024) ppw >>= 1;
+    const size_t smem = per_point * ppw * 8;
+    if (smem > 200 * 1024) return set_error(FC_ERR_UNSUPPORTED, "channel count too large for the SIMT engine (%d)", gc);
+    const int grid = grid_for(ceil_div(total, 8 * ppw), 1);
+    switch (ppw) {
+        case 4:
+            set_smem(gmc_kernel<T, DP, REV, 4>, smem);
+            gmc_kernel<T, DP, REV, 4><<<grid, 256, smem, st>>>(total, n, gc, k, cout, rows, loc, nbr, csr, w, out, feat, theta, centre, dloc);
+            break;
+        case 2:
+            set_smem(gmc_kernel<T, DP, REV, 2>, smem);
+            gmc_kernel<T, DP, REV, 2><<<grid, 256, smem, st>>>(total, n, gc, k, cout, rows, loc, nbr, csr, w, out, feat, theta, centre, dloc);
+            break;
+        default:
+            set_smem(gmc_kernel<T, DP, REV, 1>, smem);
+            gmc_kernel<T, DP, REV, 1><<<grid, 256, smem, st>>>(total, n, gc, k, cout, rows, loc, nbr, csr, w, out, feat, theta, centre, dloc);
+            break;
+    }
+    count_launch();
+    return check_launch("gmc_kernel");
+}
+
+#define FC_DP_SWITCH(d, CALL)                                        \
+    switch (d) {                                                     \
+        case 1: { constexpr int DPC = 1; return CALL; }               \
+        case 2: { constexpr int DPC = 2; return CALL; }               \
+        case 3: { constexpr int DPC = 3; return CALL; }               \
+        case 4: { constexpr int DPC = 4; return CALL; }               \
+        case 5: { constexpr int DPC = 5; return CALL; }               \
+        case 6: { constexpr int DPC = 6; return CALL; }               \
+        case 7: { constexpr int DPC = 7; return CALL; }               \
+        case 8: { constexpr int DPC = 8; return CALL; }               \
+        default: return set_error(FC_ERR_UNSUPPORTED, "spatial dimension d=%d outside [1, %d]", d, kMaxDp); \
+    }
+
+template <typename T>
+int launch_gmc(bool reverse, int64_t total, int64_t n, int d, int gc, int k, int cout, const T *rows,
+               const T *loc, const int32_t *nbr, Csr csr, const T *w, T *out, const T *feat,
+               const T *theta, const T *centre, T *dloc, cudaStream_t st) {
+    if (reverse) {
+        FC_DP_SWITCH(d, (launch_gmc_dp<T, DPC, true>(total, n, gc, k, cout, rows, loc, nbr, csr, w, out, feat, theta, centre, dloc, st)));
+    } else {
+        FC_DP_SWITCH(d, (launch_gmc_dp<T, DPC, false>(total, n, gc, k, cout, rows, loc, nbr, csr, w, out, feat, theta, centre, dloc, st)));
+    }
+}
+
+template <typename T, int DP>
+static int launch_dloc_centre_dp(int64_t total, int64_t n, int cin, int k, int cout, const T *feat,
+                                 const int32_t *nbr, const T *g, const T *theta, T *centre,
+                                 cudaStream_t st) {
+    const size_t smem = (size_t)8 * cout * sizeof(T);
+    set_smem(dloc_centre_kernel<T, DP>, smem);
+    dloc_centre_kernel<T, DP><<<grid_for(ceil_div(total, 8), 1), 256, smem, st>>>(total, n, cin, k, cout, feat, nbr, g, theta, centre);
+    count_launch();
+    return check_launch("dloc_centre_kernel");
+}
+
+template <typename T>
+int launch_dloc_centre(int64_t total, int64_t n, int d, int cin, int k, int cout, const T *feat,
+                       const int32_t *nbr, const T *g, const T *theta, T *centre, cudaStream_t st) {
+    FC_DP_SWITCH(d, (launch_dloc_centre_dp<T, DPC>(total, n, cin, k, cout, feat, nbr, g, theta, centre, st)));
+}
+
+template <typename T, int DP>
+static int launch_dtheta_dp(int64_t total, int64_t n, int cin, int k, int cout, const T *feat,
+                            const T *loc, const int32_t *nbr, const T *g, T *d_theta,
+                            T *d_theta_b, cudaStream_t st) {
+    constexpr int RPT = 8;
+    const int ktot = cin * (DP + 1);
+    const int64_t E = (int64_t)cout * ktot;
+    const int slices = (int)ceil_div(E, 256 * RPT);
+    int tile = 32;
+    while (tile > 8 && (size_t)tile * (ktot + cout) * sizeof(T) > 96 * 1024) tile >>= 1;
+    const size_t smem = (size_t)tile * (ktot + cout) * sizeof(T);
+    if (smem > 200 * 1024) return set_error(FC_ERR_UNSUPPORTED, "channel count too large for the SIMT d_theta engine");
+    int64_t want_blocks = (int64_t)num_sms() * 4;
+    int64_t chunks = ceil_div(want_blocks, slices);
+    chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, ceil_div(total, tile)));
+    const int64_t chunk_pts = ceil_div(ceil_div(total, chunks), tile) * tile;
+    chunks = ceil_div(total, chunk_pts);
+    T *partial = (T *)scratch_alloc((size_t)chunks * E * sizeof(T), st);
+    if (!partial) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+    set_smem(dtheta_partial_kernel<T, DP, RPT>, smem);
+    dtheta_partial_kernel<T, DP, RPT><<<dim3((unsigned)chunks, (unsigned)slices), 256, smem, st>>>(
+        total, n, cin, k, cout, feat, loc, nbr, g, partial, chunk_pts, tile);
+    count_launch();
+    dtheta_reduce_kernel<T><<<grid_for(E, 256), 256, 0, st>>>((int)chunks, cin, DP, cout, partial, d_theta, d_theta_b);
+    count_launch();
+    scratch_free(partial, st);
+    return check_launch("dtheta kernels");
+}
+
+template <typename T>
+int launch_dtheta(int64_t total, int64_t n, int d, int cin, int k, int cout, const T *feat,
+                  const T *loc, const int32_t *nbr, const T *g, T *d_theta, T *d_theta_b,
+                  cudaStream_t st) {
+    FC_DP_SWITCH(d, (launch_dtheta_dp<T, DPC>(total, n, cin, k, cout, feat, loc, nbr, g, d_theta, d_theta_b, st)));
+}
+
+#define FC_INST(T)                                                                                   \
+    template void launch_pack<T>(int, int, int, const T *, const T *, T *, T *, cudaStream_t);      \
+    template int launch_gmc<T>(bool, int64_t, int64_t, int, int, int, int, const T *, const T *,    \
+                               const int32_t *, Csr, const T *, T *, const T *, const T *,          \
+                               const T *, T *, cudaStream_t);                                       \
+    template int launch_dloc_centre<T>(int64_t, int64_t, int, int, int, int, const T *,             \
+                                       const int32_t *, const T *, const T *, T *, cudaStream_t);  \
+    template int launch_dtheta<T>(int64_t, int64_t, int, int, int, int, const T *, const T *,       \
+                                  const int32_t *, const T *, T *, T *, cudaStream_t);
+FC_INST(float)
+FC_INST(double)
+
+}  // namespace fc

@@ -1,0 +1,450 @@
+// knn.cu -- exact self-kNN neighbourhood builder.
+//
+// Contract (neighborhood.py:1-8, :149-187; _native.pyx:171-255): row i is
+// [i, the k-1 nearest OTHER points by (squared distance, index)], the distance
+// accumulated in fp64 left to right over the coordinates, each term (p_i - p_j)^2
+// separately rounded (no FMA) -- so equal inputs give bit-identical rows.
+//  * brute : tiled all-pairs scan (candidates in ascending index, so an equal
+//            distance never displaces an earlier index);
+//  * grid  : cell-binned search in Chebyshev shells around the query cell, stopped
+//            only when the k-1-th distance is strictly below the distance to every
+//            unscanned cell (with a conservative margin) -- exact, not approximate.
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <vector>
+
+#include "fc_common.cuh"
+
+namespace fc {
+
+
+__device__ __forceinline__ bool key_less(double d1, int32_t j1, double d2, int32_t j2) {
+    return d1 < d2 || (d1 == d2 && j1 < j2);
+}
+
+template <int KK>
+__device__ __forceinline__ void topk_insert(double (&bd)[KK], int32_t (&bi)[KK], double dist, int32_t j) {
+    if (!key_less(dist, j, bd[KK - 1], bi[KK - 1])) return;
+#pragma unroll
+    for (int q = KK - 1; q > 0; --q) {
+        if (key_less(dist, j, bd[q], bi[q])) {
+            const bool sh = key_less(dist, j, bd[q - 1], bi[q - 1]);
+            bd[q] = sh ? bd[q - 1] : dist;
+            bi[q] = sh ? bi[q - 1] : j;
+        }
+    }
+    if (key_less(dist, j, bd[0], bi[0])) {
+        bd[0] = dist;
+        bi[0] = j;
+    }
+}
+
+template <typename PT>
+__device__ __forceinline__ double coord(const PT *p, int64_t i, int d, int t) {
+    return (double)p[i * d + t];
+}
+
+// ------------------------------------------------------------------------ brute force
+template <typename PT, int KK>
+__global__ void __launch_bounds__(128)
+    knn_brute_kernel(int64_t n, int d, int k, const PT *__restrict__ pts, int32_t *__restrict__ out) {
+    __shared__ double tile[128 * kMaxDp];
+    const int64_t base = (int64_t)blockIdx.y * n;
+    const int64_t i = (int64_t)blockIdx.x * 128 + threadIdx.x;
+    double pi[kMaxDp];
+#pragma unroll
+    for (int t = 0; t < kMaxDp; ++t) pi[t] = (i < n && t < d) ? coord(pts, base + i, d, t) : 0.0;
+    double bd[KK];
+    int32_t bi[KK];
+#pragma unroll
+    for (int q = 0; q < KK; ++q) {
+        bd[q] = DBL_MAX;
+        bi[q] = INT_MAX;
+    }
+    for (int64_t t0 = 0; t0 < n; t0 += 128) {
+        const int64_t jl = t0 + threadIdx.x;
+        if (jl < n)
+            for (int t = 0; t < d; ++t) tile[threadIdx.x * kMaxDp + t] = coord(pts, base + jl, d, t);
+        __syncthreads();
+        const int m = (int)min((int64_t)128, n - t0);
+        if (i < n) {
+            for (int jj = 0; jj < m; ++jj) {
+                const int32_t j = (int32_t)(t0 + jj);
+                if (j == i) continue;
+                double dist = 0.0;
+#pragma unroll
+                for (int t = 0; t < kMaxDp; ++t) {
+                    if (t < d) {
+                        const double dv = __dsub_rn(pi[t], tile[jj * kMaxDp + t]);
+                        dist = __dadd_rn(dist, __dmul_rn(dv, dv));
+                    }
+                }
+                topk_insert<KK>(bd, bi, dist, j);
+            }
+        }
+        __syncthreads();
+    }
+    if (i < n) {
+        int32_t *row = out + (base + i) * k;
+        row[0] = (int32_t)i;
+#pragma unroll
+        for (int q = 0; q < KK; ++q)
+            if (q < k - 1) row[1 + q] = bi[q];
+    }
+}
+
+// Generic (large k) variant: the candidate list lives in local memory.
+template <typename PT>
+__global__ void __launch_bounds__(128)
+    knn_brute_big_kernel(int64_t n, int d, int k, const PT *__restrict__ pts, double *__restrict__ wd,
+                         int32_t *__restrict__ out) {
+    const int64_t base = (int64_t)blockIdx.y * n;
+    const int64_t i = (int64_t)blockIdx.x * 128 + threadIdx.x;
+    if (i >= n) return;
+    const int kk = k - 1;
+    int32_t *row = out + (base + i) * k;
+    double *bd = wd + (base + i) * (int64_t)kk;  // scratch distances, indices go to row[1..]
+    int32_t *bi = row + 1;
+    row[0] = (int32_t)i;
+    int cnt = 0;
+    for (int64_t jl = 0; jl < n; ++jl) {
+        if (jl == i) continue;
+        double dist = 0.0;
+        for (int t = 0; t < d; ++t) {
+            const double dv = __dsub_rn(coord(pts, base + i, d, t), coord(pts, base + jl, d, t));
+            dist = __dadd_rn(dist, __dmul_rn(dv, dv));
+        }
+        int m;
+        if (cnt == kk) {
+            if (!(dist < bd[kk - 1])) continue;
+            m = kk - 1;
+        } else {
+            m = cnt;
+        }
+        int q = m;
+        while (q > 0 && bd[q - 1] > dist) {
+            bd[q] = bd[q - 1];
+            bi[q] = bi[q - 1];
+            --q;
+        }
+        bd[q] = dist;
+        bi[q] = (int32_t)jl;
+        if (cnt < kk) ++cnt;
+    }
+}
+
+// ------------------------------------------------------------------------ grid
+struct GridParams {
+    double lo[3];
+    double h;
+    int G[3];
+    int bits[3];
+    int d;
+};
+
+__device__ __forceinline__ int64_t interleave_cell(const GridParams &gp, int cx, int cy, int cz) {
+    int64_t code = 0;
+    int pos = 0;
+    const int c[3] = {cx, cy, cz};
+    const int maxb = max(gp.bits[0], max(gp.bits[1], gp.bits[2]));
+    for (int l = 0; l < maxb; ++l)
+        for (int t = 0; t < 3; ++t)
+            if (l < gp.bits[t]) code |= (int64_t)((c[t] >> l) & 1) << (pos++);
+    return code;
+}
+
+__device__ __forceinline__ int cell_coord(const GridParams &gp, double x, int t) {
+    if (t >= gp.d) return 0;
+    double f = floor(__ddiv_rn(__dsub_rn(x, gp.lo[t]), gp.h));
+    int c = (int)f;
+    if (f < 0) c = 0;
+    if (f >= gp.G[t]) c = gp.G[t] - 1;
+    return c;
+}
+
+template <typename PT>
+__global__ void bbox_kernel(int64_t n, int d, const PT *__restrict__ pts, double *__restrict__ box) {
+    // one block, 1024 threads: box[t] = min, box[3+t] = max
+    __shared__ double smin[3][32], smax[3][32];
+    double mn[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, mx[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+        for (int t = 0; t < d && t < 3; ++t) {
+            const double v = coord(pts, i, d, t);
+            mn[t] = fmin(mn[t], v);
+            mx[t] = fmax(mx[t], v);
+        }
+    for (int t = 0; t < 3; ++t) {
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[t] = fmin(mn[t], __shfl_xor_sync(0xffffffffu, mn[t], o));
+            mx[t] = fmax(mx[t], __shfl_xor_sync(0xffffffffu, mx[t], o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            smin[t][threadIdx.x >> 5] = mn[t];
+            smax[t][threadIdx.x >> 5] = mx[t];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        for (int t = 0; t < 3; ++t) {
+            double a = threadIdx.x < (blockDim.x >> 5) ? smin[t][threadIdx.x] : DBL_MAX;
+            double b = threadIdx.x < (blockDim.x >> 5) ? smax[t][threadIdx.x] : -DBL_MAX;
+            for (int o = 16; o > 0; o >>= 1) {
+                a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+                b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+            }
+            if (threadIdx.x == 0) {
+                box[t] = a;
+                box[3 + t] = b;
+            }
+        }
+    }
+}
+
+template <typename PT>
+__global__ void cell_bucket_kernel(int64_t n, int d, const PT *__restrict__ pts, GridParams gp,
+                                   int32_t *__restrict__ bucket) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int c[3] = {0, 0, 0};
+        for (int t = 0; t < d && t < 3; ++t) c[t] = cell_coord(gp, coord(pts, i, d, t), t);
+        bucket[i] = (int32_t)interleave_cell(gp, c[0], c[1], c[2]);
+    }
+}
+
+template <typename PT>
+__global__ void sorted_points_kernel(int64_t n, int d, const PT *__restrict__ pts,
+                                     const int32_t *__restrict__ ent, double4 *__restrict__ sp) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = ent[q];
+        double4 v;
+        v.x = coord(pts, i, d, 0);
+        v.y = d > 1 ? coord(pts, i, d, 1) : 0.0;
+        v.z = d > 2 ? coord(pts, i, d, 2) : 0.0;
+        v.w = 0.0;
+        sp[q] = v;
+    }
+}
+
+template <int KK>
+__global__ void __launch_bounds__(128)
+    knn_grid_query_kernel(int64_t n, int k, const double4 *__restrict__ sp,
+                          const int32_t *__restrict__ ent, const int32_t *__restrict__ off,
+                          GridParams gp, int32_t *__restrict__ out) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int32_t i = ent[q];
+    const double4 pi = sp[q];
+    const double px[3] = {pi.x, pi.y, pi.z};
+    int c[3];
+    for (int t = 0; t < 3; ++t) c[t] = cell_coord(gp, px[t], t);
+    double bd[KK];
+    int32_t bi[KK];
+#pragma unroll
+    for (int a = 0; a < KK; ++a) {
+        bd[a] = DBL_MAX;
+        bi[a] = INT_MAX;
+    }
+    const int kk = k - 1;
+    const int rmax = max(gp.G[0], max(gp.G[1], gp.G[2]));
+    const double margin = gp.h * 1e-7;
+    for (int r = 0;; ++r) {
+        for (int dz = -r; dz <= r; ++dz) {
+            const int z = c[2] + dz;
+            if (z < 0 || z >= gp.G[2]) continue;
+            for (int dy = -r; dy <= r; ++dy) {
+                const int y = c[1] + dy;
+                if (y < 0 || y >= gp.G[1]) continue;
+                const bool full = (dz == -r || dz == r || dy == -r || dy == r);
+                const int step = full ? 1 : (r > 0 ? 2 * r : 1);
+                for (int dx = -r; dx <= r; dx += step) {
+                    const int x = c[0] + dx;
+                    if (x < 0 || x >= gp.G[0]) continue;
+                    const int64_t b = interleave_cell(gp, x, y, z);
+                    const int32_t s1 = off[b + 1];
+                    for (int32_t s = off[b]; s < s1; ++s) {
+                        const int32_t j = ent[s];
+                        if (j == i) continue;
+                        const double4 pj = sp[s];
+                        double dist = 0.0, dv;
+                        dv = __dsub_rn(pi.x, pj.x);
+                        dist = __dadd_rn(dist, __dmul_rn(dv, dv));
+                        if (gp.d > 1) {
+                            dv = __dsub_rn(pi.y, pj.y);
+                            dist = __dadd_rn(dist, __dmul_rn(dv, dv));
+                        }
+                        if (gp.d > 2) {
+                            dv = __dsub_rn(pi.z, pj.z);
+                            dist = __dadd_rn(dist, __dmul_rn(dv, dv));
+                        }
+                        topk_insert<KK>(bd, bi, dist, j);
+                    }
+                }
+            }
+        }
+        if (r >= rmax) break;
+        // distance from the query to the nearest face of the scanned block beyond which
+        // unscanned points may exist
+        double dmin = DBL_MAX;
+        for (int t = 0; t < 3; ++t) {
+            if (c[t] - r > 0) dmin = fmin(dmin, px[t] - (gp.lo[t] + (double)(c[t] - r) * gp.h));
+            if (c[t] + r < gp.G[t] - 1) dmin = fmin(dmin, (gp.lo[t] + (double)(c[t] + r + 1) * gp.h) - px[t]);
+        }
+        if (dmin == DBL_MAX) break;  // the block covers the whole grid
+        dmin -= margin;
+        double worst = DBL_MAX;
+#pragma unroll
+        for (int a = 0; a < KK; ++a)
+            if (a == kk - 1) worst = bd[a];
+        if (dmin > 0.0 && worst < dmin * dmin) break;
+    }
+    int32_t *row = out + (int64_t)i * k;
+    row[0] = i;
+#pragma unroll
+    for (int a = 0; a < KK; ++a)
+        if (a < kk) row[1 + a] = bi[a];
+}
+
+// ------------------------------------------------------------------------ host side
+static int grid_1d(int64_t items, int block = 256) {
+    int64_t g = ceil_div(items, block);
+    const int64_t cap = (int64_t)num_sms() * 16;
+    if (g > cap) g = cap;
+    return (int)std::max<int64_t>(g, 1);
+}
+
+template <typename PT>
+static int knn_brute(int64_t batch, int64_t n, int d, int k, const PT *pts, int32_t *out, cudaStream_t st) {
+    const dim3 grid((unsigned)ceil_div(n, 128), (unsigned)batch);
+    const int kk = k - 1;
+    if (kk <= 4) knn_brute_kernel<PT, 4><<<grid, 128, 0, st>>>(n, d, k, pts, out);
+    else if (kk <= 8) knn_brute_kernel<PT, 8><<<grid, 128, 0, st>>>(n, d, k, pts, out);
+    else if (kk <= 16) knn_brute_kernel<PT, 16><<<grid, 128, 0, st>>>(n, d, k, pts, out);
+    else if (kk <= 32) knn_brute_kernel<PT, 32><<<grid, 128, 0, st>>>(n, d, k, pts, out);
+    else {
+        double *wd = (double *)scratch_alloc(sizeof(double) * batch * n * kk, st);
+        if (!wd) return set_error(FC_ERR_CUDA, "scratch allocation failed (knn)");
+        knn_brute_big_kernel<PT><<<grid, 128, 0, st>>>(n, d, k, pts, wd, out);
+        scratch_free(wd, st);
+    }
+    count_launch();
+    return check_launch("knn_brute");
+}
+
+// Build the cell CSR of one cloud; returns grid params.  off [buckets+1], ent [n].
+template <typename PT>
+static int cell_csr(int64_t n, int d, const PT *pts, GridParams *gp_out, int32_t **off_out,
+                    int32_t **ent_out, int64_t *buckets_out, cudaStream_t st) {
+    double *box_d = (double *)scratch_alloc(6 * sizeof(double), st);
+    bbox_kernel<PT><<<1, 1024, 0, st>>>(n, d, pts, box_d);
+    count_launch();
+    double box[6];
+    cudaMemcpyAsync(box, box_d, sizeof(box), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    scratch_free(box_d, st);
+    if (int rc = check_launch("bbox")) return rc;
+    GridParams gp{};
+    gp.d = d;
+    double ext[3];
+    int deff = 0;
+    double vol = 1.0;
+    for (int t = 0; t < 3; ++t) {
+        ext[t] = t < d ? box[3 + t] - box[t] : 0.0;
+        gp.lo[t] = t < d ? box[t] : 0.0;
+        if (ext[t] > 0) {
+            ++deff;
+            vol *= ext[t];
+        }
+    }
+    const double target_cells = std::max(1.0, (double)n / 2.0);
+    double h = deff > 0 ? std::pow(vol / target_cells, 1.0 / deff) : 1.0;
+    if (!(h > 0) || !std::isfinite(h)) h = 1.0;
+    // clamp per-axis resolution to 1024 cells
+    for (int t = 0; t < 3; ++t)
+        if (ext[t] > 0 && ext[t] / h > 1024.0) h = ext[t] / 1024.0;
+    gp.h = h;
+    int total_bits = 0;
+    for (int t = 0; t < 3; ++t) {
+        gp.G[t] = ext[t] > 0 ? (int)std::min(1024.0, std::floor(ext[t] / h) + 1.0) : 1;
+        int b = 0;
+        while ((1 << b) < gp.G[t]) ++b;
+        gp.bits[t] = b;
+        total_bits += b;
+    }
+    if (total_bits > 30) return set_error(FC_ERR_UNSUPPORTED, "kNN grid too fine (%d bits)", total_bits);
+    const int64_t buckets = (int64_t)1 << total_bits;
+    int32_t *bucket = (int32_t *)scratch_alloc(sizeof(int32_t) * n, st);
+    int32_t *off = (int32_t *)scratch_alloc(sizeof(int32_t) * (buckets + 1), st);
+    int32_t *ent = (int32_t *)scratch_alloc(sizeof(int32_t) * n, st);
+    int32_t *bad = (int32_t *)scratch_alloc(sizeof(int32_t), st);
+    if (!bucket || !off || !ent || !bad) return set_error(FC_ERR_CUDA, "scratch allocation failed (grid)");
+    cudaMemsetAsync(bad, 0, sizeof(int32_t), st);
+    cell_bucket_kernel<PT><<<grid_1d(n), 256, 0, st>>>(n, d, pts, gp, bucket);
+    count_launch();
+    int rc = build_csr(bucket, n, BucketFn{2, buckets, 1}, buckets, off, ent, bad, st);
+    scratch_free(bucket, st);
+    scratch_free(bad, st);
+    if (rc) return rc;
+    *gp_out = gp;
+    *off_out = off;
+    *ent_out = ent;
+    *buckets_out = buckets;
+    return FC_OK;
+}
+
+template <typename PT>
+static int knn_grid(int64_t batch, int64_t n, int d, int k, const PT *pts, int32_t *out, cudaStream_t st) {
+    if (d > 3) return set_error(FC_ERR_UNSUPPORTED, "grid kNN supports d <= 3");
+    const int kk = k - 1;
+    if (kk > 32) return set_error(FC_ERR_UNSUPPORTED, "grid kNN supports k <= 33");
+    for (int64_t b = 0; b < batch; ++b) {
+        const PT *p = pts + b * n * d;
+        int32_t *o = out + b * n * k;
+        GridParams gp;
+        int32_t *off = nullptr, *ent = nullptr;
+        int64_t buckets = 0;
+        if (int rc = cell_csr<PT>(n, d, p, &gp, &off, &ent, &buckets, st)) return rc;
+        double4 *sp = (double4 *)scratch_alloc(sizeof(double4) * n, st);
+        sorted_points_kernel<PT><<<grid_1d(n), 256, 0, st>>>(n, d, p, ent, sp);
+        count_launch();
+        const unsigned g = (unsigned)ceil_div(n, 128);
+        if (kk <= 4) knn_grid_query_kernel<4><<<g, 128, 0, st>>>(n, k, sp, ent, off, gp, o);
+        else if (kk <= 8) knn_grid_query_kernel<8><<<g, 128, 0, st>>>(n, k, sp, ent, off, gp, o);
+        else if (kk <= 16) knn_grid_query_kernel<16><<<g, 128, 0, st>>>(n, k, sp, ent, off, gp, o);
+        else knn_grid_query_kernel<32><<<g, 128, 0, st>>>(n, k, sp, ent, off, gp, o);
+        count_launch();
+        scratch_free(sp, st);
+        scratch_free(off, st);
+        scratch_free(ent, st);
+        if (int rc = check_launch("knn_grid")) return rc;
+    }
+    return FC_OK;
+}
+
+template <typename PT>
+int launch_knn(int64_t batch, int64_t n, int d, int k, const PT *pts, int32_t *out, int algo, cudaStream_t st) {
+    if (algo == FC_KNN_AUTO) algo = (n > 8192 && d <= 3 && k <= 33) ? FC_KNN_GRID : FC_KNN_BRUTE;
+    if (algo == FC_KNN_GRID) return knn_grid<PT>(batch, n, d, k, pts, out, st);
+    return knn_brute<PT>(batch, n, d, k, pts, out, st);
+}
+
+template <typename PT>
+int launch_spatial_order(int64_t n, int d, const PT *pts, int32_t *order, cudaStream_t st) {
+    if (d > 3) return set_error(FC_ERR_UNSUPPORTED, "spatial order supports d <= 3");
+    GridParams gp;
+    int32_t *off = nullptr, *ent = nullptr;
+    int64_t buckets = 0;
+    if (int rc = cell_csr<PT>(n, d, pts, &gp, &off, &ent, &buckets, st)) return rc;
+    cudaMemcpyAsync(order, ent, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st);
+    scratch_free(off, st);
+    scratch_free(ent, st);
+    return check_launch("spatial_order");
+}
+
+template int launch_knn<float>(int64_t, int64_t, int, int, const float *, int32_t *, int, cudaStream_t);
+template int launch_knn<double>(int64_t, int64_t, int, int, const double *, int32_t *, int, cudaStream_t);
+template int launch_spatial_order<float>(int64_t, int, const float *, int32_t *, cudaStream_t);
+template int launch_spatial_order<double>(int64_t, int, const double *, int32_t *, cudaStream_t);
+
+}  // namespace fc

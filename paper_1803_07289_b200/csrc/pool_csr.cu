@@ -1,0 +1,347 @@
+// pool_csr.cu -- flex_pool (neighbourhood max-pool) forward/backward, the reverse-CSR
+// builder (a stable counting sort, no float atomics) and row gather/scatter.
+#include "fc_common.cuh"
+
+namespace fc {
+
+static int grid_1d(int64_t items, int block = 256) {
+    int64_t g = ceil_div(items, block);
+    const int64_t cap = (int64_t)num_sms() * 16;
+    if (g > cap) g = cap;
+    return (int)std::max<int64_t>(g, 1);
+}
+
+// ---------------------------------------------------------------- flex_pool forward
+// out[p,c] = max_s f[j_s, c]; argmax = winning cloud-local index, ties to the lower index
+// (_native.pyx:144-155: start from slot 0, replace on v > best or (v == best and j < bj)).
+template <typename T>
+__global__ void pool_fwd_kernel(int64_t total, int64_t n, int c, int k, const T *__restrict__ feat,
+                                const int32_t *__restrict__ nbr, T *__restrict__ out,
+                                int32_t *__restrict__ argmax) {
+    const int64_t items = total * c;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < items;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = idx / c;
+        const int ch = (int)(idx - p * c);
+        const int64_t base = (p / n) * n;
+        const int32_t *row = nbr + p * k;
+        int32_t bj = row[0];
+        T bv = feat[(base + bj) * c + ch];
+        for (int s = 1; s < k; ++s) {
+            const int32_t j = row[s];
+            const T v = feat[(base + j) * c + ch];
+            if (v > bv || (v == bv && j < bj)) {
+                bv = v;
+                bj = j;
+            }
+        }
+        out[idx] = bv;
+        argmax[idx] = bj;
+    }
+}
+
+// ---------------------------------------------------------------- flex_pool backward
+// Through the reverse neighbourhood: the winner of (i, c) is a neighbour of i, so
+// d_f[j,c] = sum over i in R(j) (ascending, each i once) of [argmax[i,c]==j] g[i,c]:
+// the additions of _native.pyx:165-168 in the same order -> bitwise identical.
+template <typename T>
+__global__ void pool_bwd_kernel(int64_t total, int64_t n, int c, int k, const T *__restrict__ g,
+                                const int32_t *__restrict__ argmax, Csr csr, T *__restrict__ df) {
+    const int64_t items = total * c;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < items;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = idx / c;
+        const int ch = (int)(idx - j * c);
+        const int32_t jl = (int32_t)(j - (j / n) * n);
+        T acc = T(0);
+        int64_t prev = -1;
+        for (int32_t q = csr.off[j]; q < csr.off[j + 1]; ++q) {
+            const int64_t i = (int64_t)csr.ent[q] / k;
+            if (i == prev) continue;  // row i lists j twice: its gradient is routed once
+            prev = i;
+            if (argmax[i * c + ch] == jl) acc = Ar<T>::add(acc, g[i * c + ch]);
+        }
+        df[idx] = acc;
+    }
+}
+
+// Record-only backward (flexops.py:154-165): buckets (row, channel) of the record.
+template <typename T>
+__global__ void pool_bwd_record_kernel(int64_t n_rows, int c, const T *__restrict__ g,
+                                       const int32_t *__restrict__ off,
+                                       const int32_t *__restrict__ ent, T *__restrict__ df) {
+    const int64_t items = n_rows * c;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < items;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        T acc = T(0);
+        for (int32_t q = off[idx]; q < off[idx + 1]; ++q) acc = Ar<T>::add(acc, g[ent[q]]);
+        df[idx] = acc;
+    }
+}
+
+// ---------------------------------------------------------------- counting-sort CSR
+// (bucket functions: BucketFn in fc_common.cuh)
+
+__global__ void csr_count_kernel(const int32_t *__restrict__ keys, int64_t count, BucketFn bf,
+                                 int32_t *__restrict__ counts, int32_t *__restrict__ bad) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t key = keys[e];
+        if (key < 0 || key >= bf.n) {
+            atomicAdd(bad, 1);
+            continue;
+        }
+        atomicAdd(&counts[bf(e, key)], 1);
+    }
+}
+
+__global__ void csr_fill_kernel(const int32_t *__restrict__ keys, int64_t count, BucketFn bf,
+                                int32_t *__restrict__ cursor, int32_t *__restrict__ ent) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t key = keys[e];
+        if (key < 0 || key >= bf.n) continue;
+        const int32_t pos = atomicAdd(&cursor[bf(e, key)], 1);
+        ent[pos] = (int32_t)e;
+    }
+}
+
+// The fill order inside a bucket is arbitrary; sorting each (short) segment makes the
+// result a deterministic, stable counting sort.
+__global__ void csr_sort_segments_kernel(int64_t buckets, const int32_t *__restrict__ off,
+                                         int32_t *__restrict__ ent) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < buckets;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t lo = off[b], hi = off[b + 1];
+        for (int32_t a = lo + 1; a < hi; ++a) {
+            const int32_t v = ent[a];
+            int32_t q = a;
+            while (q > lo && ent[q - 1] > v) {
+                ent[q] = ent[q - 1];
+                --q;
+            }
+            ent[q] = v;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- exclusive scan (int32)
+constexpr int kScanTile = 4096;  // 1024 threads x 4 items
+
+__global__ void __launch_bounds__(1024)
+    scan_block_kernel(const int32_t *__restrict__ in, int32_t *__restrict__ out, int64_t n,
+                      int32_t *__restrict__ block_sums) {
+    __shared__ int32_t warp_tot[32];
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + threadIdx.x * 4;
+    int32_t v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = (base + i < n) ? in[base + i] : 0;
+    const int32_t tsum = v[0] + v[1] + v[2] + v[3];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t inc = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) warp_tot[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int32_t w = warp_tot[lane];
+        int32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        warp_tot[lane] = wi - w;  // exclusive
+        if (lane == 31 && block_sums) block_sums[blockIdx.x] = wi;
+    }
+    __syncthreads();
+    int32_t run = warp_tot[warp] + inc - tsum;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (base + i < n) out[base + i] = run;
+        run += v[i];
+    }
+}
+
+__global__ void scan_add_kernel(int32_t *__restrict__ out, int64_t n, const int32_t *__restrict__ add) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] += add[i / kScanTile];
+}
+
+// out[i] = sum_{q<i} in[q] for i in [0, n).
+static void exclusive_scan(const int32_t *in, int32_t *out, int64_t n, cudaStream_t st) {
+    const int64_t blocks = ceil_div(n, kScanTile);
+    if (blocks <= 1) {
+        scan_block_kernel<<<1, 1024, 0, st>>>(in, out, n, nullptr);
+        count_launch();
+        return;
+    }
+    int32_t *sums = (int32_t *)scratch_alloc(sizeof(int32_t) * blocks * 2, st);
+    int32_t *sums_scan = sums + blocks;
+    scan_block_kernel<<<(unsigned)blocks, 1024, 0, st>>>(in, out, n, sums);
+    count_launch();
+    exclusive_scan(sums, sums_scan, blocks, st);
+    scan_add_kernel<<<grid_1d(n), 256, 0, st>>>(out, n, sums_scan);
+    count_launch();
+    scratch_free(sums, st);
+}
+
+// Generic stable CSR build: offsets [buckets+1], entries [count].  Returns the number
+// of out-of-range keys through *bad_host if non-null (synchronising), else leaves the
+// device counter in *bad_dev.
+int build_csr(const int32_t *keys, int64_t count, BucketFn bf, int64_t buckets, int32_t *off,
+              int32_t *ent, int32_t *bad_dev, cudaStream_t st) {
+    int32_t *counts = (int32_t *)scratch_alloc(sizeof(int32_t) * (buckets + 1) * 2, st);
+    if (!counts) return set_error(FC_ERR_CUDA, "scratch allocation failed (csr)");
+    int32_t *cursor = counts + buckets + 1;
+    cudaMemsetAsync(counts, 0, sizeof(int32_t) * (buckets + 1), st);
+    csr_count_kernel<<<grid_1d(count), 256, 0, st>>>(keys, count, bf, counts, bad_dev);
+    count_launch();
+    exclusive_scan(counts, off, buckets + 1, st);
+    cudaMemcpyAsync(cursor, off, sizeof(int32_t) * (buckets + 1), cudaMemcpyDeviceToDevice, st);
+    csr_fill_kernel<<<grid_1d(count), 256, 0, st>>>(keys, count, bf, cursor, ent);
+    count_launch();
+    csr_sort_segments_kernel<<<grid_1d(buckets), 256, 0, st>>>(buckets, off, ent);
+    count_launch();
+    scratch_free(counts, st);
+    return check_launch("build_csr");
+}
+
+// ---------------------------------------------------------------- rows
+template <typename T>
+__global__ void gather_rows_kernel(int64_t rows_out, int c, const T *__restrict__ in,
+                                   const int32_t *__restrict__ sel, T *__restrict__ out) {
+    const int64_t items = rows_out * c;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < items;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = idx / c;
+        out[idx] = in[(int64_t)sel[r] * c + (idx - r * c)];
+    }
+}
+
+__global__ void scatter_owner_kernel(int64_t rows_in, const int32_t *__restrict__ sel,
+                                     int32_t *__restrict__ owner) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows_in;
+         r += (int64_t)gridDim.x * blockDim.x)
+        atomicMax(&owner[sel[r]], (int32_t)r);
+}
+
+template <typename T>
+__global__ void scatter_rows_kernel(int64_t rows_out, int c, const T *__restrict__ in,
+                                    const int32_t *__restrict__ owner, T *__restrict__ out) {
+    const int64_t items = rows_out * c;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < items;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = idx / c;
+        const int32_t o = owner[r];
+        out[idx] = o >= 0 ? in[(int64_t)o * c + (idx - r * c)] : T(0);
+    }
+}
+
+__global__ void fill_i32_kernel(int32_t *p, int64_t n, int32_t v) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+__global__ void narrow_indices_kernel(const int64_t *__restrict__ in, int32_t *__restrict__ out,
+                                      int64_t count, int64_t hi, int32_t *__restrict__ bad) {
+    int32_t local_bad = 0;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = in[e];
+        if (v < 0 || v >= hi) {
+            ++local_bad;
+            out[e] = 0;
+        } else {
+            out[e] = (int32_t)v;
+        }
+    }
+    if (local_bad) atomicAdd(bad, local_bad);
+}
+
+__global__ void check_indices_kernel(const int32_t *__restrict__ in, int64_t count, int64_t hi,
+                                     int32_t *__restrict__ bad) {
+    int32_t local_bad = 0;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = in[e];
+        if (v < 0 || v >= hi) ++local_bad;
+    }
+    if (local_bad) atomicAdd(bad, local_bad);
+}
+
+// ---------------------------------------------------------------- launchers
+template <typename T>
+int launch_pool_fwd(int64_t total, int64_t n, int c, int k, const T *feat, const int32_t *nbr,
+                    T *out, int32_t *argmax, cudaStream_t st) {
+    pool_fwd_kernel<T><<<grid_1d(total * c), 256, 0, st>>>(total, n, c, k, feat, nbr, out, argmax);
+    count_launch();
+    return check_launch("pool_fwd_kernel");
+}
+template <typename T>
+int launch_pool_bwd(int64_t total, int64_t n, int c, int k, const T *g, const int32_t *argmax,
+                    Csr csr, T *df, cudaStream_t st) {
+    pool_bwd_kernel<T><<<grid_1d(total * c), 256, 0, st>>>(total, n, c, k, g, argmax, csr, df);
+    count_launch();
+    return check_launch("pool_bwd_kernel");
+}
+template <typename T>
+int launch_pool_bwd_record(int64_t n_rows, int c, const T *g, const int32_t *off,
+                           const int32_t *ent, T *df, cudaStream_t st) {
+    pool_bwd_record_kernel<T><<<grid_1d(n_rows * c), 256, 0, st>>>(n_rows, c, g, off, ent, df);
+    count_launch();
+    return check_launch("pool_bwd_record_kernel");
+}
+template <typename T>
+int launch_gather_rows(int64_t rows_out, int c, const T *in, const int32_t *sel, T *out,
+                       cudaStream_t st) {
+    gather_rows_kernel<T><<<grid_1d(rows_out * c), 256, 0, st>>>(rows_out, c, in, sel, out);
+    count_launch();
+    return check_launch("gather_rows_kernel");
+}
+template <typename T>
+int launch_scatter_rows(int64_t rows_in, int64_t rows_out, int c, const T *in, const int32_t *sel,
+                        T *out, cudaStream_t st) {
+    int32_t *owner = (int32_t *)scratch_alloc(sizeof(int32_t) * std::max<int64_t>(rows_out, 1), st);
+    fill_i32_kernel<<<grid_1d(rows_out), 256, 0, st>>>(owner, rows_out, -1);
+    count_launch();
+    scatter_owner_kernel<<<grid_1d(rows_in), 256, 0, st>>>(rows_in, sel, owner);
+    count_launch();
+    scatter_rows_kernel<T><<<grid_1d(rows_out * c), 256, 0, st>>>(rows_out, c, in, owner, out);
+    count_launch();
+    scratch_free(owner, st);
+    return check_launch("scatter_rows");
+}
+
+int launch_narrow_indices(const int64_t *in, int32_t *out, int64_t count, int64_t hi, int32_t *bad,
+                          cudaStream_t st) {
+    narrow_indices_kernel<<<grid_1d(count), 256, 0, st>>>(in, out, count, hi, bad);
+    count_launch();
+    return check_launch("narrow_indices_kernel");
+}
+int launch_check_indices(const int32_t *in, int64_t count, int64_t hi, int32_t *bad, cudaStream_t st) {
+    check_indices_kernel<<<grid_1d(count), 256, 0, st>>>(in, count, hi, bad);
+    count_launch();
+    return check_launch("check_indices_kernel");
+}
+
+#define FC_POOL_INST(T)                                                                          \
+    template int launch_pool_fwd<T>(int64_t, int64_t, int, int, const T *, const int32_t *, T *,  \
+                                    int32_t *, cudaStream_t);                                    \
+    template int launch_pool_bwd<T>(int64_t, int64_t, int, int, const T *, const int32_t *, Csr,  \
+                                    T *, cudaStream_t);                                          \
+    template int launch_pool_bwd_record<T>(int64_t, int, const T *, const int32_t *,             \
+                                           const int32_t *, T *, cudaStream_t);                  \
+    template int launch_gather_rows<T>(int64_t, int, const T *, const int32_t *, T *,            \
+                                       cudaStream_t);                                            \
+    template int launch_scatter_rows<T>(int64_t, int64_t, int, const T *, const int32_t *, T *,  \
+                                        cudaStream_t);
+FC_POOL_INST(float)
+FC_POOL_INST(double)
+
+}  // namespace fc
