@@ -55,10 +55,12 @@ enum { FC_F32 = 0, FC_F64 = 1 };
 
 /* Contraction engine for FC_F32 (ignored for FC_F64, which is always SIMT fp64). */
 enum {
-    FC_MODE_AUTO = 0,      /* tensor-core 3xTF32 where the shape is covered, else SIMT */
-    FC_MODE_SIMT = 1,      /* CUDA-core fp32 FMA                                       */
-    FC_MODE_TC_TF32X3 = 2, /* tcgen05 kind::tf32, 3-pass hi/lo split, fp32 accumulate  */
-    FC_MODE_TC_BF16 = 3    /* tcgen05 kind::f16 bf16 operands, fp32 accumulate (1e-2)  */
+    FC_MODE_AUTO = 0,     /* tensor-core split engine where the shape is covered, else SIMT */
+    FC_MODE_SIMT = 1,     /* CUDA-core fp32 FMA                                             */
+    FC_MODE_TC_SPLIT = 2, /* tcgen05 kind::f16: each fp32 operand split into fp16 hi + lo    */
+                          /* with power-of-two scaling, 3 MMAs (hi*hi + hi*lo + lo*hi),      */
+                          /* fp32 accumulate -- fp32-level accuracy (1e-4 rel / 1e-5 abs)    */
+    FC_MODE_TC_BF16 = 3   /* tcgen05 kind::f16, bf16 operands, 1 MMA, fp32 accumulate (1e-2) */
 };
 
 /* kNN algorithm selector. */

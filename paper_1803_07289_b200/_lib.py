@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libflexconv_b200.so")
 
 FC_F32, FC_F64 = 0, 1
-MODE_AUTO, MODE_SIMT, MODE_TC_TF32X3, MODE_TC_BF16 = 0, 1, 2, 3
+MODE_AUTO, MODE_SIMT, MODE_TC_SPLIT, MODE_TC_BF16 = 0, 1, 2, 3
 KNN_AUTO, KNN_BRUTE, KNN_GRID = 0, 1, 2
 
 _STATUS = {

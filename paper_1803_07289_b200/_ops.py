@@ -16,7 +16,7 @@ import torch
 from . import _lib
 from .errors import ShapeMismatchError, UnsupportedError
 
-MODES = {"auto": _lib.MODE_AUTO, "simt": _lib.MODE_SIMT, "tf32x3": _lib.MODE_TC_TF32X3,
+MODES = {"auto": _lib.MODE_AUTO, "simt": _lib.MODE_SIMT, "split": _lib.MODE_TC_SPLIT,
          "bf16": _lib.MODE_TC_BF16}
 
 

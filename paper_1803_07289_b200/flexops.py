@@ -6,7 +6,7 @@ Inputs may be numpy arrays (the reference's types) or torch tensors:
     float to float64, flexops.py:30-31,70-74); the fp64 engine follows the reference's
     operation order, so forward and pooling results are bitwise identical to _native.
   * torch in -> torch out on the same device, computed in the tensor's dtype
-    (float32 selects the fp32 engines: `mode` = "auto" | "simt" | "tf32x3" | "bf16").
+    (float32 selects the fp32 engines: `mode` = "auto" | "simt" | "split" | "bf16").
 There is no CPU implementation: the arithmetic always runs in libflexconv_b200.so.
 """
 

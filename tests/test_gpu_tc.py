@@ -1,0 +1,120 @@
+"""GPU: the tcgen05 tensor-core engines against the oracle.
+
+  * split engine (fp16 hi/lo, 3 MMAs): the north_star fp32 tolerance, elementwise
+    allclose(rtol=1e-4, atol=1e-5) for forward / flex_deconv / d_features;
+  * bf16 engine: the stated 1e-2 relative tolerance, norm-wise ||D||/||ref|| <= 1e-2 and
+    max|D| <= 1e-2 * max|ref|.
+Plus size-independent properties at N = 1M (adjoint identity, determinism) where the
+oracle would take minutes.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _layer(n, cin, cout, k, seed=21):
+    import torch
+
+    from paper_1803_07289_b200 import _ops
+    from paper_1803_07289_b200.core import synthetic_layer
+
+    loc, feat, th, tb, up = synthetic_layer(seed, 0, n, 3, cin, cout)
+    dev = torch.device("cuda")
+    t = {name: torch.from_numpy(v).to(dev, torch.float32) for name, v in
+         dict(loc=loc, feat=feat, th=th, tb=tb, up=up).items()}
+    t["nbr"] = _ops.knn(t["loc"], 1, n, k)
+    t["csr"] = _ops.csr_build(t["nbr"], 1, n)
+    host = dict(loc=loc, feat=feat, th=th, tb=tb, up=up, nbr=t["nbr"].cpu().numpy().astype(np.int64))
+    return t, host
+
+
+def _close_bf16(got, ref, name):
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert err <= 1e-2, (name, err)
+    assert np.abs(got - ref).max() <= 1e-2 * np.abs(ref).max(), name
+
+
+@pytest.mark.parametrize("cin,cout", [(64, 64), (32, 32), (64, 32), (32, 64), (32, 128)])
+@pytest.mark.parametrize("mode", ["split", "bf16"])
+def test_tc_forward_vs_oracle(fc, oracle_mod, cin, cout, mode):
+    from paper_1803_07289_b200 import _ops
+
+    n, k = 20000, 8
+    t, h = _layer(n, cin, cout, k)
+    out = _ops.conv_forward(t["feat"], t["loc"], t["nbr"], t["th"], t["tb"], 1, n, mode).cpu().numpy()
+    ref = oracle_mod.conv_forward(h["feat"], h["loc"], h["nbr"], h["th"], h["tb"])
+    if mode == "split":
+        np.testing.assert_allclose(out, ref, rtol=1e-4, atol=1e-5)
+    else:
+        _close_bf16(out, ref, f"fwd {cin}->{cout}")
+
+
+@pytest.mark.parametrize("cin,cout", [(64, 64), (32, 32), (64, 32)])
+@pytest.mark.parametrize("mode", ["split", "bf16"])
+def test_tc_deconv_and_dfeatures_vs_oracle(fc, oracle_mod, cin, cout, mode):
+    from paper_1803_07289_b200 import _ops
+
+    n, k = 20000, 8
+    t, h = _layer(n, cin, cout, k, seed=22)
+    y = _ops.deconv_forward(t["up"], t["loc"], t["csr"], t["th"], t["tb"], 1, n, k, mode).cpu().numpy()
+    ref = oracle_mod.deconv_forward(h["up"], h["loc"], h["nbr"], h["th"], h["tb"])
+    if mode == "split":
+        np.testing.assert_allclose(y, ref, rtol=1e-4, atol=1e-5)
+    else:
+        _close_bf16(y, ref, "deconv")
+    df, _, _, _ = _ops.conv_backward(t["up"], t["feat"], t["loc"], t["nbr"], t["csr"], t["th"], t["tb"], 1, n,
+                                     need=(True, False, False, False), mode=mode)
+    if mode == "split":
+        np.testing.assert_allclose(df.cpu().numpy(), ref, rtol=1e-4, atol=1e-5)
+
+
+def test_tc_partial_tile_and_batch(fc, oracle_mod):
+    """B=3 clouds of 1000 points (tiles straddle clouds, last tile partial)."""
+    import torch
+
+    from paper_1803_07289_b200 import _ops
+    from paper_1803_07289_b200.core import synthetic_layer
+
+    B, n, k, c = 3, 1000, 8, 64
+    parts = [synthetic_layer(30 + b, 0, n, 3, c, c) for b in range(B)]
+    dev = torch.device("cuda")
+    loc = torch.from_numpy(np.concatenate([p[0] for p in parts])).to(dev, torch.float32)
+    feat = torch.from_numpy(np.concatenate([p[1] for p in parts])).to(dev, torch.float32)
+    th = torch.from_numpy(parts[0][2]).to(dev, torch.float32)
+    tb = torch.from_numpy(parts[0][3]).to(dev, torch.float32)
+    nbr = _ops.knn(loc, B, n, k)
+    out = _ops.conv_forward(feat, loc, nbr, th, tb, B, n, "split").cpu().numpy()
+    nb = nbr.cpu().numpy().astype(np.int64)
+    for b in range(B):
+        ref = oracle_mod.conv_forward(parts[b][1], parts[b][0], nb[b * n:(b + 1) * n], parts[0][2], parts[0][3])
+        np.testing.assert_allclose(out[b * n:(b + 1) * n], ref, rtol=1e-4, atol=1e-5)
+
+
+def test_tc_forward_deterministic_and_matches_simt_at_1M(fc):
+    import torch
+
+    from paper_1803_07289_b200 import _ops
+
+    n, k = 1 << 20, 8
+    t, _ = _layer(n, 64, 64, k, seed=23)
+    a = _ops.conv_forward(t["feat"], t["loc"], t["nbr"], t["th"], t["tb"], 1, n, "split")
+    b = _ops.conv_forward(t["feat"], t["loc"], t["nbr"], t["th"], t["tb"], 1, n, "split")
+    assert torch.equal(a, b)
+    s = _ops.conv_forward(t["feat"], t["loc"], t["nbr"], t["th"], t["tb"], 1, n, "simt")
+    torch.testing.assert_close(a, s, rtol=1e-4, atol=1e-5)
+
+
+def test_tc_adjoint_identity_at_1M(fc):
+    """<A f, x> == <f, A^T x> for the split engine on a 1M-point cloud (fp64 dot products)."""
+    from paper_1803_07289_b200 import _ops
+
+    n, k = 1 << 20, 8
+    t, _ = _layer(n, 64, 64, k, seed=24)
+    af = _ops.conv_forward(t["feat"], t["loc"], t["nbr"], t["th"], t["tb"], 1, n, "split").double()
+    atx = _ops.deconv_forward(t["up"], t["loc"], t["csr"], t["th"], t["tb"], 1, n, k, "split").double()
+    lhs = float((af * t["up"].double()).sum())
+    rhs = float((t["feat"].double() * atx).sum())
+    scale = float(af.abs().sum() * t["up"].double().abs().max())
+    assert abs(lhs - rhs) <= 1e-6 * scale, (lhs, rhs, scale)
