@@ -426,6 +426,16 @@ int launch_dtheta(int64_t total, int64_t n, int d, int cin, int k, int cout, con
     FC_DP_SWITCH(d, (launch_dtheta_dp<T, DPC>(total, n, cin, k, cout, feat, loc, nbr, g, d_theta, d_theta_b, st)));
 }
 
+template <typename T>
+int launch_dtheta_reduce(int chunks, int cin, int d, int cout, const T *partial, T *d_theta, T *d_theta_b,
+                         cudaStream_t st) {
+    const int64_t E = (int64_t)cout * cin * (d + 1);
+    dtheta_reduce_kernel<T><<<grid_for(E, 256), 256, 0, st>>>(chunks, cin, d, cout, partial, d_theta, d_theta_b);
+    count_launch();
+    return check_launch("dtheta_reduce_kernel");
+}
+template int launch_dtheta_reduce<float>(int, int, int, int, const float *, float *, float *, cudaStream_t);
+
 #define FC_INST(T)                                                                                   \
     template void launch_pack<T>(int, int, int, const T *, const T *, T *, T *, cudaStream_t);      \
     template int launch_gmc<T>(bool, int64_t, int64_t, int, int, int, int, const T *, const T *,    \

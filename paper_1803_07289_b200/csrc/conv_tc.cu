@@ -49,6 +49,10 @@ struct TcArgs {
     const float *binv;    // 1 / (B scale)
     float *out;
     int64_t num_tiles;
+    // REVERSE + DLOC only: location gradient d_loc[j] = centre[j] - sum_c f[j,c] U_j[c,:]
+    const float *feat;    // [total, NOUT] conv input features
+    const float *centre;  // [total, 3] centre-role term (tc_dtheta kernel)
+    float *dloc;          // [total, 3]
 };
 
 template <bool SPLIT>
@@ -75,7 +79,7 @@ __device__ __forceinline__ float split_scale(float m, float &inv) {
     return ldexpf(1.f, 14 - e);
 }
 
-template <int GC, int NOUT, bool SPLIT>
+template <int GC, int NOUT, bool SPLIT, bool DLOC = false>
 struct TcLayout {
     static constexpr int KT = 4 * GC;                      // K = (Dp + 1) * GC, Dp = 3
     static constexpr int A_BYTES = kTcM * KT * 2;          // one 16-bit A image
@@ -86,7 +90,9 @@ struct TcLayout {
     static constexpr int RS_OFF = B_OFF + B_BYTES * NSPLIT;  // float rs[2][128]
     static constexpr int BAR_OFF = RS_OFF + 2 * kTcM * 4;    // 5 x uint64 + tmem holder
     static constexpr int SMEM = BAR_OFF + 64 + 1024;         // + alignment slack
-    static constexpr int TMEM_COLS = (2 * NOUT <= 32) ? 32 : (2 * NOUT <= 64) ? 64 : (2 * NOUT <= 128) ? 128 : 256;
+    // per accumulator buffer: D (NOUT columns) [+ U_0..U_2 (3 x NOUT) for DLOC]; 2 buffers
+    static constexpr int CPB = NOUT * (DLOC ? 4 : 1);
+    static constexpr int TMEM_COLS = (2 * CPB <= 32) ? 32 : (2 * CPB <= 64) ? 64 : (2 * CPB <= 128) ? 128 : (2 * CPB <= 256) ? 256 : 512;
 };
 
 // ---------------------------------------------------------------------------------
@@ -245,9 +251,10 @@ struct Idx {
 };
 
 // ---------------------------------------------------------------------------------
-template <int GC, int NOUT, bool SPLIT, bool REVERSE, int KFIX>
+template <int GC, int NOUT, bool SPLIT, bool REVERSE, int KFIX, bool DLOC = false>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_gmc_kernel(TcArgs a) {
-    using L = TcLayout<GC, NOUT, SPLIT>;
+    static_assert(!DLOC || REVERSE, "the location-gradient epilogue belongs to the reverse pass");
+    using L = TcLayout<GC, NOUT, SPLIT, DLOC>;
     using G = Geo<GC>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -297,15 +304,33 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gmc_kernel(TcArgs a) {
             mbar_wait(full, i & 1);
             if (i >= 2) mbar_wait(d_free + (i & 1), ((i >> 1) + 1) & 1);
             tc_fence_after();
-            const uint32_t d_tmem = tmem_base + (uint32_t)((i & 1) * NOUT);
+            const uint32_t d_tmem = tmem_base + (uint32_t)((i & 1) * L::CPB);
+            // byte offset of 16-bit element k of a K-major SW128 operand with `rows` rows
+            auto koff = [](int k, int rows) { return (uint32_t)((k >> 6) * rows * 128 + (k & 63) * 2); };
 #pragma unroll
             for (int s = 0; s < L::KT / 16; ++s) {
-                const uint32_t aoff = (uint32_t)((s >> 2) * kTcM * 128 + (s & 3) * 32);
-                const uint32_t boff = (uint32_t)((s >> 2) * NOUT * 128 + (s & 3) * 32);
+                const uint32_t aoff = koff(16 * s, kTcM), boff = koff(16 * s, NOUT);
                 mma_f16(d_tmem, desc_sw128(a_hi + aoff), desc_sw128(b_hi + boff), idesc, s > 0 ? 1u : 0u);
                 if (SPLIT) {
                     mma_f16(d_tmem, desc_sw128(a_hi + aoff), desc_sw128(b_lo + boff), idesc, 1u);
                     mma_f16(d_tmem, desc_sw128(a_lo + aoff), desc_sw128(b_hi + boff), idesc, 1u);
+                }
+            }
+            if constexpr (DLOC) {
+                // U_t[p, c] = sum_c' Yb[p, c'] theta[c', c, t]: A = the bias-moment block
+                // (k in [3GC, 4GC)), B = K-block t of the resident adjoint image B_rev.
+#pragma unroll
+                for (int t = 0; t < 3; ++t) {
+                    const uint32_t u_tmem = d_tmem + (uint32_t)(NOUT * (1 + t));
+#pragma unroll
+                    for (int s = 0; s < GC / 16; ++s) {
+                        const uint32_t aoff = koff(3 * GC + 16 * s, kTcM), boff = koff(t * GC + 16 * s, NOUT);
+                        mma_f16(u_tmem, desc_sw128(a_hi + aoff), desc_sw128(b_hi + boff), idesc, s > 0 ? 1u : 0u);
+                        if (SPLIT) {
+                            mma_f16(u_tmem, desc_sw128(a_hi + aoff), desc_sw128(b_lo + boff), idesc, 1u);
+                            mma_f16(u_tmem, desc_sw128(a_lo + aoff), desc_sw128(b_hi + boff), idesc, 1u);
+                        }
+                    }
                 }
             }
             mma_commit(mma_done + (i & 1));
@@ -320,18 +345,52 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gmc_kernel(TcArgs a) {
         mbar_wait(mma_done + (i & 1), (i >> 1) & 1);
         tc_fence_after();
         const int64_t p = tile * kTcM + row;
+        const bool pv = p < a.total;
         const float inv = rs[(i & 1) * kTcM + row];
         float *orow = a.out + p * NOUT;
+        const uint32_t tbase = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)((i & 1) * L::CPB);
+        float nb0 = 0.f, nb1 = 0.f, nb2 = 0.f;
 #pragma unroll
         for (int c0 = 0; c0 < NOUT; c0 += 16) {
             float v[16];
-            tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)((i & 1) * NOUT + c0), v);
-            if (p < a.total) {
+            tmem_ld16(tbase + (uint32_t)c0, v);
+            if (pv) {
 #pragma unroll
                 for (int q = 0; q < 16; q += 4) {
                     float4 w = make_float4(v[q] * inv, v[q + 1] * inv, v[q + 2] * inv, v[q + 3] * inv);
                     *reinterpret_cast<float4 *>(orow + c0 + q) = w;
                 }
+            }
+            if constexpr (DLOC) {
+                // neighbour role: -sum_c f[p, c] U_t[p, c] (the -dt terms of _native.pyx:121-127)
+                float f[16];
+                if (pv) {
+#pragma unroll
+                    for (int q = 0; q < 16; q += 4) {
+                        const float4 x = __ldg(reinterpret_cast<const float4 *>(a.feat + p * NOUT + c0 + q));
+                        f[q] = x.x, f[q + 1] = x.y, f[q + 2] = x.z, f[q + 3] = x.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) f[q] = 0.f;
+                }
+                float u[16];
+                tmem_ld16(tbase + (uint32_t)(NOUT + c0), u);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) nb0 = fmaf(f[q], u[q], nb0);
+                tmem_ld16(tbase + (uint32_t)(2 * NOUT + c0), u);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) nb1 = fmaf(f[q], u[q], nb1);
+                tmem_ld16(tbase + (uint32_t)(3 * NOUT + c0), u);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) nb2 = fmaf(f[q], u[q], nb2);
+            }
+        }
+        if constexpr (DLOC) {
+            if (pv) {
+                a.dloc[p * 3 + 0] = a.centre[p * 3 + 0] - nb0 * inv;
+                a.dloc[p * 3 + 1] = a.centre[p * 3 + 1] - nb1 * inv;
+                a.dloc[p * 3 + 2] = a.centre[p * 3 + 2] - nb2 * inv;
             }
         }
         tc_fence_before();
@@ -529,12 +588,376 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gmc_kernel(TcArgs a) {
     }
 }
 
+// =================================================================================
+// Backward, forward-gather half: d_theta / d_theta_b and the centre role of d_locations.
+//
+//   D[k, c'] = sum_p X_p[k] g_p[c']            (d_theta, k = t*64 + c;  _native.pyx:106-112)
+//   Z_t[p, c'] = sum_c X_p[3, c] theta[c', c, t],  centre[p, t] = sum_c' g_p[c'] Z_t[p, c']
+//                                               (the +dt terms of _native.pyx:121-127)
+// d_theta reduces over POINTS, so it is fed point-chunk by point-chunk (16 points) through a
+// 2-stage shared-memory ring as kind::tf32 MMAs with M = k (two halves of 128), N = c', K =
+// points, both operands MN-major; tf32 hi/lo split (3 MMAs) keeps fp32 accuracy with no
+// scaling, so the accumulator stays in TMEM across all tiles of the CTA (deterministic per
+// CTA); the per-CTA partials are then reduced in fixed order (dtheta_reduce_kernel).
+// Z is an fp16-split M = 128 (points) GEMM on the bias moments, B = K-blocks 0..2 of the
+// forward image.  GC = c_in = 64 and CO = c_out = 64 (the headline shape).
+// =================================================================================
+constexpr int kDtChunk = 16;  // points per d_theta chunk (2 tf32 k-steps)
+
+struct DtArgs {
+    int64_t total, n;
+    int k;
+    const float *feat, *loc, *g;
+    const int32_t *nbr;
+    const uint8_t *bimg;  // forward fp16 image (hi, lo); K-blocks 0..2 used
+    const float *binv;
+    float *partial;       // [gridDim.x][CO * 4 * GC], layout (c', c, t) like dtheta_partial_kernel
+    float *centre;        // [total, 3]
+    int64_t num_tiles;
+};
+
+struct DtLayout {
+    static constexpr int GC = 64, CO = 64;
+    static constexpr int XST = kDtChunk * 4 * GC * 4;   // one tf32 X chunk image (16 KB)
+    static constexpr int GST = kDtChunk * CO * 4;       // one tf32 G chunk image (4 KB)
+    static constexpr int XB = kTcM * GC * 2;            // fp16 bias-moment tile (16 KB)
+    static constexpr int BZ = CO * 128;                 // one K-block of the forward image (8 KB)
+    static constexpr int X_OFF = 0;                     // [stage][hi, lo]
+    static constexpr int G_OFF = X_OFF + 2 * 2 * XST;   // [stage][hi, lo]
+    static constexpr int XB_OFF = G_OFF + 2 * 2 * GST;  // [buf][hi, lo]
+    static constexpr int B_OFF = XB_OFF + 2 * 2 * XB;   // [hi K-blocks 0..2][lo K-blocks 0..2]
+    static constexpr int RS_OFF = B_OFF + 2 * 3 * BZ;   // float rs[2][128]
+    static constexpr int BAR_OFF = RS_OFF + 2 * kTcM * 4;
+    static constexpr int SMEM = BAR_OFF + 128 + 1024;
+    static constexpr int TMEM_COLS = 512;               // D: 2 x 64, Z: 2 x 192
+};
+
+__device__ __forceinline__ uint32_t f32_to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+// tf32 hi / lo of 4 values -> 16-byte stores at hi_addr and lo_addr
+__device__ __forceinline__ void store_tf32x4(uint32_t hi_addr, uint32_t lo_addr, float2 a, float2 b) {
+    const uint32_t h0 = f32_to_tf32(a.x), h1 = f32_to_tf32(a.y), h2 = f32_to_tf32(b.x), h3 = f32_to_tf32(b.y);
+    sts128(hi_addr, h0, h1, h2, h3);
+    sts128(lo_addr, __float_as_uint(a.x - __uint_as_float(h0)), __float_as_uint(a.y - __uint_as_float(h1)),
+           __float_as_uint(b.x - __uint_as_float(h2)), __float_as_uint(b.y - __uint_as_float(h3)));
+}
+
+// MN-major tf32 operand descriptor.  The only MN-major smem layout the hardware takes for
+// 32-bit elements is SWIZZLE_128B_BASE32B: atoms of 4 K-rows x 128 B (32 elements along
+// MN), the 32-byte chunk index XOR-ed with (row % 4).  MN blocks of 128 B are LBO apart,
+// 4-row K groups SBO apart.
+__device__ __forceinline__ uint64_t desc_sw128b32_mn(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B
+    return d;
+}
+// byte offset of 4 consecutive MN elements starting at mn (multiple of 4) in K-row r of an
+// SW128_BASE32B MN-major chunk image with 16 K-rows per MN block
+__device__ __forceinline__ uint32_t mn32_off(int mn, int r) {
+    const int blk = mn >> 5, in = mn & 31;
+    return (uint32_t)(blk * 2048 + (r >> 2) * 512 + (r & 3) * 128 + ((((in >> 3) ^ (r & 3))) << 5) + (in & 7) * 4);
+}
+__host__ __device__ constexpr uint32_t idesc_tf32_mn(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+        "}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+template <int KFIX>
+__global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
+    using L = DtLayout;
+    constexpr int GC = L::GC, CO = L::CO;
+    using G = Geo<GC>;  // 16 lanes per point, 2 points per group
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t s_base = smem_u32(smem);
+    float *rs = reinterpret_cast<float *>(smem + L::RS_OFF);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + L::BAR_OFF);
+    uint64_t *chunk_full = bar + 0;   // [2] count 8 warps
+    uint64_t *chunk_empty = bar + 2;  // [2] tcgen05.commit
+    uint64_t *z_done = bar + 4;       // [2] tcgen05.commit
+    uint64_t *z_free = bar + 6;       // [2] count 4 epilogue warps
+    uint64_t *dt_done = bar + 8;      // tcgen05.commit
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bar + 9);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 2; ++q) {
+            mbar_init(chunk_full + q, 8);
+            mbar_init(chunk_empty + q, 1);
+            mbar_init(z_done + q, 1);
+            mbar_init(z_free + q, kEpiWarps);
+        }
+        mbar_init(dt_done, 1);
+        fence_mbar_init();
+    }
+    if (warp == kMmaWarp) tmem_alloc(tmem_holder, L::TMEM_COLS);
+    {  // K-blocks 0..2 of the forward image (hi, then lo) -> resident B for Z
+        const int img_b = CO * 4 * GC * 2;  // bytes of one full forward image
+        for (int h = 0; h < 2; ++h) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(a.bimg + h * img_b);
+            uint4 *dst = reinterpret_cast<uint4 *>(smem + L::B_OFF + h * 3 * L::BZ);
+            for (int i = threadIdx.x; i < 3 * L::BZ / 16; i += blockDim.x) dst[i] = src[i];
+        }
+    }
+    const float binv = a.binv[0];
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+    const int64_t tiles_mine = a.num_tiles > blockIdx.x ? ceil_div(a.num_tiles - blockIdx.x, gridDim.x) : 0;
+
+    // ---------------------------------------------------------------- MMA issue (warp 15, lane 0)
+    int mma_chunk = 0;  // next chunk (in this CTA's order) whose MMAs are to be issued
+    auto issue_chunk = [&](int64_t u_global) {
+        // u_global = tile_local * 8 + c
+        const int c = (int)(u_global & 7);
+        const int st = c & 1;
+        const int64_t u = u_global >> 1;  // completion index of stage st
+        if (lane == 0) {
+            mbar_wait(chunk_full + st, (uint32_t)(u & 1));
+            tc_fence_after();
+            constexpr uint32_t idesc = idesc_tf32_mn(kTcM, CO);
+            const uint32_t xh = s_base + L::X_OFF + st * 2 * L::XST, xl = xh + L::XST;
+            const uint32_t gh = s_base + L::G_OFF + st * 2 * L::GST, gl = gh + L::GST;
+#pragma unroll
+            for (int mh = 0; mh < 2; ++mh) {
+#pragma unroll
+                for (int ks = 0; ks < kDtChunk / 8; ++ks) {
+                    const uint32_t ao = (uint32_t)(mh * 4 * 2048 + ks * 1024), bo = (uint32_t)(ks * 1024);
+                    const uint32_t first = (u_global == 0 && ks == 0) ? 0u : 1u;
+                    const uint32_t d = tmem_base + (uint32_t)(mh * CO);
+                    mma_tf32(d, desc_sw128b32_mn(xh + ao, 2048, 512), desc_sw128b32_mn(gh + bo, 2048, 512), idesc, first);
+                    mma_tf32(d, desc_sw128b32_mn(xh + ao, 2048, 512), desc_sw128b32_mn(gl + bo, 2048, 512), idesc, 1u);
+                    mma_tf32(d, desc_sw128b32_mn(xl + ao, 2048, 512), desc_sw128b32_mn(gh + bo, 2048, 512), idesc, 1u);
+                }
+            }
+            mma_commit(chunk_empty + st);
+        }
+        __syncwarp();
+    };
+    auto issue_z = [&](int i) {
+        if (lane == 0) {
+            if (i >= 2) mbar_wait(z_free + (i & 1), ((i >> 1) + 1) & 1);
+            tc_fence_after();
+            constexpr uint32_t idesc = idesc_f16(kTcM, CO, 0);
+            const uint32_t ah = s_base + L::XB_OFF + (i & 1) * 2 * L::XB, al = ah + L::XB;
+            const uint32_t bh = s_base + L::B_OFF, bl = bh + 3 * L::BZ;
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const uint32_t z = tmem_base + 2 * CO + (uint32_t)((i & 1) * 3 * CO + t * CO);
+#pragma unroll
+                for (int s = 0; s < GC / 16; ++s) {
+                    const uint32_t ao = (uint32_t)(s * 32), bo = (uint32_t)(t * L::BZ + s * 32);
+                    mma_f16(z, desc_sw128(ah + ao), desc_sw128(bh + bo), idesc, s > 0 ? 1u : 0u);
+                    mma_f16(z, desc_sw128(ah + ao), desc_sw128(bl + bo), idesc, 1u);
+                    mma_f16(z, desc_sw128(al + ao), desc_sw128(bh + bo), idesc, 1u);
+                }
+            }
+            mma_commit(z_done + (i & 1));
+        }
+        __syncwarp();
+    };
+    // ---------------------------------------------------------------- Z epilogue (warps 0..3)
+    auto epilogue_z = [&](int i) {
+        const int64_t tile = blockIdx.x + (int64_t)i * gridDim.x;
+        const int row = warp * 32 + lane;
+        const int64_t p = tile * kTcM + row;
+        mbar_wait(z_done + (i & 1), (i >> 1) & 1);
+        tc_fence_after();
+        const float inv = rs[(i & 1) * kTcM + row];
+        const uint32_t tb = tmem_base + ((uint32_t)(warp * 32) << 16) + 2 * CO + (uint32_t)((i & 1) * 3 * CO);
+        float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+#pragma unroll
+        for (int q0 = 0; q0 < CO; q0 += 16) {
+            float gv[16];
+            if (p < a.total) {
+#pragma unroll
+                for (int q = 0; q < 16; q += 4) {
+                    const float4 x = __ldg(reinterpret_cast<const float4 *>(a.g + p * CO + q0 + q));
+                    gv[q] = x.x, gv[q + 1] = x.y, gv[q + 2] = x.z, gv[q + 3] = x.w;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) gv[q] = 0.f;
+            }
+            float z[16];
+            tmem_ld16(tb + (uint32_t)q0, z);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) c0 = fmaf(gv[q], z[q], c0);
+            tmem_ld16(tb + (uint32_t)(CO + q0), z);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) c1 = fmaf(gv[q], z[q], c1);
+            tmem_ld16(tb + (uint32_t)(2 * CO + q0), z);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) c2 = fmaf(gv[q], z[q], c2);
+        }
+        if (p < a.total) {
+            a.centre[p * 3 + 0] = c0 * inv;
+            a.centre[p * 3 + 1] = c1 * inv;
+            a.centre[p * 3 + 2] = c2 * inv;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(z_free + (i & 1));
+    };
+
+    // ---------------------------------------------------------------- gather producers
+    // warp w: parity q = w / 8 fills stage q of the chunks c = q, q+2, q+4, q+6 of each tile,
+    // group r = w % 8 (points 2r, 2r+1 of the chunk).
+    {
+        const int q = warp >> 3, r = warp & 7;
+        const int pt = lane / G::LPR, cl = lane % G::LPR;
+        const int ipt = lane >> 3, slot = lane & 7;
+        for (int64_t tl = 0; tl < tiles_mine; ++tl) {
+            const int i = (int)tl;
+            const int64_t tile = blockIdx.x + tl * gridDim.x;
+            for (int c = q; c < 8; c += 2) {
+                const int64_t u = tl * 4 + (c >> 1);  // this stage's use count
+                const int64_t p0 = tile * kTcM + c * kDtChunk + 2 * r;
+                // ---- moments of points p0, p0+1 (lane group pt)
+                Mom acc;
+                mom_zero(acc);
+                const int64_t myp = p0 + ipt;
+                const bool pv = ipt < 2 && myp < a.total;
+                const int cnt = KFIX ? KFIX : a.k;
+                for (int b0 = 0; b0 < cnt; b0 += kSlots) {
+                    int32_t j = 0;
+                    float o0 = 0.f, o1 = 0.f, o2 = 0.f;
+                    if (pv && b0 + slot < cnt) {
+                        const int32_t base = myp < a.n ? 0 : (int32_t)((myp / a.n) * a.n);
+                        j = base + __ldg(a.nbr + myp * cnt + b0 + slot);
+                        o0 = __ldg(a.loc + myp * 3 + 0) - __ldg(a.loc + (int64_t)j * 3 + 0);
+                        o1 = __ldg(a.loc + myp * 3 + 1) - __ldg(a.loc + (int64_t)j * 3 + 1);
+                        o2 = __ldg(a.loc + myp * 3 + 2) - __ldg(a.loc + (int64_t)j * 3 + 2);
+                    }
+                    float4 v[kSlots];
+#pragma unroll
+                    for (int s = 0; s < kSlots; ++s) {
+                        const int32_t jj = __shfl_sync(0xffffffffu, j, pt * 8 + s);
+                        v[s] = (b0 + s < cnt) ? __ldg(reinterpret_cast<const float4 *>(a.feat + (int64_t)jj * GC) + cl)
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int s = 0; s < kSlots; ++s) {
+                        const float w0 = __shfl_sync(0xffffffffu, o0, pt * 8 + s);
+                        const float w1 = __shfl_sync(0xffffffffu, o1, pt * 8 + s);
+                        const float w2 = __shfl_sync(0xffffffffu, o2, pt * 8 + s);
+                        if (b0 + s < cnt) mom_add(acc, v[s], w0, w1, w2);
+                    }
+                }
+                const int64_t pme = p0 + pt;
+                const bool valid = pme < a.total;
+                if (!valid) mom_zero(acc);
+                float4 gv = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (valid) gv = __ldg(reinterpret_cast<const float4 *>(a.g + pme * CO) + cl);
+                // ---- wait for the ring stage (and, at a tile's first chunk, the Xb/rs buffer)
+                if (u >= 1) mbar_wait(chunk_empty + q, (uint32_t)((u - 1) & 1));
+                if (c == q && i >= 2) mbar_wait(z_free + (i & 1), ((i >> 1) + 1) & 1);
+                // X chunk row (tf32 hi/lo, MN-major): row rr = 2r + pt of the chunk
+                const int rr = 2 * r + pt;
+                const uint32_t xh = s_base + L::X_OFF + q * 2 * L::XST, xl = xh + L::XST;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const uint32_t off = mn32_off(t * GC + 4 * cl, rr);
+                    store_tf32x4(xh + off, xl + off, acc.m[t][0], acc.m[t][1]);
+                }
+                {   // G chunk row (tf32 hi/lo, MN-major over c')
+                    const uint32_t gh = s_base + L::G_OFF + q * 2 * L::GST, gl = gh + L::GST;
+                    const uint32_t off = mn32_off(4 * cl, rr);
+                    store_tf32x4(gh + off, gl + off, make_float2(gv.x, gv.y), make_float2(gv.z, gv.w));
+                }
+                {   // bias moments -> Xb tile row (fp16 hi/lo, per-row scale), K-major over c
+                    float inv = 1.f;
+                    float m = 0.f;
+                    m = fmaxf(fmaxf(fabsf(acc.m[3][0].x), fabsf(acc.m[3][0].y)), fmaxf(fabsf(acc.m[3][1].x), fabsf(acc.m[3][1].y)));
+                    for (int o = G::LPR >> 1; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                    const float sc = split_scale(m, inv);
+                    const int row = c * kDtChunk + rr;
+                    const uint32_t ah = s_base + L::XB_OFF + (i & 1) * 2 * L::XB, al = ah + L::XB;
+                    const int kin = 4 * cl;
+                    const uint32_t off = (uint32_t)((row >> 3) * 1024 + (row & 7) * 128 + (((kin >> 3) ^ (row & 7)) << 4) + (kin & 7) * 2);
+                    uint32_t l0, l1;
+                    const uint32_t h0 = cvt_pair<true>(fmul2(acc.m[3][0], make_float2(sc, sc)), l0);
+                    const uint32_t h1 = cvt_pair<true>(fmul2(acc.m[3][1], make_float2(sc, sc)), l1);
+                    sts64(ah + off, h0, h1);
+                    sts64(al + off, l0, l1);
+                    if (cl == 0) rs[(i & 1) * kTcM + row] = inv * binv;
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(chunk_full + q);
+                if (warp == kMmaWarp) {
+                    // warp 15 (odd chunks) issues the MMAs of this chunk and the even one before it
+                    issue_chunk(tl * 8 + c - 1);
+                    issue_chunk(tl * 8 + c);
+                    if (c == 7) issue_z(i);
+                }
+            }
+            if (warp < kEpiWarps && i >= 1) epilogue_z(i - 1);
+        }
+        if (warp == kMmaWarp && lane == 0) mma_commit(dt_done);
+        __syncwarp();
+        if (warp < kEpiWarps && tiles_mine > 0) epilogue_z((int)tiles_mine - 1);
+    }
+    // ---------------------------------------------------------------- drain d_theta partials
+    if (warp < kEpiWarps) {
+        if (tiles_mine > 0) {
+            mbar_wait(dt_done, 0);
+            tc_fence_after();
+        }
+        float *part = a.partial + (int64_t)blockIdx.x * (CO * 4 * GC);
+#pragma unroll
+        for (int mh = 0; mh < 2; ++mh) {
+            const int kx = mh * 128 + warp * 32 + lane;  // k = t*64 + c
+            const int t = kx / GC, cc = kx % GC;
+#pragma unroll
+            for (int n0 = 0; n0 < CO; n0 += 16) {
+                float v[16];
+                tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(mh * CO + n0), v);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const int cp = n0 + q;
+                    part[(int64_t)cp * (GC * 4) + cc * 4 + t] = tiles_mine > 0 ? v[q] : 0.f;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, L::TMEM_COLS);
+    }
+}
+
 // ---------------------------------------------------------------------------------
 // host side
-template <int GC, int NOUT, bool SPLIT, bool REVERSE, int KFIX>
+template <int GC, int NOUT, bool SPLIT, bool REVERSE, int KFIX, bool DLOC = false>
 static int launch_tc(const TcArgs &a0, int cin, int cout, const float *theta, const float *theta_b,
                      cudaStream_t st) {
-    using L = TcLayout<GC, NOUT, SPLIT>;
+    using L = TcLayout<GC, NOUT, SPLIT, DLOC>;
     TcArgs a = a0;
     uint8_t *img = (uint8_t *)scratch_alloc((size_t)L::B_BYTES * L::NSPLIT + 256, st);
     if (!img) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc)");
@@ -546,12 +969,12 @@ static int launch_tc(const TcArgs &a0, int cin, int cout, const float *theta, co
     a.num_tiles = ceil_div(a.total, kTcM);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(tc_gmc_kernel<GC, NOUT, SPLIT, REVERSE, KFIX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(tc_gmc_kernel<GC, NOUT, SPLIT, REVERSE, KFIX, DLOC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              L::SMEM);
         attr = true;
     }
     const int grid = (int)std::min<int64_t>(a.num_tiles, num_sms());
-    tc_gmc_kernel<GC, NOUT, SPLIT, REVERSE, KFIX><<<grid, kTcThreads, L::SMEM, st>>>(a);
+    tc_gmc_kernel<GC, NOUT, SPLIT, REVERSE, KFIX, DLOC><<<grid, kTcThreads, L::SMEM, st>>>(a);
     count_launch();
     scratch_free(img, st);
     return check_launch("tc_gmc_kernel");
@@ -561,6 +984,10 @@ template <int GC, int NOUT, bool SPLIT, bool REVERSE>
 static int launch_tc_k(const TcArgs &a, int cin, int cout, const float *theta, const float *theta_b,
                        cudaStream_t st) {
     if (!REVERSE && a.k == kSlots) return launch_tc<GC, NOUT, SPLIT, REVERSE, kSlots>(a, cin, cout, theta, theta_b, st);
+    if constexpr (REVERSE && NOUT <= 64) {
+        if (a.dloc) return launch_tc<GC, NOUT, SPLIT, true, 0, true>(a, cin, cout, theta, theta_b, st);
+    }
+    if (REVERSE && a.dloc) return set_error(FC_ERR_UNSUPPORTED, "tensor-core location gradient needs c_in <= 64");
     return launch_tc<GC, NOUT, SPLIT, REVERSE, 0>(a, cin, cout, theta, theta_b, st);
 }
 
@@ -607,6 +1034,95 @@ int tc_conv_forward(int mode, int64_t total, int64_t n, int c_in, int d, int k, 
 }
 
 int tc_reverse_supported(int mode, int gc, int d, int cout) { return tc_shape_ok(mode, gc, d, cout) ? 1 : 0; }
+
+template <typename T>
+int launch_dtheta_reduce(int chunks, int cin, int d, int cout, const T *partial, T *d_theta, T *d_theta_b,
+                         cudaStream_t st);
+
+// Full fp32 backward on the tensor cores (c_in = c_out = 64, d = 3):
+//   tc_dtheta_kernel : d_theta partials + centre term of d_locations
+//   dtheta_reduce    : fixed-order reduction of the per-CTA partials (fp64 accumulate)
+//   tc_gmc (reverse) : d_features (+ neighbour term of d_locations)
+int tc_backward_supported(int mode, int cin, int d, int cout) {
+    return (d == 3 && cin == 64 && cout == 64 && mode != FC_MODE_SIMT) ? 1 : 0;
+}
+
+int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int cout, const float *g,
+                const float *feat, const float *loc, const int32_t *nbr, Csr csr, const float *theta,
+                const float *theta_b, float *d_features, float *d_locations, float *d_theta, float *d_theta_b,
+                cudaStream_t st) {
+    (void)d;
+    using L = DtLayout;
+    const int64_t num_tiles = ceil_div(total, kTcM);
+    const int grid = (int)std::min<int64_t>(num_tiles, num_sms());
+    float *centre = nullptr;
+    int rc = FC_OK;
+    if (d_theta || d_theta_b || d_locations) {
+        const size_t img_bytes = (size_t)cout * 4 * cin * 2 * 2;
+        uint8_t *img = (uint8_t *)scratch_alloc(img_bytes + 256, st);
+        float *partial = (float *)scratch_alloc(sizeof(float) * grid * cout * cin * 4, st);
+        centre = (float *)scratch_alloc(sizeof(float) * total * 3, st);
+        if (!img || !partial || !centre) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc backward)");
+        float *binv = reinterpret_cast<float *>(img + img_bytes);
+        tc_pack_b_kernel<true><<<1, 1024, 0, st>>>(cin, cout, theta, theta_b, 0, cout, cin, img, binv);
+        count_launch();
+        DtArgs a{};
+        a.total = total;
+        a.n = n;
+        a.k = k;
+        a.feat = feat;
+        a.loc = loc;
+        a.g = g;
+        a.nbr = nbr;
+        a.bimg = img;
+        a.binv = binv;
+        a.partial = partial;
+        a.centre = centre;
+        a.num_tiles = num_tiles;
+        static bool attr8 = false, attr0 = false;
+        if (k == kSlots) {
+            if (!attr8) {
+                cudaFuncSetAttribute(tc_dtheta_kernel<kSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+                attr8 = true;
+            }
+            tc_dtheta_kernel<kSlots><<<grid, kTcThreads, L::SMEM, st>>>(a);
+        } else {
+            if (!attr0) {
+                cudaFuncSetAttribute(tc_dtheta_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+                attr0 = true;
+            }
+            tc_dtheta_kernel<0><<<grid, kTcThreads, L::SMEM, st>>>(a);
+        }
+        count_launch();
+        rc = check_launch("tc_dtheta_kernel");
+        if (!rc && (d_theta || d_theta_b))
+            rc = launch_dtheta_reduce<float>(grid, cin, 3, cout, partial, d_theta, d_theta_b, st);
+        scratch_free(img, st);
+        scratch_free(partial, st);
+        if (rc) return rc;
+    }
+    if (d_features || d_locations) {
+        float *df = d_features;
+        float *df_scratch = nullptr;
+        if (!df) df = df_scratch = (float *)scratch_alloc(sizeof(float) * total * cin, st);
+        TcArgs a{};
+        a.total = total;
+        a.n = n;
+        a.k = k;
+        a.rows = g;
+        a.loc = loc;
+        a.csr = csr;
+        a.out = df;
+        a.feat = feat;
+        a.centre = centre;
+        a.dloc = d_locations;
+        if (mode == FC_MODE_TC_BF16) rc = dispatch_tc<false, true>(cout, cin, a, cin, cout, theta, theta_b, st);
+        else rc = dispatch_tc<true, true>(cout, cin, a, cin, cout, theta, theta_b, st);
+        scratch_free(df_scratch, st);
+    }
+    scratch_free(centre, st);
+    return rc;
+}
 
 int tc_reverse_gmc(int mode, int64_t total, int64_t n, int gc, int d, int k, int cout, const float *rows,
                    const float *loc, Csr csr, const float *theta, const float *theta_b, float *out,

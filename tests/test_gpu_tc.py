@@ -70,6 +70,41 @@ def test_tc_deconv_and_dfeatures_vs_oracle(fc, oracle_mod, cin, cout, mode):
         np.testing.assert_allclose(df.cpu().numpy(), ref, rtol=1e-4, atol=1e-5)
 
 
+def _close_reduction(got, ref, name):
+    floor = 1e-5 + 1e-6 * float(np.abs(ref).max())
+    np.testing.assert_allclose(got, ref, rtol=1e-4, atol=floor, err_msg=name)
+    assert np.linalg.norm(got - ref) <= 1e-5 * np.linalg.norm(ref), name
+
+
+@pytest.mark.parametrize("n", [20000, 1000, 200])
+def test_tc_backward_64_vs_oracle(fc, oracle_mod, n):
+    """Full tensor-core backward (d_features, d_theta, d_theta_b, d_locations) at 64->64."""
+    from paper_1803_07289_b200 import _ops
+
+    k = 8
+    t, h = _layer(n, 64, 64, k, seed=25)
+    df, dth, dtb, dl = _ops.conv_backward(t["up"], t["feat"], t["loc"], t["nbr"], t["csr"], t["th"], t["tb"], 1, n,
+                                          need=(True, True, True, True), mode="split")
+    rdf, rdth, rdtb, rdl = oracle_mod.conv_backward(h["up"], h["feat"], h["loc"], h["nbr"], h["th"], h["tb"])
+    np.testing.assert_allclose(df.cpu().numpy(), rdf, rtol=1e-4, atol=1e-5)
+    _close_reduction(dth.cpu().numpy(), rdth, "d_theta")
+    _close_reduction(dtb.cpu().numpy(), rdtb, "d_theta_b")
+    _close_reduction(dl.cpu().numpy(), rdl, "d_locations")
+
+
+def test_tc_backward_bitwise_deterministic(fc):
+    import torch
+
+    from paper_1803_07289_b200 import _ops
+
+    n = 50000
+    t, _ = _layer(n, 64, 64, 8, seed=26)
+    run = lambda: _ops.conv_backward(t["up"], t["feat"], t["loc"], t["nbr"], t["csr"], t["th"], t["tb"], 1, n)  # noqa: E731
+    a, b = run(), run()
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+
+
 def test_tc_partial_tile_and_batch(fc, oracle_mod):
     """B=3 clouds of 1000 points (tiles straddle clouds, last tile partial)."""
     import torch
