@@ -251,6 +251,352 @@ struct Idx {
 };
 
 // ---------------------------------------------------------------------------------
+// Software-pipelined forward gather for k = 8 (one 8-slot batch per group).
+// A warp walks its sequence of groups ("items"); item w covers points p0(w) .. p0(w)+PPI-1.
+// Three-deep pipeline: raw index + centre position of item w+2 are issued during w, the
+// neighbour positions of w+1 are issued (and its rows prefetched to L2) during w, and the
+// rows of w are loaded and accumulated during w; no load result is consumed in the
+// iteration that issues it.
+struct GatherSrc {
+    const float *rows, *loc;
+    const int32_t *nbr;
+    int64_t total, n;
+};
+struct ItemMap {
+    int ipt;         // items per tile for this warp
+    int sub_base;    // first point of item 0 within its tile
+    int sub_stride;  // points between consecutive items of one tile
+    __device__ __forceinline__ int64_t p0(int64_t w) const {
+        return ((int64_t)blockIdx.x + (w / ipt) * gridDim.x) * kTcM + sub_base + (w % ipt) * sub_stride;
+    }
+};
+
+template <int GC>
+struct FwdPipe8 {
+    using G = Geo<GC>;
+    struct Raw {
+        int32_t nb, base;  // cloud-local neighbour index, cloud base
+        float l0, l1, l2;
+        bool v;
+    };
+    GatherSrc s;
+    ItemMap im;
+    int64_t items;
+    int pt, cl, ipt, slot;
+    Idx cur;
+    Raw r1;
+    int32_t j1;
+    float nl0, nl1, nl2;
+
+    __device__ __forceinline__ Raw raw_load(int64_t w) const {
+        Raw r{0, 0, 0.f, 0.f, 0.f, false};
+        if (w < items) {
+            const int64_t myp = im.p0(w) + ipt;
+            r.v = ipt < G::PPI && myp < s.total;
+            if (r.v) {
+                r.base = myp < s.n ? 0 : (int32_t)((myp / s.n) * s.n);
+                r.nb = __ldg(s.nbr + myp * kSlots + slot);
+                r.l0 = __ldg(s.loc + myp * 3 + 0);
+                r.l1 = __ldg(s.loc + myp * 3 + 1);
+                r.l2 = __ldg(s.loc + myp * 3 + 2);
+            }
+        }
+        return r;
+    }
+    __device__ __forceinline__ void issue_pos(const Raw &r) {
+        j1 = r.base + r.nb;
+        nl0 = nl1 = nl2 = 0.f;
+        if (r.v) {
+            nl0 = __ldg(s.loc + (int64_t)j1 * 3 + 0);
+            nl1 = __ldg(s.loc + (int64_t)j1 * 3 + 1);
+            nl2 = __ldg(s.loc + (int64_t)j1 * 3 + 2);
+        }
+    }
+    __device__ __forceinline__ void make_cur(const Raw &r) {
+        cur.j = j1;
+        cur.o0 = r.v ? r.l0 - nl0 : 0.f;
+        cur.o1 = r.v ? r.l1 - nl1 : 0.f;
+        cur.o2 = r.v ? r.l2 - nl2 : 0.f;
+    }
+    __device__ __forceinline__ void start(GatherSrc src, ItemMap map, int64_t n_items, int lane) {
+        s = src;
+        im = map;
+        items = n_items;
+        pt = lane / G::LPR;
+        cl = lane % G::LPR;
+        ipt = lane >> 3;
+        slot = lane & 7;
+        const Raw r0 = raw_load(0);
+        issue_pos(r0);
+        make_cur(r0);
+        r1 = raw_load(1);
+    }
+    // moments of item w (issues the prefetches of w+1 and w+2)
+    __device__ __forceinline__ void gather(int64_t w, Mom &acc) {
+        float4 v[kSlots];
+#pragma unroll
+        for (int q = 0; q < kSlots; ++q) {
+            const int32_t jj = __shfl_sync(0xffffffffu, cur.j, pt * 8 + q);
+            v[q] = __ldg(reinterpret_cast<const float4 *>(s.rows + (int64_t)jj * GC) + cl);
+        }
+        issue_pos(r1);
+        if (r1.v) {
+            const float *rp = s.rows + (int64_t)j1 * GC;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(rp));
+            if (GC * 4 > 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + 32));
+        }
+        r2_ = raw_load(w + 2);
+        mom_zero(acc);
+#pragma unroll
+        for (int q = 0; q < kSlots; ++q) {
+            const float w0 = __shfl_sync(0xffffffffu, cur.o0, pt * 8 + q);
+            const float w1 = __shfl_sync(0xffffffffu, cur.o1, pt * 8 + q);
+            const float w2 = __shfl_sync(0xffffffffu, cur.o2, pt * 8 + q);
+            mom_add(acc, v[q], w0, w1, w2);
+        }
+    }
+    // after the caller consumed item w: offsets of w+1 become current
+    __device__ __forceinline__ void advance() {
+        make_cur(r1);
+        r1 = r2_;
+    }
+    Raw r2_;
+};
+
+// ---------------------------------------------------------------------------------
+// Software-pipelined REVERSE gather (GC = 64: 2 points per item, 16 index slots per point,
+// lane = point * 16 + slot).  The reverse list of point p is ent[off[p] .. off[p+1]) (flat
+// forward slots e, source point i = e / k, offset l_i - l_p).  Four-deep pipeline:
+// off[] of item w+3, ent[] (+ centre position) of w+2, source positions of w+1 are issued
+// during w; rows of w are loaded in 8-slot sub-batches and accumulated in list order.
+// Lists longer than 16 finish on a (rare) unpipelined tail.
+struct RevPipe16 {
+    static constexpr int GC = 64;
+    const float *rows, *loc;
+    Csr csr;
+    int64_t total;
+    int k;
+    ItemMap im;
+    int64_t items;
+    int pt, cl, ipt, slot;
+    // stage "off" (item w+3): list range of the lane's point
+    int32_t oq0_3, ocnt_3;
+    // stage "ent" (item w+2)
+    int32_t eq0_2, ecnt_2, ent_2;
+    float lp0_2, lp1_2, lp2_2;
+    // stage "pos" (item w+1)
+    int32_t pq0_1, pcnt_1, j_1;
+    float lp0_1, lp1_1, lp2_1, nl0_1, nl1_1, nl2_1;
+    // current (item w)
+    int32_t q0, cnt, j;
+    float o0, o1, o2;
+
+    __device__ __forceinline__ void load_off(int64_t w, int32_t &q0o, int32_t &cnto) const {
+        q0o = 0;
+        cnto = 0;
+        if (w < items) {
+            const int64_t myp = im.p0(w) + ipt;
+            if (myp < total) {
+                q0o = __ldg(csr.off + myp);
+                cnto = __ldg(csr.off + myp + 1) - q0o;
+            }
+        }
+    }
+    __device__ __forceinline__ void load_ent(int64_t w, int32_t q0i, int32_t cnti) {
+        eq0_2 = q0i;
+        ecnt_2 = cnti;
+        ent_2 = -1;
+        lp0_2 = lp1_2 = lp2_2 = 0.f;
+        if (w < items) {
+            const int64_t myp = im.p0(w) + ipt;
+            if (myp < total) {
+                lp0_2 = __ldg(loc + myp * 3 + 0);
+                lp1_2 = __ldg(loc + myp * 3 + 1);
+                lp2_2 = __ldg(loc + myp * 3 + 2);
+                if (slot < cnti) ent_2 = __ldg(csr.ent + q0i + slot);
+            }
+        }
+    }
+    __device__ __forceinline__ void load_pos() {
+        pq0_1 = eq0_2;
+        pcnt_1 = ecnt_2;
+        lp0_1 = lp0_2, lp1_1 = lp1_2, lp2_1 = lp2_2;
+        j_1 = ent_2 >= 0 ? ent_2 / k : 0;
+        nl0_1 = nl1_1 = nl2_1 = 0.f;
+        if (ent_2 >= 0) {
+            nl0_1 = __ldg(loc + (int64_t)j_1 * 3 + 0);
+            nl1_1 = __ldg(loc + (int64_t)j_1 * 3 + 1);
+            nl2_1 = __ldg(loc + (int64_t)j_1 * 3 + 2);
+        }
+    }
+    __device__ __forceinline__ void make_cur() {
+        q0 = pq0_1;
+        cnt = pcnt_1;
+        j = j_1;
+        const bool v = slot < pcnt_1;
+        o0 = v ? nl0_1 - lp0_1 : 0.f;
+        o1 = v ? nl1_1 - lp1_1 : 0.f;
+        o2 = v ? nl2_1 - lp2_1 : 0.f;
+    }
+    __device__ __forceinline__ void start(const float *rows_, const float *loc_, Csr csr_, int64_t total_, int k_,
+                                          ItemMap map, int64_t n_items, int lane) {
+        rows = rows_;
+        loc = loc_;
+        csr = csr_;
+        total = total_;
+        k = k_;
+        im = map;
+        items = n_items;
+        pt = lane >> 4;
+        cl = lane & 15;
+        ipt = lane >> 4;
+        slot = lane & 15;
+        int32_t a0, c0;
+        load_off(0, a0, c0);
+        load_ent(0, a0, c0);
+        load_pos();
+        make_cur();  // item 0 (blocking, once)
+        load_off(1, a0, c0);
+        load_ent(1, a0, c0);
+        load_off(2, oq0_3, ocnt_3);
+    }
+    __device__ __forceinline__ void sub_batch(int b0, int mycnt, Mom &acc) const {
+        float4 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int32_t jj = __shfl_sync(0xffffffffu, j, pt * 16 + b0 + q);
+            v[q] = (b0 + q < mycnt) ? __ldg(reinterpret_cast<const float4 *>(rows + (int64_t)jj * GC) + cl)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const float w0 = __shfl_sync(0xffffffffu, o0, pt * 16 + b0 + q);
+            const float w1 = __shfl_sync(0xffffffffu, o1, pt * 16 + b0 + q);
+            const float w2 = __shfl_sync(0xffffffffu, o2, pt * 16 + b0 + q);
+            if (b0 + q < mycnt) mom_add(acc, v[q], w0, w1, w2);
+        }
+    }
+    // moments of item w; issues the loads of items w+1 .. w+3
+    __device__ __forceinline__ void gather(int64_t w, Mom &acc) {
+        const int mycnt = __shfl_sync(0xffffffffu, cnt, pt * 16);
+        const int c0 = __shfl_sync(0xffffffffu, cnt, 0), c1 = __shfl_sync(0xffffffffu, cnt, 16);
+        const int maxcnt = max(c0, c1);
+        mom_zero(acc);
+        // rows of the first 8 slots first, then the prefetches of later items
+        float4 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int32_t jj = __shfl_sync(0xffffffffu, j, pt * 16 + q);
+            v[q] = (q < mycnt) ? __ldg(reinterpret_cast<const float4 *>(rows + (int64_t)jj * GC) + cl)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        load_pos();                    // item w+1: source positions
+        load_ent(w + 2, oq0_3, ocnt_3);  // item w+2: list entries
+        load_off(w + 3, oq0_3, ocnt_3);  // item w+3: list ranges
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const float w0 = __shfl_sync(0xffffffffu, o0, pt * 16 + q);
+            const float w1 = __shfl_sync(0xffffffffu, o1, pt * 16 + q);
+            const float w2 = __shfl_sync(0xffffffffu, o2, pt * 16 + q);
+            if (q < mycnt) mom_add(acc, v[q], w0, w1, w2);
+        }
+        if (maxcnt > 8) sub_batch(8, mycnt, acc);
+        if (maxcnt > 16) {
+            // tail: lists longer than 16 entries, unpipelined, still in list order
+            const int64_t myp = im.p0(w) + ipt;
+            const float lp0 = myp < total ? __ldg(loc + myp * 3 + 0) : 0.f;
+            const float lp1 = myp < total ? __ldg(loc + myp * 3 + 1) : 0.f;
+            const float lp2 = myp < total ? __ldg(loc + myp * 3 + 2) : 0.f;
+            for (int b0 = 16; b0 < maxcnt; b0 += 16) {
+                int32_t jt = 0;
+                float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+                if (b0 + slot < cnt) {
+                    jt = __ldg(csr.ent + q0 + b0 + slot) / k;
+                    t0 = __ldg(loc + (int64_t)jt * 3 + 0) - lp0;
+                    t1 = __ldg(loc + (int64_t)jt * 3 + 1) - lp1;
+                    t2 = __ldg(loc + (int64_t)jt * 3 + 2) - lp2;
+                }
+                for (int q = 0; q < 16; ++q) {
+                    const int32_t jj = __shfl_sync(0xffffffffu, jt, pt * 16 + q);
+                    const float w0 = __shfl_sync(0xffffffffu, t0, pt * 16 + q);
+                    const float w1 = __shfl_sync(0xffffffffu, t1, pt * 16 + q);
+                    const float w2 = __shfl_sync(0xffffffffu, t2, pt * 16 + q);
+                    if (b0 + q < mycnt) {
+                        const float4 x = __ldg(reinterpret_cast<const float4 *>(rows + (int64_t)jj * GC) + cl);
+                        mom_add(acc, x, w0, w1, w2);
+                    }
+                }
+            }
+        }
+    }
+    __device__ __forceinline__ void advance() { make_cur(); }
+};
+
+// ---------------------------------------------------------------------------------
+// Accumulator drain of tile i by one epilogue warp (TMEM lane quadrant = warp % 4): one
+// thread per output row.  Kept out of line so that its registers do not add to the live
+// set of the gather pipeline it interrupts.
+template <int NOUT, bool DLOC, int CPB>
+__device__ __noinline__ void tc_gmc_epilogue(const TcArgs &a, int i, int warp, int lane, uint32_t tmem_base,
+                                             const float *rs, uint64_t *mma_done, uint64_t *d_free) {
+    const int64_t tile = blockIdx.x + (int64_t)i * gridDim.x;
+    const int row = warp * 32 + lane;
+    mbar_wait(mma_done + (i & 1), (i >> 1) & 1);
+    tc_fence_after();
+    const int64_t p = tile * kTcM + row;
+    const bool pv = p < a.total;
+    const float inv = rs[(i & 1) * kTcM + row];
+    float *orow = a.out + p * NOUT;
+    const uint32_t tbase = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)((i & 1) * CPB);
+    float nb0 = 0.f, nb1 = 0.f, nb2 = 0.f;
+#pragma unroll 1
+    for (int c0 = 0; c0 < NOUT; c0 += 16) {
+        float v[16];
+        tmem_ld16(tbase + (uint32_t)c0, v);
+        if (pv) {
+#pragma unroll
+            for (int q = 0; q < 16; q += 4) {
+                float4 w = make_float4(v[q] * inv, v[q + 1] * inv, v[q + 2] * inv, v[q + 3] * inv);
+                *reinterpret_cast<float4 *>(orow + c0 + q) = w;
+            }
+        }
+        if constexpr (DLOC) {
+            // neighbour role: -sum_c f[p, c] U_t[p, c] (the -dt terms of _native.pyx:121-127)
+            float f[16];
+            if (pv) {
+#pragma unroll
+                for (int q = 0; q < 16; q += 4) {
+                    const float4 x = __ldg(reinterpret_cast<const float4 *>(a.feat + p * NOUT + c0 + q));
+                    f[q] = x.x, f[q + 1] = x.y, f[q + 2] = x.z, f[q + 3] = x.w;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) f[q] = 0.f;
+            }
+            float u[16];
+            tmem_ld16(tbase + (uint32_t)(NOUT + c0), u);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) nb0 = fmaf(f[q], u[q], nb0);
+            tmem_ld16(tbase + (uint32_t)(2 * NOUT + c0), u);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) nb1 = fmaf(f[q], u[q], nb1);
+            tmem_ld16(tbase + (uint32_t)(3 * NOUT + c0), u);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) nb2 = fmaf(f[q], u[q], nb2);
+        }
+    }
+    if constexpr (DLOC) {
+        if (pv) {
+            a.dloc[p * 3 + 0] = a.centre[p * 3 + 0] - nb0 * inv;
+            a.dloc[p * 3 + 1] = a.centre[p * 3 + 1] - nb1 * inv;
+            a.dloc[p * 3 + 2] = a.centre[p * 3 + 2] - nb2 * inv;
+        }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(d_free + (i & 1));
+}
+
 template <int GC, int NOUT, bool SPLIT, bool REVERSE, int KFIX, bool DLOC = false>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_gmc_kernel(TcArgs a) {
     static_assert(!DLOC || REVERSE, "the location-gradient epilogue belongs to the reverse pass");
@@ -340,62 +686,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gmc_kernel(TcArgs a) {
     // ---------------------------------------------------------------- epilogue (warps 0..3)
     // warp q owns TMEM lanes / tile rows 32q .. 32q+31; one thread per output row.
     auto epilogue = [&](int i) {
-        const int64_t tile = blockIdx.x + (int64_t)i * gridDim.x;
-        const int row = warp * 32 + lane;
-        mbar_wait(mma_done + (i & 1), (i >> 1) & 1);
-        tc_fence_after();
-        const int64_t p = tile * kTcM + row;
-        const bool pv = p < a.total;
-        const float inv = rs[(i & 1) * kTcM + row];
-        float *orow = a.out + p * NOUT;
-        const uint32_t tbase = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)((i & 1) * L::CPB);
-        float nb0 = 0.f, nb1 = 0.f, nb2 = 0.f;
-#pragma unroll
-        for (int c0 = 0; c0 < NOUT; c0 += 16) {
-            float v[16];
-            tmem_ld16(tbase + (uint32_t)c0, v);
-            if (pv) {
-#pragma unroll
-                for (int q = 0; q < 16; q += 4) {
-                    float4 w = make_float4(v[q] * inv, v[q + 1] * inv, v[q + 2] * inv, v[q + 3] * inv);
-                    *reinterpret_cast<float4 *>(orow + c0 + q) = w;
-                }
-            }
-            if constexpr (DLOC) {
-                // neighbour role: -sum_c f[p, c] U_t[p, c] (the -dt terms of _native.pyx:121-127)
-                float f[16];
-                if (pv) {
-#pragma unroll
-                    for (int q = 0; q < 16; q += 4) {
-                        const float4 x = __ldg(reinterpret_cast<const float4 *>(a.feat + p * NOUT + c0 + q));
-                        f[q] = x.x, f[q + 1] = x.y, f[q + 2] = x.z, f[q + 3] = x.w;
-                    }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 16; ++q) f[q] = 0.f;
-                }
-                float u[16];
-                tmem_ld16(tbase + (uint32_t)(NOUT + c0), u);
-#pragma unroll
-                for (int q = 0; q < 16; ++q) nb0 = fmaf(f[q], u[q], nb0);
-                tmem_ld16(tbase + (uint32_t)(2 * NOUT + c0), u);
-#pragma unroll
-                for (int q = 0; q < 16; ++q) nb1 = fmaf(f[q], u[q], nb1);
-                tmem_ld16(tbase + (uint32_t)(3 * NOUT + c0), u);
-#pragma unroll
-                for (int q = 0; q < 16; ++q) nb2 = fmaf(f[q], u[q], nb2);
-            }
-        }
-        if constexpr (DLOC) {
-            if (pv) {
-                a.dloc[p * 3 + 0] = a.centre[p * 3 + 0] - nb0 * inv;
-                a.dloc[p * 3 + 1] = a.centre[p * 3 + 1] - nb1 * inv;
-                a.dloc[p * 3 + 2] = a.centre[p * 3 + 2] - nb2 * inv;
-            }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(d_free + (i & 1));
+        tc_gmc_epilogue<NOUT, DLOC, L::CPB>(a, i, warp, lane, tmem_base, rs, mma_done, d_free);
     };
 
     {
@@ -506,58 +797,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gmc_kernel(TcArgs a) {
             //   neighbour position of g+1 issued (and its rows prefetched to L2) during g,
             //   rows of g loaded and accumulated during g.
             // (the loaded values are only consumed one iteration later)
-            struct Raw {
-                int32_t nb, base;  // cloud-local neighbour index, cloud base
-                float l0, l1, l2;
-                bool v;
-                __device__ int32_t j() const { return base + nb; }
-            };
-            auto raw_load = [&](int64_t w) {
-                Raw r{0, 0, 0.f, 0.f, 0.f, false};
-                if (w < items) {
-                    const int64_t myp = item_p0(w) + ipt;
-                    r.v = ipt < G::PPI && myp < a.total;
-                    if (r.v) {
-                        r.base = myp < a.n ? 0 : (int32_t)((myp / a.n) * a.n);
-                        r.nb = __ldg(a.nbr + myp * kSlots + slot);
-                        r.l0 = __ldg(a.loc + myp * 3 + 0);
-                        r.l1 = __ldg(a.loc + myp * 3 + 1);
-                        r.l2 = __ldg(a.loc + myp * 3 + 2);
-                    }
-                }
-                return r;
-            };
-            Idx cur;
-            int cdummy;
-            if (items > 0) idx_load(item_p0(0), 0, cur, cdummy);
-            Raw r1 = raw_load(1);
+            FwdPipe8<GC> pipe;
+            pipe.start(GatherSrc{a.rows, a.loc, a.nbr, a.total, a.n},
+                       ItemMap{G::GPW, gw * G::PPI, kGatherWarps * G::PPI}, items, lane);
             for (int64_t w = 0; w < items; ++w) {
-                const int64_t p0 = item_p0(w);
-                float4 v[kSlots];
-                batch_load(cur, kSlots, v);
-                // g+1: neighbour positions, and its rows into L2
-                const int32_t j1 = r1.j();
-                float nl0 = 0.f, nl1 = 0.f, nl2 = 0.f;
-                if (r1.v) {
-                    nl0 = __ldg(a.loc + (int64_t)j1 * 3 + 0);
-                    nl1 = __ldg(a.loc + (int64_t)j1 * 3 + 1);
-                    nl2 = __ldg(a.loc + (int64_t)j1 * 3 + 2);
-                    const float *rp = a.rows + (int64_t)j1 * GC;
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(rp));
-                    if (GC * 4 > 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + 32));
-                }
-                // g+2: raw indices
-                const Raw r2 = raw_load(w + 2);
                 Mom acc;
-                mom_zero(acc);
-                batch_acc(cur, kSlots, v, acc);
-                finish(w, p0, acc);
-                // offsets of g+1
-                cur.j = j1;
-                cur.o0 = r1.v ? r1.l0 - nl0 : 0.f;
-                cur.o1 = r1.v ? r1.l1 - nl1 : 0.f;
-                cur.o2 = r1.v ? r1.l2 - nl2 : 0.f;
-                r1 = r2;
+                pipe.gather(w, acc);
+                finish(w, item_p0(w), acc);
+                pipe.advance();
+            }
+        } else if (REVERSE && GC == 64) {
+            RevPipe16 pipe;
+            pipe.start(a.rows, a.loc, a.csr, a.total, a.k, ItemMap{G::GPW, gw * G::PPI, kGatherWarps * G::PPI}, items,
+                       lane);
+            for (int64_t w = 0; w < items; ++w) {
+                Mom acc;
+                pipe.gather(w, acc);
+                finish(w, item_p0(w), acc);
+                pipe.advance();
             }
         } else {
             for (int64_t w = 0; w < items; ++w) {
@@ -830,41 +1087,49 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
         const int q = warp >> 3, r = warp & 7;
         const int pt = lane / G::LPR, cl = lane % G::LPR;
         const int ipt = lane >> 3, slot = lane & 7;
+        // items of this warp: (tile, chunk c = q + 2m), group r of the chunk
+        const ItemMap im{4, q * kDtChunk + 2 * r, 2 * kDtChunk};
+        FwdPipe8<GC> pipe;
+        if (KFIX == kSlots) pipe.start(GatherSrc{a.feat, a.loc, a.nbr, a.total, a.n}, im, tiles_mine * 4, lane);
         for (int64_t tl = 0; tl < tiles_mine; ++tl) {
             const int i = (int)tl;
             const int64_t tile = blockIdx.x + tl * gridDim.x;
             for (int c = q; c < 8; c += 2) {
-                const int64_t u = tl * 4 + (c >> 1);  // this stage's use count
+                const int64_t u = tl * 4 + (c >> 1);  // this stage's use count (= item index)
                 const int64_t p0 = tile * kTcM + c * kDtChunk + 2 * r;
                 // ---- moments of points p0, p0+1 (lane group pt)
                 Mom acc;
-                mom_zero(acc);
-                const int64_t myp = p0 + ipt;
-                const bool pv = ipt < 2 && myp < a.total;
-                const int cnt = KFIX ? KFIX : a.k;
-                for (int b0 = 0; b0 < cnt; b0 += kSlots) {
-                    int32_t j = 0;
-                    float o0 = 0.f, o1 = 0.f, o2 = 0.f;
-                    if (pv && b0 + slot < cnt) {
-                        const int32_t base = myp < a.n ? 0 : (int32_t)((myp / a.n) * a.n);
-                        j = base + __ldg(a.nbr + myp * cnt + b0 + slot);
-                        o0 = __ldg(a.loc + myp * 3 + 0) - __ldg(a.loc + (int64_t)j * 3 + 0);
-                        o1 = __ldg(a.loc + myp * 3 + 1) - __ldg(a.loc + (int64_t)j * 3 + 1);
-                        o2 = __ldg(a.loc + myp * 3 + 2) - __ldg(a.loc + (int64_t)j * 3 + 2);
-                    }
-                    float4 v[kSlots];
+                if (KFIX == kSlots) {
+                    pipe.gather(u, acc);
+                } else {
+                    mom_zero(acc);
+                    const int64_t myp = p0 + ipt;
+                    const bool pv = ipt < 2 && myp < a.total;
+                    const int cnt = a.k;
+                    for (int b0 = 0; b0 < cnt; b0 += kSlots) {
+                        int32_t j = 0;
+                        float o0 = 0.f, o1 = 0.f, o2 = 0.f;
+                        if (pv && b0 + slot < cnt) {
+                            const int32_t base = myp < a.n ? 0 : (int32_t)((myp / a.n) * a.n);
+                            j = base + __ldg(a.nbr + myp * cnt + b0 + slot);
+                            o0 = __ldg(a.loc + myp * 3 + 0) - __ldg(a.loc + (int64_t)j * 3 + 0);
+                            o1 = __ldg(a.loc + myp * 3 + 1) - __ldg(a.loc + (int64_t)j * 3 + 1);
+                            o2 = __ldg(a.loc + myp * 3 + 2) - __ldg(a.loc + (int64_t)j * 3 + 2);
+                        }
+                        float4 v[kSlots];
 #pragma unroll
-                    for (int s = 0; s < kSlots; ++s) {
-                        const int32_t jj = __shfl_sync(0xffffffffu, j, pt * 8 + s);
-                        v[s] = (b0 + s < cnt) ? __ldg(reinterpret_cast<const float4 *>(a.feat + (int64_t)jj * GC) + cl)
-                                              : make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
+                        for (int s = 0; s < kSlots; ++s) {
+                            const int32_t jj = __shfl_sync(0xffffffffu, j, pt * 8 + s);
+                            v[s] = (b0 + s < cnt) ? __ldg(reinterpret_cast<const float4 *>(a.feat + (int64_t)jj * GC) + cl)
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
 #pragma unroll
-                    for (int s = 0; s < kSlots; ++s) {
-                        const float w0 = __shfl_sync(0xffffffffu, o0, pt * 8 + s);
-                        const float w1 = __shfl_sync(0xffffffffu, o1, pt * 8 + s);
-                        const float w2 = __shfl_sync(0xffffffffu, o2, pt * 8 + s);
-                        if (b0 + s < cnt) mom_add(acc, v[s], w0, w1, w2);
+                        for (int s = 0; s < kSlots; ++s) {
+                            const float w0 = __shfl_sync(0xffffffffu, o0, pt * 8 + s);
+                            const float w1 = __shfl_sync(0xffffffffu, o1, pt * 8 + s);
+                            const float w2 = __shfl_sync(0xffffffffu, o2, pt * 8 + s);
+                            if (b0 + s < cnt) mom_add(acc, v[s], w0, w1, w2);
+                        }
                     }
                 }
                 const int64_t pme = p0 + pt;
@@ -908,6 +1173,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(chunk_full + q);
+                if (KFIX == kSlots) pipe.advance();
                 if (warp == kMmaWarp) {
                     // warp 15 (odd chunks) issues the MMAs of this chunk and the even one before it
                     issue_chunk(tl * 8 + c - 1);
