@@ -69,6 +69,35 @@ def algo_bytes_per_point(c_in, c_out, d, k, s=4):
     return fwd, bwd
 
 
+def kernel_bytes_per_point(name, c_in, c_out, d, k, s=4):
+    """Algorithmic bytes per centre point that each library kernel must move (every
+    tensor it reads or writes once)."""
+    table = {
+        # features + positions + neighbour row in, output row out
+        "tc_forward": s * c_in + 4 * d + 4 * k + s * c_out,
+        "simt_forward": s * c_in + 4 * d + 4 * k + s * c_out,
+        # + upstream row in, centre-role location term out
+        "tc_dtheta": s * c_in + 4 * d + 4 * k + s * c_out + 4 * d,
+        # upstream + positions + reverse CSR (offset + k entries on average) + own features
+        # + centre term in; d_features + d_locations out
+        "tc_reverse_dloc": s * c_out + 4 * d + (4 + 4 * k) + s * c_in + 4 * d + s * c_in + 4 * d,
+        "tc_reverse": s * c_out + 4 * d + (4 + 4 * k) + s * c_in,
+        "simt_reverse": s * c_out + 4 * d + (4 + 4 * k) + s * c_in + s * c_in + 4 * d + 4 * d,
+    }
+    return table.get(name)
+
+
+def ncu_traffic(name):
+    """DRAM bytes per point of kernel `name` from the committed ncu capture summary
+    (profiles/ncu_traffic.json, written by scripts/ncu_traffic.py), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    return d.get("kernels", {}).get(name, {}).get("dram_bytes_per_point")
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
@@ -262,17 +291,34 @@ def main():
     if not args.no_e2e:
         e2e = run_e2e(args, torch, _ops, feat, pos, nbr, g, theta, theta_b, n, k, world, dist)
 
+    # ---------------- per-kernel device times (library CUDA events on the launching stream),
+    # taken in a separate pass after the timed region so the timed region stays clean
+    with _lib.KernelTimer() as kt:
+        for _ in range(max(1, min(args.steps, 5))):
+            step()
+    kern = {name: statistics.mean(v) for name, v in kt.times.items() if v and min(v) >= 0}
+
     hbm, bf16, src = peaks()
     fwd_b, bwd_b = algo_bytes_per_point(c, c, d, k)
-    # dominant kernel = the larger phase; achieved = algorithmic bytes / its device time
-    if bwd_ms >= fwd_ms:
-        dom, dom_ms, dom_b = "conv_backward", bwd_ms, bwd_b
+    kernels = {}
+    for name, ms in kern.items():
+        b = kernel_bytes_per_point(name, c, c, d, k)
+        kernels[name] = {"ms": round(ms, 4), "bytes_per_point": b,
+                         "GBps": round(b * n / ms / 1e6, 1) if b else None,
+                         "frac": round(b * n / ms / 1e6 / hbm, 4) if b else None}
+    dom = max(kern, key=kern.get) if kern else None
+    if dom is not None and kernel_bytes_per_point(dom, c, c, d, k):
+        dom_b, dom_ms = kernel_bytes_per_point(dom, c, c, d, k), kern[dom]
     else:
-        dom, dom_ms, dom_b = "conv_forward", fwd_ms, fwd_b
+        dom, dom_b, dom_ms = "conv_backward", bwd_b, bwd_ms
     achieved = dom_b * n / (dom_ms / 1e3) / 1e9
+    traffic = ncu_traffic(dom)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": src,
-                "algorithmic_bytes_per_point": dom_b,
+                "frac": round(achieved / hbm, 4),
+                "traffic": round(traffic * n) if traffic else None,
+                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read+write)" if traffic else None,
+                "peak_source": src + " (MEASURED_PEAKS.json hbm_gbs)" if src == "measured" else src,
+                "algorithmic_bytes_per_point": dom_b, "kernels": kernels,
                 "phases": {"forward": {"ms": round(fwd_ms, 4), "bytes_per_point": fwd_b,
                                        "GBps": round(fwd_b * n / fwd_ms / 1e6, 1)},
                            "backward": {"ms": round(bwd_ms, 4), "bytes_per_point": bwd_b,

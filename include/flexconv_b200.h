@@ -71,6 +71,15 @@ const char *fc_last_error(void);
 /* Number of kernel launches this library has issued (process-wide counter). */
 uint64_t fc_launch_count(void);
 
+/* Optional per-kernel timing: while enabled, CUDA events are recorded on the launching
+ * stream around each main kernel; after synchronising, fc_profile_ms(i) is the device time
+ * of record i (fc_profile_name(i) names the kernel).  Used by bench.py's roofline. */
+void fc_profile_enable(int on);
+void fc_profile_reset(void);
+int fc_profile_count(void);
+const char *fc_profile_name(int i);
+float fc_profile_ms(int i);
+
 /* ---- flex_conv -------------------------------------------------------------------
  * Replaces _native.flex_conv_forward(features, locations, neighbors, theta, theta_b,
  * out, num_threads) (_native.pyx:25-28), called by flexops.flex_conv_forward

@@ -34,6 +34,11 @@ SIGNATURES = {
     "fc_abi_version": [],
     "fc_last_error": [],
     "fc_launch_count": [],
+    "fc_profile_enable": [_I],
+    "fc_profile_reset": [],
+    "fc_profile_count": [],
+    "fc_profile_name": [_I],
+    "fc_profile_ms": [_I],
     "fc_conv_forward": [_I, _I, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P],
     "fc_conv_backward": [_I, _I, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "fc_deconv_forward": [_I, _I, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
@@ -49,7 +54,8 @@ SIGNATURES = {
     "fc_indices_to_i32": [_P, _P, _I64, _I64, _P, _P],
     "fc_check_indices": [_P, _I64, _I64, _P, _P],
 }
-_RESTYPE = {"fc_last_error": ctypes.c_char_p, "fc_launch_count": ctypes.c_uint64}
+_RESTYPE = {"fc_last_error": ctypes.c_char_p, "fc_launch_count": ctypes.c_uint64, "fc_profile_enable": None,
+            "fc_profile_reset": None, "fc_profile_name": ctypes.c_char_p, "fc_profile_ms": ctypes.c_float}
 
 _lib = None
 
@@ -80,6 +86,27 @@ def call(name: str, *args) -> None:
 
 def launch_count() -> int:
     return int(lib().fc_launch_count())
+
+
+class KernelTimer:
+    """Context manager: per-kernel CUDA-event times recorded by the library on the
+    launching stream (fc_profile_*).  `.times` maps kernel name -> list of ms."""
+
+    def __enter__(self):
+        lib().fc_profile_reset()
+        lib().fc_profile_enable(1)
+        self.times = {}
+        return self
+
+    def __exit__(self, *exc):
+        import torch
+
+        lib().fc_profile_enable(0)
+        torch.cuda.synchronize()
+        for i in range(lib().fc_profile_count()):
+            name = lib().fc_profile_name(i).decode()
+            self.times.setdefault(name, []).append(float(lib().fc_profile_ms(i)))
+        lib().fc_profile_reset()
 
 
 def symbols() -> list[str]:

@@ -27,6 +27,34 @@ int check_launch(const char *what) {
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+// ---- optional per-kernel event timing (fc_profile_*): CUDA events recorded on the
+// launching stream around the main kernels, read back after the caller synchronises.
+struct ProfRec {
+    const char *name;
+    cudaEvent_t a, b;
+};
+static std::atomic<int> g_prof_on{0};
+static ProfRec g_prof[4096];
+static std::atomic<int> g_prof_n{0};
+static ProfRec *g_prof_open = nullptr;
+
+void prof_begin(const char *name, cudaStream_t st) {
+    if (!g_prof_on.load()) return;
+    const int i = g_prof_n.fetch_add(1);
+    if (i >= 4096) return;
+    ProfRec &r = g_prof[i];
+    r.name = name;
+    cudaEventCreate(&r.a);
+    cudaEventCreate(&r.b);
+    cudaEventRecord(r.a, st);
+    g_prof_open = &r;
+}
+void prof_end(cudaStream_t st) {
+    if (!g_prof_on.load() || !g_prof_open) return;
+    cudaEventRecord(g_prof_open->b, st);
+    g_prof_open = nullptr;
+}
+
 // Stream-ordered scratch from the device's default memory pool (kept resident: the
 // release threshold is raised once so repeated calls do not return memory to the OS).
 void *scratch_alloc(size_t bytes, cudaStream_t st) {
@@ -129,6 +157,27 @@ extern "C" {
 int fc_abi_version(void) { return FC_ABI_VERSION; }
 const char *fc_last_error(void) { return g_err; }
 uint64_t fc_launch_count(void) { return g_launches.load(); }
+
+void fc_profile_enable(int on) { g_prof_on.store(on ? 1 : 0); }
+void fc_profile_reset(void) {
+    const int n = std::min(g_prof_n.load(), 4096);
+    for (int i = 0; i < n; ++i) {
+        cudaEventDestroy(g_prof[i].a);
+        cudaEventDestroy(g_prof[i].b);
+    }
+    g_prof_n.store(0);
+}
+int fc_profile_count(void) { return std::min(g_prof_n.load(), 4096); }
+const char *fc_profile_name(int i) { return (i >= 0 && i < fc_profile_count()) ? g_prof[i].name : ""; }
+float fc_profile_ms(int i) {
+    if (i < 0 || i >= fc_profile_count()) return -1.f;
+    float ms = -1.f;
+    if (cudaEventElapsedTime(&ms, g_prof[i].a, g_prof[i].b) != cudaSuccess) {
+        cudaGetLastError();
+        return -1.f;
+    }
+    return ms;
+}
 
 int fc_conv_forward(int dtype, int mode, int64_t batch, int64_t n, int c_in, int d, int k, int c_out,
                     const void *features, const void *locations, const int32_t *neighbors,

@@ -331,6 +331,7 @@ static int launch_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, cons
     const size_t smem = per_point * ppw * 8;
     if (smem > 200 * 1024) return set_error(FC_ERR_UNSUPPORTED, "channel count too large for the SIMT engine (%d)", gc);
     const int grid = grid_for(ceil_div(total, 8 * ppw), 1);
+    prof_begin(REV ? "simt_reverse" : "simt_forward", st);
     switch (ppw) {
         case 4:
             set_smem(gmc_kernel<T, DP, REV, 4>, smem);
@@ -345,6 +346,7 @@ static int launch_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, cons
             gmc_kernel<T, DP, REV, 1><<<grid, 256, smem, st>>>(total, n, gc, k, cout, rows, loc, nbr, csr, w, out, feat, theta, centre, dloc);
             break;
     }
+    prof_end(st);
     count_launch();
     return check_launch("gmc_kernel");
 }

@@ -1240,7 +1240,9 @@ static int launch_tc(const TcArgs &a0, int cin, int cout, const float *theta, co
         attr = true;
     }
     const int grid = (int)std::min<int64_t>(a.num_tiles, num_sms());
+    prof_begin(REVERSE ? (DLOC ? "tc_reverse_dloc" : "tc_reverse") : "tc_forward", st);
     tc_gmc_kernel<GC, NOUT, SPLIT, REVERSE, KFIX, DLOC><<<grid, kTcThreads, L::SMEM, st>>>(a);
+    prof_end(st);
     count_launch();
     scratch_free(img, st);
     return check_launch("tc_gmc_kernel");
@@ -1346,6 +1348,7 @@ int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int c
         a.centre = centre;
         a.num_tiles = num_tiles;
         static bool attr8 = false, attr0 = false;
+        prof_begin("tc_dtheta", st);
         if (k == kSlots) {
             if (!attr8) {
                 cudaFuncSetAttribute(tc_dtheta_kernel<kSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
@@ -1359,6 +1362,7 @@ int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int c
             }
             tc_dtheta_kernel<0><<<grid, kTcThreads, L::SMEM, st>>>(a);
         }
+        prof_end(st);
         count_launch();
         rc = check_launch("tc_dtheta_kernel");
         if (!rc && (d_theta || d_theta_b))

@@ -87,5 +87,8 @@ int build_csr(const int32_t *keys, int64_t count, BucketFn bf, int64_t buckets, 
 void *scratch_alloc(size_t bytes, cudaStream_t st);
 void scratch_free(void *p, cudaStream_t st);
 void count_launch();
+// per-kernel event timing (fc_profile_*); no-ops unless enabled
+void prof_begin(const char *name, cudaStream_t st);
+void prof_end(cudaStream_t st);
 
 }  // namespace fc
