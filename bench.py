@@ -113,6 +113,23 @@ class ClockSampler:
         self._th = None
 
     def _run(self):
+        try:  # NVML (what nvidia-smi reads), sampled every 10 ms
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append([str(self.gpu), str(sm), str(mx), "", hex(rs)] +
+                                 ["Active" if rs & b else "Not Active" for b in bits])
+                self._stop.wait(0.01)
+            return
+        except Exception:  # noqa: BLE001 -- fall back to nvidia-smi
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
