@@ -21,6 +21,8 @@
 //   BF16: single bf16 MMA per k-step (stated 1e-2 relative tolerance).
 // REVERSE = the same kernel over the reverse neighbourhood (d_features of the backward
 // and flex_deconv): Y_j = sum_{(i,s) in R(j)} (l_i - l_j, 1) (x) g_i, out = Y_j . B_rev.
+#include <cstdlib>
+
 #include "fc_common.cuh"
 #include "sm100.cuh"
 
@@ -1285,10 +1287,31 @@ int tc_conv_forward_supported(int mode, int c_in, int d, int k, int c_out) {
     return tc_shape_ok(mode, c_in, d, c_out) ? 1 : 0;
 }
 
+void launch_pack_b(bool split, int cin, int cout, const float *theta, const float *theta_b, int reverse, int nout,
+                   int gc, uint8_t *img, float *binv, cudaStream_t st) {
+    if (split) tc_pack_b_kernel<true><<<1, 1024, 0, st>>>(cin, cout, theta, theta_b, reverse, nout, gc, img, binv);
+    else tc_pack_b_kernel<false><<<1, 1024, 0, st>>>(cin, cout, theta, theta_b, reverse, nout, gc, img, binv);
+    count_launch();
+}
+
+int tc_fast_forward(bool split, int64_t total, int64_t n, const float *feat, const float *loc, const int32_t *nbr,
+                    const float *theta, const float *theta_b, float *out, cudaStream_t st);
+
+static bool fast_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("FC_NO_FAST");
+        on = (e && e[0] == '1') ? 0 : 1;
+    }
+    return on == 1;
+}
+
 int tc_conv_forward(int mode, int64_t total, int64_t n, int c_in, int d, int k, int c_out, const float *feat,
                     const float *loc, const int32_t *nbr, const float *theta, const float *theta_b, float *out,
                     cudaStream_t st) {
     (void)d;
+    if (c_in == 64 && c_out == 64 && k == kSlots && fast_enabled())
+        return tc_fast_forward(mode != FC_MODE_TC_BF16, total, n, feat, loc, nbr, theta, theta_b, out, st);
     TcArgs a{};
     a.total = total;
     a.n = n;

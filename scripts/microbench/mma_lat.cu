@@ -1,0 +1,67 @@
+// microbenchmark: steady-state cycles per tcgen05.mma kind::f16 (cta_group::1) for M x N x 16,
+// operands K-major SW128 in shared memory, one issuing thread, commit + wait per chain.
+#include <cstdint>
+#include <cstdio>
+
+#include "../../paper_1803_07289_b200/csrc/sm100.cuh"
+using namespace fc::sm100;
+
+__global__ void k(long long *out, int M, int N, int nmma, int reps) {
+    extern __shared__ __align__(1024) uint8_t sm_raw[];
+    uint8_t *sm = (uint8_t *)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+    // A: 4 K-blocks x M rows x 128 B (<= 64 KB); B: 4 K-blocks x N rows x 128 B (<= 128 KB)
+    uint8_t *A = sm, *B = sm + 65536;
+    uint64_t *bar = (uint64_t *)(sm + 65536 + 131072);
+    uint32_t *holder = (uint32_t *)(bar + 2);
+    for (int i = threadIdx.x; i < (65536 + 131072) / 4; i += blockDim.x) ((uint32_t *)sm)[i] = 0x3c003c00u;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    if (threadIdx.x < 32) tmem_alloc(holder, 256);
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    uint32_t tb = *holder;
+    if (threadIdx.x == 0) {
+        const uint32_t idesc = idesc_f16(M, N, 0);
+        const uint32_t a = smem_u32(A), b = smem_u32(B);
+        long long best = 1ll << 60;
+        for (int r = 0; r < reps; ++r) {
+            long long t0 = clock64();
+            for (int m = 0; m < nmma; ++m) {
+                const int t = m & 3, kk = (m >> 2) & 3;
+                mma_f16(tb, desc_sw128(a + t * (M * 128) + kk * 32), desc_sw128(b + t * (N * 128) + kk * 32), idesc,
+                        m > 0);
+            }
+            mma_commit(bar);
+            mbar_wait(bar, r & 1);
+            long long dt = clock64() - t0;
+            best = dt < best ? dt : best;
+        }
+        out[0] = best;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        tc_fence_after();
+        tmem_dealloc(tb, 256);
+    }
+}
+int main() {
+    long long *d, h;
+    cudaMalloc(&d, 16);
+    const int smem = 65536 + 131072 + 2048;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int shapes[][2] = {{128, 64}, {128, 128}, {128, 256}, {64, 64}, {64, 128}, {64, 256}};
+    for (auto &sh : shapes) {
+        for (int n : {1, 8, 32, 96}) {
+            k<<<1, 128, smem>>>(d, sh[0], sh[1], n, 10);
+            cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+            printf("M=%3d N=%3d nmma=%3d: %6lld cyc  %.1f cyc/mma  %.0f MAC/cyc\n", sh[0], sh[1], n, h, (double)h / n,
+                   (double)sh[0] * sh[1] * 16 * n / h);
+        }
+    }
+    printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
+}
