@@ -870,7 +870,7 @@ struct DtArgs {
     const int32_t *nbr;
     const uint8_t *bimg;  // forward fp16 image (hi, lo); K-blocks 0..2 used
     const float *binv;
-    float *partial;       // [gridDim.x][CO * 4 * GC], layout (c', c, t) like dtheta_partial_kernel
+    float *partial;       // [gridDim.x][2 (hi / lo lanes)][CO * 4 * GC], layout (c', c, t) like dtheta_partial_kernel
     float *centre;        // [total, 3]
     int64_t num_tiles;
 };
@@ -888,7 +888,7 @@ struct DtLayout {
     static constexpr int RS_OFF = B_OFF + 2 * 3 * BZ;   // float rs[2][128]
     static constexpr int BAR_OFF = RS_OFF + 2 * kTcM * 4;
     static constexpr int SMEM = BAR_OFF + 128 + 1024;
-    static constexpr int TMEM_COLS = 512;               // D: 2 x 64, Z: 2 x 192
+    static constexpr int TMEM_COLS = 512;               // D: 256 (M = [c' hi; c' lo], N = k), Z: 192
 };
 
 __device__ __forceinline__ uint32_t f32_to_tf32(float x) {
@@ -990,49 +990,48 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
     // ---------------------------------------------------------------- MMA issue (warp 15, lane 0)
     int mma_chunk = 0;  // next chunk (in this CTA's order) whose MMAs are to be issued
     auto issue_chunk = [&](int64_t u_global) {
-        // u_global = tile_local * 8 + c
+        // u_global = tile_local * 8 + c.  D[(c' | c'+64), k] += [G_hi; G_lo]^T . X_hi + [G_hi; G_lo]^T . X_lo:
+        // M = 128 (upstream channel hi / lo parts), N = 256 (all moment columns), K = 8 points
+        // per MMA -- a kind::tf32 MMA costs ~104 cycles up to N = 128 and ~130 at N = 256, so
+        // this is 2 MMAs per 8 points instead of 6 (M = k halves, N = c' = 64).
         const int c = (int)(u_global & 7);
         const int st = c & 1;
         const int64_t u = u_global >> 1;  // completion index of stage st
         if (lane == 0) {
             mbar_wait(chunk_full + st, (uint32_t)(u & 1));
             tc_fence_after();
-            constexpr uint32_t idesc = idesc_tf32_mn(kTcM, CO);
+            constexpr uint32_t idesc = idesc_tf32_mn(kTcM, 4 * GC);
             const uint32_t xh = s_base + L::X_OFF + st * 2 * L::XST, xl = xh + L::XST;
-            const uint32_t gh = s_base + L::G_OFF + st * 2 * L::GST, gl = gh + L::GST;
+            const uint32_t gh = s_base + L::G_OFF + st * 2 * L::GST;  // [G_hi | G_lo]: 4 MN blocks of 32
 #pragma unroll
-            for (int mh = 0; mh < 2; ++mh) {
-#pragma unroll
-                for (int ks = 0; ks < kDtChunk / 8; ++ks) {
-                    const uint32_t ao = (uint32_t)(mh * 4 * 2048 + ks * 1024), bo = (uint32_t)(ks * 1024);
-                    const uint32_t first = (u_global == 0 && ks == 0) ? 0u : 1u;
-                    const uint32_t d = tmem_base + (uint32_t)(mh * CO);
-                    mma_tf32(d, desc_sw128b32_mn(xh + ao, 2048, 512), desc_sw128b32_mn(gh + bo, 2048, 512), idesc, first);
-                    mma_tf32(d, desc_sw128b32_mn(xh + ao, 2048, 512), desc_sw128b32_mn(gl + bo, 2048, 512), idesc, 1u);
-                    mma_tf32(d, desc_sw128b32_mn(xl + ao, 2048, 512), desc_sw128b32_mn(gh + bo, 2048, 512), idesc, 1u);
-                }
+            for (int ks = 0; ks < kDtChunk / 8; ++ks) {
+                const uint32_t ko = (uint32_t)(ks * 1024);
+                const uint32_t first = (u_global == 0 && ks == 0) ? 0u : 1u;
+                mma_tf32(tmem_base, desc_sw128b32_mn(gh + ko, 2048, 512), desc_sw128b32_mn(xh + ko, 2048, 512), idesc, first);
+                mma_tf32(tmem_base, desc_sw128b32_mn(gh + ko, 2048, 512), desc_sw128b32_mn(xl + ko, 2048, 512), idesc, 1u);
             }
             mma_commit(chunk_empty + st);
         }
         __syncwarp();
     };
     auto issue_z = [&](int i) {
+        // Z[p, (t, c')] = Xb[p, :] . theta[c', :, t] for t = 0..2 as ONE N = 192 operand: the
+        // K-blocks 0..2 of the forward image are 64-row blocks 8 KB apart, i.e. a 192-row
+        // K-major SW128 operand.  Single TMEM buffer (columns 256..447): wait until the
+        // epilogue of tile i-1 has drained it.
         if (lane == 0) {
-            if (i >= 2) mbar_wait(z_free + (i & 1), ((i >> 1) + 1) & 1);
+            if (i >= 1) mbar_wait(z_free + ((i - 1) & 1), (uint32_t)(((i - 1) >> 1) & 1));
             tc_fence_after();
-            constexpr uint32_t idesc = idesc_f16(kTcM, CO, 0);
+            constexpr uint32_t idesc = idesc_f16(kTcM, 3 * CO, 0);
             const uint32_t ah = s_base + L::XB_OFF + (i & 1) * 2 * L::XB, al = ah + L::XB;
             const uint32_t bh = s_base + L::B_OFF, bl = bh + 3 * L::BZ;
+            const uint32_t z = tmem_base + 256u;
 #pragma unroll
-            for (int t = 0; t < 3; ++t) {
-                const uint32_t z = tmem_base + 2 * CO + (uint32_t)((i & 1) * 3 * CO + t * CO);
-#pragma unroll
-                for (int s = 0; s < GC / 16; ++s) {
-                    const uint32_t ao = (uint32_t)(s * 32), bo = (uint32_t)(t * L::BZ + s * 32);
-                    mma_f16(z, desc_sw128(ah + ao), desc_sw128(bh + bo), idesc, s > 0 ? 1u : 0u);
-                    mma_f16(z, desc_sw128(ah + ao), desc_sw128(bl + bo), idesc, 1u);
-                    mma_f16(z, desc_sw128(al + ao), desc_sw128(bh + bo), idesc, 1u);
-                }
+            for (int s = 0; s < GC / 16; ++s) {
+                const uint32_t ao = (uint32_t)(s * 32), bo = (uint32_t)(s * 32);
+                mma_f16(z, desc_sw128(ah + ao), desc_sw128(bh + bo), idesc, s > 0 ? 1u : 0u);
+                mma_f16(z, desc_sw128(ah + ao), desc_sw128(bl + bo), idesc, 1u);
+                mma_f16(z, desc_sw128(al + ao), desc_sw128(bh + bo), idesc, 1u);
             }
             mma_commit(z_done + (i & 1));
         }
@@ -1046,7 +1045,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
         mbar_wait(z_done + (i & 1), (i >> 1) & 1);
         tc_fence_after();
         const float inv = rs[(i & 1) * kTcM + row];
-        const uint32_t tb = tmem_base + ((uint32_t)(warp * 32) << 16) + 2 * CO + (uint32_t)((i & 1) * 3 * CO);
+        const uint32_t tb = tmem_base + ((uint32_t)(warp * 32) << 16) + 256u;
         float c0 = 0.f, c1 = 0.f, c2 = 0.f;
 #pragma unroll
         for (int q0 = 0; q0 < CO; q0 += 16) {
@@ -1195,20 +1194,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
             mbar_wait(dt_done, 0);
             tc_fence_after();
         }
-        float *part = a.partial + (int64_t)blockIdx.x * (CO * 4 * GC);
+        // TMEM lane m = c' (hi part, warps 0-1) or 64 + c' (lo part, warps 2-3): two partial
+        // slices per CTA, summed by dtheta_reduce_kernel with the other CTAs' (fixed order)
+        const int m = warp * 32 + lane;
+        const int cp = m & 63;
+        float *part = a.partial + ((int64_t)blockIdx.x * 2 + (m >> 6)) * (CO * 4 * GC);
+#pragma unroll 1
+        for (int n0 = 0; n0 < 4 * GC; n0 += 16) {
+            float v[16];
+            tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)n0, v);
 #pragma unroll
-        for (int mh = 0; mh < 2; ++mh) {
-            const int kx = mh * 128 + warp * 32 + lane;  // k = t*64 + c
-            const int t = kx / GC, cc = kx % GC;
-#pragma unroll
-            for (int n0 = 0; n0 < CO; n0 += 16) {
-                float v[16];
-                tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(mh * CO + n0), v);
-#pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    const int cp = n0 + q;
-                    part[(int64_t)cp * (GC * 4) + cc * 4 + t] = tiles_mine > 0 ? v[q] : 0.f;
-                }
+            for (int q = 0; q < 16; ++q) {
+                const int kx = n0 + q;  // k = t*64 + c
+                const int t = kx / GC, cc = kx % GC;
+                part[(int64_t)cp * (GC * 4) + cc * 4 + t] = tiles_mine > 0 ? v[q] : 0.f;
             }
         }
     }
@@ -1351,7 +1350,7 @@ int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int c
     if (d_theta || d_theta_b || d_locations) {
         const size_t img_bytes = (size_t)cout * 4 * cin * 2 * 2;
         uint8_t *img = (uint8_t *)scratch_alloc(img_bytes + 256, st);
-        float *partial = (float *)scratch_alloc(sizeof(float) * grid * cout * cin * 4, st);
+        float *partial = (float *)scratch_alloc(sizeof(float) * 2 * grid * cout * cin * 4, st);
         centre = (float *)scratch_alloc(sizeof(float) * total * 3, st);
         if (!img || !partial || !centre) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc backward)");
         float *binv = reinterpret_cast<float *>(img + img_bytes);
@@ -1389,7 +1388,7 @@ int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int c
         count_launch();
         rc = check_launch("tc_dtheta_kernel");
         if (!rc && (d_theta || d_theta_b))
-            rc = launch_dtheta_reduce<float>(grid, cin, 3, cout, partial, d_theta, d_theta_b, st);
+            rc = launch_dtheta_reduce<float>(2 * grid, cin, 3, cout, partial, d_theta, d_theta_b, st);
         scratch_free(img, st);
         scratch_free(partial, st);
         if (rc) return rc;

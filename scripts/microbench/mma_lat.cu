@@ -6,7 +6,11 @@
 #include "../../paper_1803_07289_b200/csrc/sm100.cuh"
 using namespace fc::sm100;
 
-__global__ void k(long long *out, int M, int N, int nmma, int reps) {
+__device__ __forceinline__ void mma_tf32_(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+                 "l"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
+}
+__global__ void k(long long *out, int M, int N, int nmma, int reps, int tf32) {
     extern __shared__ __align__(1024) uint8_t sm_raw[];
     uint8_t *sm = (uint8_t *)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
     // A: 4 K-blocks x M rows x 128 B (<= 64 KB); B: 4 K-blocks x N rows x 128 B (<= 128 KB)
@@ -25,14 +29,16 @@ __global__ void k(long long *out, int M, int N, int nmma, int reps) {
     tc_fence_after();
     uint32_t tb = *holder;
     if (threadIdx.x == 0) {
-        const uint32_t idesc = idesc_f16(M, N, 0);
+        const uint32_t idesc = tf32 ? ((1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24))
+                                    : idesc_f16(M, N, 0);
         const uint32_t a = smem_u32(A), b = smem_u32(B);
         long long best = 1ll << 60;
         for (int r = 0; r < reps; ++r) {
             long long t0 = clock64();
             for (int m = 0; m < nmma; ++m) {
                 const int t = m & 3, kk = (m >> 2) & 3;
-                mma_f16(tb, desc_sw128(a + t * (M * 128) + kk * 32), desc_sw128(b + t * (N * 128) + kk * 32), idesc,
+                if (tf32) mma_tf32_(tb, desc_sw128(a + t * (M * 128) + kk * 32), desc_sw128(b + t * (N * 128) + kk * 32), idesc, m > 0);
+                else mma_f16(tb, desc_sw128(a + t * (M * 128) + kk * 32), desc_sw128(b + t * (N * 128) + kk * 32), idesc,
                         m > 0);
             }
             mma_commit(bar);
@@ -55,13 +61,14 @@ int main() {
     const int smem = 65536 + 131072 + 2048;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int shapes[][2] = {{128, 64}, {128, 128}, {128, 256}, {64, 64}, {64, 128}, {64, 256}};
-    for (auto &sh : shapes) {
-        for (int n : {1, 8, 32, 96}) {
-            k<<<1, 128, smem>>>(d, sh[0], sh[1], n, 10);
-            cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-            printf("M=%3d N=%3d nmma=%3d: %6lld cyc  %.1f cyc/mma  %.0f MAC/cyc\n", sh[0], sh[1], n, h, (double)h / n,
-                   (double)sh[0] * sh[1] * 16 * n / h);
+    for (int tf = 0; tf < 2; ++tf)
+        for (auto &sh : shapes) {
+            for (int n : {1, 32, 96}) {
+                k<<<1, 128, smem>>>(d, sh[0], sh[1], n, 10, tf);
+                cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+                printf("%s M=%3d N=%3d nmma=%3d: %6lld cyc  %.1f cyc/mma  %.0f MAC/cyc\n", tf ? "tf32" : "f16 ", sh[0], sh[1],
+                       n, h, (double)h / n, (double)sh[0] * sh[1] * (tf ? 8 : 16) * n / h);
+            }
         }
-    }
     printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
 }
