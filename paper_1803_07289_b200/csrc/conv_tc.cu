@@ -1249,9 +1249,19 @@ static int launch_tc(const TcArgs &a0, int cin, int cout, const float *theta, co
     return check_launch("tc_gmc_kernel");
 }
 
+int tc_fast_reverse(bool split, int64_t total, int k, const float *rows, const float *loc, Csr csr, const float *theta,
+                    const float *theta_b, float *out, const float *feat, const float *centre, float *dloc,
+                    cudaStream_t st);
+static bool fast_enabled();
+
 template <int GC, int NOUT, bool SPLIT, bool REVERSE>
 static int launch_tc_k(const TcArgs &a, int cin, int cout, const float *theta, const float *theta_b,
                        cudaStream_t st) {
+    if constexpr (REVERSE && GC == 64 && NOUT == 64) {
+        if (fast_enabled())
+            return tc_fast_reverse(SPLIT, a.total, a.k, a.rows, a.loc, a.csr, theta, theta_b, a.out, a.feat, a.centre,
+                                   a.dloc, st);
+    }
     if (!REVERSE && a.k == kSlots) return launch_tc<GC, NOUT, SPLIT, REVERSE, kSlots>(a, cin, cout, theta, theta_b, st);
     if constexpr (REVERSE && NOUT <= 64) {
         if (a.dloc) return launch_tc<GC, NOUT, SPLIT, true, 0, true>(a, cin, cout, theta, theta_b, st);
