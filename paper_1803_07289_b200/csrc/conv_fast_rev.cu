@@ -388,6 +388,34 @@ __global__ void __launch_bounds__(rThreads, 1) tc_rev64_kernel(RevArgs a) {
                 v[s2] = ldg_nc4(ok ? src + (int64_t)jr * 64 : zsrc);
             }
         };
+        auto load4 = [&](const Item &it, int h, int b0) {
+            const float *src = a.rows + 32 * h + 4 * cl;
+            const float *zsrc = a.zero + 4 * cl;
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+                const int sl = b0 + s2;
+                const bool ok = sl < it.cnt;
+                const int32_t jr = lds32(it.es + (uint32_t)((ok ? it.start + sl : rCap) * 16));
+                v[s2] = ldg_nc4(ok ? src + (int64_t)jr * 64 : zsrc);
+            }
+        };
+        auto fma4 = [&](const Item &it, int b0, Mom4 &x) {
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+                const int sl = b0 + s2;
+                const float4 e = lds128f(it.es + (uint32_t)((sl < it.cnt ? it.start + sl : rCap) * 16));
+                const float2 lo = make_float2(v[s2].x, v[s2].y), hi = make_float2(v[s2].z, v[s2].w);
+                const float2 w0 = make_float2(e.y, e.y), w1 = make_float2(e.z, e.z), w2 = make_float2(e.w, e.w);
+                x.m[0][0] = ffma2(lo, w0, x.m[0][0]);
+                x.m[0][1] = ffma2(hi, w0, x.m[0][1]);
+                x.m[1][0] = ffma2(lo, w1, x.m[1][0]);
+                x.m[1][1] = ffma2(hi, w1, x.m[1][1]);
+                x.m[2][0] = ffma2(lo, w2, x.m[2][0]);
+                x.m[2][1] = ffma2(hi, w2, x.m[2][1]);
+                x.m[3][0] = fadd2(x.m[3][0], lo);
+                x.m[3][1] = fadd2(x.m[3][1], hi);
+            }
+        };
         auto fma8 = [&](const Item &it, int b0, Mom4 &x) {
 #pragma unroll
             for (int s2 = 0; s2 < 8; ++s2) {
@@ -461,9 +489,9 @@ __global__ void __launch_bounds__(rThreads, 1) tc_rev64_kernel(RevArgs a) {
                     direct_item(cur, h, x);
                 } else {
                     if (cur.mx > 0) fma8(cur, 0, x);
-                    for (int b0 = 8; b0 < cur.mx; b0 += 8) {
-                        load8(cur, h, b0);
-                        fma8(cur, b0, x);
+                    for (int b0 = 8; b0 < cur.mx; b0 += 4) {  // tails in 4-slot batches
+                        load4(cur, h, b0);
+                        fma4(cur, b0, x);
                     }
                 }
                 if (hk >= 2) {  // last use of the group's stage by this warp

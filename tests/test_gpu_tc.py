@@ -153,3 +153,38 @@ def test_tc_adjoint_identity_at_1M(fc):
     rhs = float((t["feat"].double() * atx).sum())
     scale = float(af.abs().sum() * t["up"].double().abs().max())
     assert abs(lhs - rhs) <= 1e-6 * scale, (lhs, rhs, scale)
+
+
+@pytest.mark.parametrize("hub_degree", [40, 900])
+def test_tc_reverse_long_lists_vs_oracle(fc, oracle_mod, hub_degree):
+    """Reverse lists longer than the staged per-row limit (16) and 64-row groups whose lists
+    overflow the stage capacity take the direct CSR path of the fast reverse kernel: a
+    hand-built neighbourhood where `hub_degree` points all list a few hub points."""
+    import torch
+
+    from paper_1803_07289_b200 import _ops
+    from paper_1803_07289_b200.core import synthetic_layer
+
+    n, k = 4096, 8
+    loc, feat, th, tb, up = synthetic_layer(41, 0, n, 3, 64, 64)
+    rng = np.random.default_rng(7)
+    nbr = np.empty((n, k), np.int64)
+    nbr[:, 0] = np.arange(n)
+    nbr[:, 1:] = rng.integers(0, n, size=(n, k - 1))
+    hubs = [5, 70, 200]  # rows in different 64-row groups
+    for h in hubs:
+        rows = rng.choice(n, size=hub_degree, replace=False)
+        nbr[rows, 1 + (h % (k - 1))] = h
+    dev = torch.device("cuda")
+    tl = {name: torch.from_numpy(v).to(dev, torch.float32) for name, v in
+          dict(loc=loc, feat=feat, th=th, tb=tb, up=up).items()}
+    nb = torch.from_numpy(nbr).to(dev, torch.int32)
+    csr = _ops.csr_build(nb, 1, n)
+    y = _ops.deconv_forward(tl["up"], tl["loc"], csr, tl["th"], tl["tb"], 1, n, k, "split").cpu().numpy()
+    ref = oracle_mod.deconv_forward(up, loc, nbr, th, tb)
+    np.testing.assert_allclose(y, ref, rtol=1e-4, atol=1e-5)
+    df, _, _, dl = _ops.conv_backward(tl["up"], tl["feat"], tl["loc"], nb, csr, tl["th"], tl["tb"], 1, n,
+                                      need=(True, True, True, True), mode="split")
+    rdf, _, _, rdl = oracle_mod.conv_backward(up, feat, loc, nbr, th, tb)
+    np.testing.assert_allclose(df.cpu().numpy(), rdf, rtol=1e-4, atol=1e-5)
+    _close_reduction(dl.cpu().numpy(), rdl, "d_locations")
