@@ -1347,6 +1347,10 @@ int tc_backward_supported(int mode, int cin, int d, int cout) {
     return (d == 3 && cin == 64 && cout == 64 && mode != FC_MODE_SIMT) ? 1 : 0;
 }
 
+int tc_fast_dtheta(int64_t total, int64_t n, const float *feat, const float *loc, const int32_t *nbr, const float *g,
+                   const float *theta, const float *theta_b, float *d_theta, float *d_theta_b, float *centre,
+                   cudaStream_t st);
+
 int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int cout, const float *g,
                 const float *feat, const float *loc, const int32_t *nbr, Csr csr, const float *theta,
                 const float *theta_b, float *d_features, float *d_locations, float *d_theta, float *d_theta_b,
@@ -1357,7 +1361,17 @@ int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int c
     const int grid = (int)std::min<int64_t>(num_tiles, num_sms());
     float *centre = nullptr;
     int rc = FC_OK;
-    if (d_theta || d_theta_b || d_locations) {
+    if ((d_theta || d_theta_b || d_locations) && k == kSlots && fast_enabled()) {
+        if (d_locations) {
+            centre = (float *)scratch_alloc(sizeof(float) * total * 3, st);
+            if (!centre) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc backward)");
+        }
+        rc = tc_fast_dtheta(total, n, feat, loc, nbr, g, theta, theta_b, d_theta, d_theta_b, centre, st);
+        if (rc) {
+            scratch_free(centre, st);
+            return rc;
+        }
+    } else if (d_theta || d_theta_b || d_locations) {
         const size_t img_bytes = (size_t)cout * 4 * cin * 2 * 2;
         uint8_t *img = (uint8_t *)scratch_alloc(img_bytes + 256, st);
         float *partial = (float *)scratch_alloc(sizeof(float) * 2 * grid * cout * cin * 4, st);
