@@ -20,6 +20,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def bench_name(kernel: str):
+    if "tc_fwd64_kernel" in kernel:
+        return "tc_forward"
+    if "tc_dt64_kernel" in kernel:
+        return "tc_dtheta"
+    m = re.search(r"tc_rev64_kernel<(?:\(bool\))?(\w+), (?:\(bool\))?(\w+)>", kernel)
+    if m:
+        return "tc_reverse_dloc" if m.group(2) in ("1", "true") else "tc_reverse"
     m = re.search(r"tc_gmc_kernel<\(?int\)?(\d+), \(?int\)?(\d+), \(?bool\)?(\d), \(?bool\)?(\d), \(?int\)?(\d+), \(?bool\)?(\d)>", kernel)
     if m:
         rev, dloc = m.group(4) == "1", m.group(6) == "1"
@@ -43,7 +50,7 @@ def main():
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     log = os.path.join(ROOT, "gpurun_out", "ncu_traffic.csv")
     cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
-           "--clock-control", "none", "-k", "regex:tc_|gmc|dtheta", "--csv", "--log-file", log,
+           "--clock-control", "none", "-k", "regex:tc_|gmc|dtheta|fwd64|rev64|dt64", "--csv", "--log-file", log,
            sys.executable, os.path.join(ROOT, "bench.py"), "--n", str(args.n), "--steps", "1", "--warmup", "1",
            "--no-cpu", "--no-e2e", "--mode", args.mode]
     subprocess.run(cmd, check=True, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
