@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_fwd64_kernel(FwdArgs a) {
         auto epilogue = [&](int i) {
             if (a.dbg & 8) return;
             const int b = i & 1;
-            mbar_wait(acc_full + b, (uint32_t)((i >> 1) & 1));
+            mbar_wait_sleep(acc_full + b, (uint32_t)((i >> 1) & 1));
             TRACE(10, i, 0);
             tc_fence_after();
             const int64_t p = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + t;
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_fwd64_kernel(FwdArgs a) {
         };
         auto store_e = [&](int i, const Nb &nb, const Pos &ps) {
             const int st = i & 1;
-            if (i >= 2) mbar_wait(e_empty + st, (uint32_t)(((i >> 1) + 1) & 1));
+            if (i >= 2) mbar_wait_sleep(e_empty + st, (uint32_t)(((i >> 1) + 1) & 1));
             TRACE(20, i, 0);
             const uint32_t es = E0 + (uint32_t)(st * L::E_STAGE);
 #pragma unroll

@@ -67,13 +67,22 @@ struct DtArgs2 {
     const float *binv;
     float *partial;       // [gridDim.x][2][64 * 4 * 64], layout (c', c, t)
     float *centre;        // [total, 3]
+    int dbg;                    // FC_DBG & 8: per-role wait-cycle counters
+    unsigned long long *clk;    // [grid][24][4]
 };
 
-__device__ __forceinline__ uint32_t tf32_rna(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
-}
+#define DT_CLK(slot, stmt)                                                  \
+    do {                                                                    \
+        long long _c0, _c1;                                                 \
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(_c0)::"memory");      \
+        stmt;                                                               \
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(_c1)::"memory");      \
+        ck[slot] += _c1 - _c0;                                              \
+    } while (0)
+
+// tf32 hi part by truncation (the low 13 mantissa bits cleared); lo = x - hi is exact and
+// carries the remaining 13 bits (read by the MMA as tf32: 2^-21 relative overall)
+__device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xffffe000u; }
 // byte offset of MN element mn in K-row r of an SW128_BASE32B MN-major image (16 K-rows per
 // MN block of 32 elements): MN blocks 2 KB apart, 4-row K groups 512 B apart
 __device__ __forceinline__ uint32_t mn32(int mn, int r) {
@@ -127,6 +136,9 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bar + 14);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    long long ck[4] = {0, 0, 0, 0};
+    long long ck_t0;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(ck_t0)::"memory");
     if (threadIdx.x == 0) {
         for (int q = 0; q < 2; ++q) {
             mbar_init(e_full + q, dIdxWarps);
@@ -172,7 +184,7 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
         // 256 + 64t + 8s .. +7), g[p, 8s .. 8s+7] from global (L2)
         auto zslice = [&](int i, int s) {
             if (s == 0) {
-                mbar_wait(z_done, (uint32_t)(i & 1));
+                DT_CLK(1, mbar_wait_sleep(z_done, (uint32_t)(i & 1)));
                 tc_fence_after();
                 pz = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + row;
                 inv = exp2i(rs[(i & 1) * kTile + row]) * binv;
@@ -213,7 +225,7 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
                 if (warp == dEpiWarp0) {
                     if (lane == 0) {
                         const int u = i * (kTile / dChunk) + c, st = u & 1;
-                        mbar_wait(c_full + st, (uint32_t)((u >> 1) & 1));
+                        DT_CLK(0, mbar_wait(c_full + st, (uint32_t)((u >> 1) & 1)));
                         tc_fence_after();
                         const uint32_t cs = C0 + (uint32_t)(st * L::STAGE);
                         const uint32_t xh = cs, xl = cs + L::XST, gh = cs + 2 * L::XST;
@@ -232,7 +244,7 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
             // Z of tile i: single TMEM buffer, free once the epilogue of tile i-1 drained it
             if (warp == dEpiWarp0) {
                 if (lane == 0) {
-                    if (i >= 1) mbar_wait(z_free + ((i - 1) & 1), (uint32_t)(((i - 1) >> 1) & 1));
+                    if (i >= 1) DT_CLK(2, mbar_wait(z_free + ((i - 1) & 1), (uint32_t)(((i - 1) >> 1) & 1)));
                     tc_fence_after();
                     const uint32_t ah = XB0 + (uint32_t)((i & 1) * 2 * L::XB), al = ah + L::XB;
                     const uint32_t bh = BZ0, bl = BZ0 + 3 * L::BZ;
@@ -312,7 +324,7 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
         };
         auto store_e = [&](int i, const Nb &nb, const Pos &ps) {
             const int st = i & 1;
-            if (i >= 2) mbar_wait(e_empty + st, (uint32_t)(((i >> 1) + 1) & 1));
+            if (i >= 2) mbar_wait_sleep(e_empty + st, (uint32_t)(((i >> 1) + 1) & 1));
             const uint32_t es = E0 + (uint32_t)(st * L::E_STAGE);
 #pragma unroll
             for (int s2 = 0; s2 < dK; ++s2)
@@ -341,15 +353,28 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
         const int cc = 2 * lane;
         const float *fsrc = a.feat + cc;
         float2 v[dK];
+        float2 gn;  // upstream row of the point whose rows are in v
         auto issue_loads = [&](int i, int c) {
-            if (c == 0) mbar_wait(e_full + (i & 1), (uint32_t)((i >> 1) & 1));
+            if (c == 0) DT_CLK(0, mbar_wait(e_full + (i & 1), (uint32_t)((i >> 1) & 1)));
             const int row = dChunk * c + warp;
+            const int64_t p = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + row;
             const uint32_t es = E0 + (uint32_t)((i & 1) * L::E_STAGE + row * 16);
             int32_t j[dK];
 #pragma unroll
             for (int s2 = 0; s2 < dK; ++s2) j[s2] = lds32(es + (uint32_t)(s2 * kTile * 16));
 #pragma unroll
             for (int s2 = 0; s2 < dK; ++s2) v[s2] = ldg_nc2(fsrc + (int64_t)j[s2] * 64);
+            gn = p < a.total ? ldg_nc2(a.g + p * 64 + cc) : make_float2(0.f, 0.f);
+        };
+        // The hand-off of a chunk stage (proxy fence = MEMBAR.CTA, which waits for all of the
+        // thread's outstanding loads, + arrival) is deferred to the next chunk, at the point
+        // where that chunk's rows have landed and the following rows are not yet issued.
+        int pend = -1;
+        auto handoff = [&]() {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(c_full + pend);
+            pend = -1;
         };
         if (T > 0) issue_loads(0, 0);
         for (int i = 0; i < T; ++i) {
@@ -370,22 +395,23 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
                     m2 = ffma2(v[s2], make_float2(e.w, e.w), m2);
                     m3 = fadd2(m3, v[s2]);
                 }
+                const float2 gv = gn;
                 if (c == kTile / dChunk - 1) {  // E(i) no longer read by this warp
                     __syncwarp();
                     if (lane == 0) mbar_arrive(e_empty + (i & 1));
                 }
-                const float2 gv = pv ? ldg_nc2(a.g + p * 64 + cc) : make_float2(0.f, 0.f);
+                if (pend >= 0) handoff();
                 if (c + 1 < kTile / dChunk) issue_loads(i, c + 1);
                 else if (i + 1 < T) issue_loads(i + 1, 0);
                 if (!pv) m0 = m1 = m2 = m3 = make_float2(0.f, 0.f);
                 // ---- Xb row (fp16 hi/lo, per-row scale) -> Z tile row `row`
-                float mx = fmaxf(fabsf(m3.x), fabsf(m3.y));
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                // row max of |Xb|: non-negative floats order like their bit patterns -> one REDUX
+                const float mx = __uint_as_float(
+                    __reduce_max_sync(0xffffffffu, __float_as_uint(fmaxf(fabsf(m3.x), fabsf(m3.y)))));
                 const int e = scale_exp(mx);
                 if (c == 0 && i >= 2) {  // Xb buffer / rs slot of tile i-2 consumed (Z MMAs done, epilogue read rs)
-                    mbar_wait(xb_free + (i & 1), (uint32_t)(((i >> 1) + 1) & 1));
-                    mbar_wait(z_free + (i & 1), (uint32_t)(((i >> 1) + 1) & 1));
+                    DT_CLK(1, mbar_wait(xb_free + (i & 1), (uint32_t)(((i >> 1) + 1) & 1)));
+                    DT_CLK(1, mbar_wait(z_free + (i & 1), (uint32_t)(((i >> 1) + 1) & 1)));
                 }
                 {
                     uint32_t lo;
@@ -397,29 +423,34 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
                 }
                 // ---- X row (tf32 hi/lo) and G row into chunk stage u & 1
                 const int u = i * (kTile / dChunk) + c, st = u & 1;
-                if (u >= 2) mbar_wait(c_empty + st, (uint32_t)(((u >> 1) + 1) & 1));
+                if (u >= 2) DT_CLK(2, mbar_wait(c_empty + st, (uint32_t)(((u >> 1) + 1) & 1)));
                 const uint32_t cs = C0 + (uint32_t)(st * L::STAGE);
                 const float2 mm[4] = {m0, m1, m2, m3};
 #pragma unroll
                 for (int tt = 0; tt < 4; ++tt) {
                     const uint32_t off = mn32(tt * 64 + cc, warp);
-                    const uint32_t h0 = tf32_rna(mm[tt].x), h1 = tf32_rna(mm[tt].y);
+                    const uint32_t h0 = tf32_hi(mm[tt].x), h1 = tf32_hi(mm[tt].y);
                     sts64u(cs + off, h0, h1);
                     sts64u(cs + L::XST + off, __float_as_uint(mm[tt].x - __uint_as_float(h0)),
                            __float_as_uint(mm[tt].y - __uint_as_float(h1)));
                 }
                 {
                     const uint32_t off = mn32(cc, warp);
-                    const uint32_t h0 = tf32_rna(gv.x), h1 = tf32_rna(gv.y);
+                    const uint32_t h0 = tf32_hi(gv.x), h1 = tf32_hi(gv.y);
                     sts64u(cs + 2 * L::XST + off, h0, h1);
                     sts64u(cs + 2 * L::XST + L::GST + off, __float_as_uint(gv.x - __uint_as_float(h0)),
                            __float_as_uint(gv.y - __uint_as_float(h1)));
                 }
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(c_full + st);
+                pend = st;
             }
         }
+        if (pend >= 0) handoff();
+    }
+    if ((a.dbg & 8) && lane == 0) {
+        long long t1;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1)::"memory");
+        unsigned long long *o = a.clk + ((int64_t)blockIdx.x * 24 + warp) * 4;
+        o[0] = ck[0], o[1] = ck[1], o[2] = ck[2], o[3] = t1 - ck_t0;
     }
     tc_fence_before();
     __syncthreads();
@@ -464,6 +495,15 @@ int tc_fast_dtheta(int64_t total, int64_t n, const float *feat, const float *loc
     a.binv = binv;
     a.partial = partial;
     a.centre = centre ? centre : cscratch;
+    {
+        const char *e = getenv("FC_DBG");
+        a.dbg = e ? atoi(e) : 0;
+    }
+    static unsigned long long *clk = nullptr;
+    if (a.dbg & 8) {
+        if (!clk) cudaMalloc(&clk, sizeof(unsigned long long) * 148 * 24 * 4);
+        a.clk = clk;
+    }
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(tc_dt64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DtL::SMEM_ALLOC);
@@ -474,6 +514,24 @@ int tc_fast_dtheta(int64_t total, int64_t n, const float *feat, const float *loc
     prof_end(st);
     count_launch();
     int rc = check_launch("tc_dt64_kernel");
+    if (a.dbg & 8) {
+        static unsigned long long h[148 * 24 * 4];
+        cudaMemcpyAsync(h, clk, sizeof(unsigned long long) * grid * 24 * 4, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        const char *nm[3] = {"gather (e_full, xb/z_free, c_empty)", "index (-)", "mma/epi (c_full, z_done, z_free)"};
+        for (int r = 0; r < 3; ++r) {
+            const int w0 = r == 0 ? 0 : (r == 1 ? dIdxWarp0 : dEpiWarp0), w1 = r == 0 ? 16 : w0 + 4;
+            for (int w = w0; w < w1; w += (r == 2 ? 1 : w1 - w0)) {
+                double acc[4] = {};
+                const int we = r == 2 ? w + 1 : w1;
+                for (int b = 0; b < grid; ++b)
+                    for (int ww = w; ww < we; ++ww)
+                        for (int k = 0; k < 4; ++k) acc[k] += (double)h[((size_t)b * 24 + ww) * 4 + k] / (grid * (we - w));
+                fprintf(stderr, "%s w%d: total %.0f  waits %.1f%% %.1f%% %.1f%%\n", nm[r], w, acc[3], 100 * acc[0] / acc[3],
+                        100 * acc[1] / acc[3], 100 * acc[2] / acc[3]);
+            }
+        }
+    }
     if (!rc && (d_theta || d_theta_b)) rc = launch_dtheta_reduce<float>(2 * grid, 64, 3, 64, partial, d_theta, d_theta_b, st);
     scratch_free(img, st);
     scratch_free(partial, st);

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(rThreads, 1) tc_rev64_kernel(RevArgs a) {
             if (h == 1) mma_commit(acc_full);
         };
         auto epilogue = [&](int i) {
-            mbar_wait(acc_full, (uint32_t)(i & 1));
+            mbar_wait_sleep(acc_full, (uint32_t)(i & 1));
             tc_fence_after();
             const int b = i & 1;
             const int tr = ew * 32 + lane;
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(rThreads, 1) tc_rev64_kernel(RevArgs a) {
             const bool direct = direct_row || start + staged > rCap;
             // store
             const int st = gg % rStages;
-            if (gg >= rStages) mbar_wait(e_empty + st, (uint32_t)(((gg / rStages) + 1) & 1));
+            if (gg >= rStages) mbar_wait_sleep(e_empty + st, (uint32_t)(((gg / rStages) + 1) & 1));
             const uint32_t es = E0 + (uint32_t)(st * L::E_STAGE);
             if (!direct) {
 #pragma unroll
