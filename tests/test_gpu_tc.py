@@ -188,3 +188,37 @@ def test_tc_reverse_long_lists_vs_oracle(fc, oracle_mod, hub_degree):
     rdf, _, _, rdl = oracle_mod.conv_backward(up, feat, loc, nbr, th, tb)
     np.testing.assert_allclose(df.cpu().numpy(), rdf, rtol=1e-4, atol=1e-5)
     _close_reduction(dl.cpu().numpy(), rdl, "d_locations")
+
+
+def test_tc_backward_batched_partial_tiles(fc, oracle_mod):
+    """Warp-specialised backward kernels on B = 3 clouds of 1000 points (cloud-local
+    neighbour indices, tiles straddling clouds, a partial last tile) vs the per-cloud oracle."""
+    import torch
+
+    from paper_1803_07289_b200 import _ops
+    from paper_1803_07289_b200.core import synthetic_layer
+
+    B, n, k, c = 3, 1000, 8, 64
+    parts = [synthetic_layer(50 + b, 0, n, 3, c, c) for b in range(B)]
+    dev = torch.device("cuda")
+    cat = lambda i: torch.from_numpy(np.concatenate([p[i] for p in parts])).to(dev, torch.float32)  # noqa: E731
+    loc, feat, up = cat(0), cat(1), cat(4)
+    th = torch.from_numpy(parts[0][2]).to(dev, torch.float32)
+    tb = torch.from_numpy(parts[0][3]).to(dev, torch.float32)
+    nbr = _ops.knn(loc, B, n, k)
+    csr = _ops.csr_build(nbr, B, n)
+    df, dth, dtb, dl = _ops.conv_backward(up, feat, loc, nbr, csr, th, tb, B, n, need=(True, True, True, True),
+                                          mode="split")
+    nb = nbr.cpu().numpy().astype(np.int64)
+    rdth = np.zeros_like(parts[0][2], dtype=np.float64)
+    rdtb = np.zeros_like(parts[0][3], dtype=np.float64)
+    for b in range(B):
+        sl = slice(b * n, (b + 1) * n)
+        rdf, r_th, r_tb, rdl = oracle_mod.conv_backward(parts[b][4], parts[b][1], parts[b][0], nb[sl], parts[0][2],
+                                                        parts[0][3])
+        np.testing.assert_allclose(df[sl].cpu().numpy(), rdf, rtol=1e-4, atol=1e-5)
+        _close_reduction(dl[sl].cpu().numpy(), rdl, "d_locations")
+        rdth += r_th
+        rdtb += r_tb
+    _close_reduction(dth.cpu().numpy(), rdth, "d_theta")
+    _close_reduction(dtb.cpu().numpy(), rdtb, "d_theta_b")
