@@ -444,6 +444,284 @@ __global__ void __launch_bounds__(kThreads, 1) tc_fwd64_kernel(FwdArgs a) {
     }
 }
 
+
+// =================================================================================
+// Wide-lane variant: lane = 8 channels of one point (one 32-byte LDG.256 per neighbour
+// slot), an item = 8 points x one channel half, 2 items per gather warp per tile.  Per
+// point this halves the load, index-entry and bookkeeping instructions of the 4-channel
+// lanes above.  20 warps (5 per SM sub-partition -> 96 registers): 16 gather warps and one
+// control warpgroup that produces the index entries, runs the epilogue and (warp 16,
+// lane 0) issues the MMAs.
+// =================================================================================
+constexpr int wGatherWarps = 16;
+constexpr int wCtlWarp0 = 16;
+constexpr int wThreads = 20 * 32;
+
+__device__ __forceinline__ void ldg_nc8(const float *p, float (&v)[8]) {
+    asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(p));
+}
+__device__ __forceinline__ void sts128u(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+template <bool SPLIT>
+__global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
+    using L = FwdL<SPLIT>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sb = smem_u32(smem);
+    const uint32_t A_hi = sb + L::A_OFF, A_lo = A_hi + L::A_BYTES;
+    const uint32_t Bimg = sb + L::B_OFF;
+    const uint32_t E0 = sb + L::E_OFF;
+    const uint32_t rs_s = sb + L::RS_OFF;  // int8 [2 buf][2 half][128]
+    const int8_t *rs = reinterpret_cast<const int8_t *>(smem + L::RS_OFF);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + L::BAR_OFF);
+    uint64_t *e_full = bar + 0;     // [2] control warps
+    uint64_t *e_empty = bar + 2;    // [2] gather warps
+    uint64_t *a_full = bar + 4;     // [2 halves] gather warps
+    uint64_t *mma_done = bar + 6;   // [2 halves] commit: A half free
+    uint64_t *acc_full = bar + 8;   // [2 bufs] commit after half 1
+    uint64_t *acc_free = bar + 10;  // [2 bufs] control warps
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bar + 12);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 2; ++q) {
+            mbar_init(e_full + q, 4);
+            mbar_init(e_empty + q, wGatherWarps);
+            mbar_init(a_full + q, wGatherWarps);
+            mbar_init(mma_done + q, 1);
+            mbar_init(acc_full + q, 1);
+            mbar_init(acc_free + q, 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == wCtlWarp0) tmem_alloc(tmem_holder, 512);
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.bimg);
+        uint4 *dst = reinterpret_cast<uint4 *>(smem + L::B_OFF);
+        for (int i = threadIdx.x; i < L::B_BYTES / 16; i += blockDim.x) dst[i] = src[i];
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+    const int T = a.num_tiles > blockIdx.x ? (int)ceil_div(a.num_tiles - blockIdx.x, gridDim.x) : 0;
+
+    if (warp >= wCtlWarp0) {
+        // ------------------------------------------------------------ control warpgroup
+        const int t = (warp - wCtlWarp0) * 32 + lane;  // tile row (index producer, epilogue)
+        const int ew = warp - wCtlWarp0;               // TMEM lane quadrant
+        const float binv = a.binv[0];
+        auto issue_mma = [&](int i, int h) {
+            constexpr uint32_t idesc = idesc_f16(kTile, L::BN, SPLIT ? 0 : 1);
+            const int b = i & 1;
+            mbar_wait(a_full + h, (uint32_t)(i & 1));
+            if (h == 0 && i >= 2) mbar_wait(acc_free + b, (uint32_t)(((i >> 1) + 1) & 1));
+            tc_fence_after();
+            const uint32_t d = tmem_base + (uint32_t)((b * 2 + h) * 128);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const int tt = ks >> 1, kk = ks & 1;
+                const uint32_t ko = (uint32_t)((32 * h + 16 * kk) * 2);
+                const uint32_t ao = (uint32_t)tt * (kTile * 128) + ko, bo = (uint32_t)tt * (L::BN * 128) + ko;
+                mma_f16(d, desc_sw128(A_hi + ao), desc_sw128(Bimg + bo), idesc, ks > 0 ? 1u : 0u);
+                if (SPLIT) mma_f16(d, desc_sw128(A_lo + ao), desc_sw128(Bimg + bo), idesc, 1u);
+            }
+            mma_commit(mma_done + h);
+            if (h == 1) mma_commit(acc_full + b);
+        };
+        auto epilogue = [&](int i) {
+            const int b = i & 1;
+            mbar_wait_sleep(acc_full + b, (uint32_t)((i >> 1) & 1));
+            tc_fence_after();
+            const int64_t p = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + t;
+            const float s0 = exp2i(rs[(b * 2 + 0) * kTile + t]) * binv;
+            const float s1 = exp2i(rs[(b * 2 + 1) * kTile + t]) * binv;
+            const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(b * 256);
+            float *orow = a.out + p * 64;
+#pragma unroll 1
+            for (int c0 = 0; c0 < 64; c0 += 16) {
+                float x0[16], x1[16], d[16];
+                tmem_ld16(tb + (uint32_t)c0, x0);
+                tmem_ld16(tb + 128u + (uint32_t)c0, x1);
+                if (SPLIT) {
+                    tmem_ld16(tb + 64u + (uint32_t)c0, d);
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) x0[c] += d[c];
+                    tmem_ld16(tb + 192u + (uint32_t)c0, d);
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) x1[c] += d[c];
+                }
+                if (p < a.total) {
+                    float o[16];
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) o[c] = fmaf(x1[c], s1, x0[c] * s0);
+                    stg256(orow + c0, o);
+                    stg256(orow + c0 + 8, o + 8);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_free + b);
+        };
+        auto produce = [&](int i) {  // entries of tile i (one thread per row)
+            const int64_t p = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + t;
+            const bool v = p < a.total;
+            int4 n0 = make_int4(0, 0, 0, 0), n1 = n0;
+            int32_t base = 0;
+            float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+            if (v) {
+                n0 = ldg_nc4i(a.nbr + p * kK);
+                n1 = ldg_nc4i(a.nbr + p * kK + 4);
+                c0 = __ldg(a.loc + p * 3 + 0);
+                c1 = __ldg(a.loc + p * 3 + 1);
+                c2 = __ldg(a.loc + p * 3 + 2);
+                if (p >= a.n) base = (int32_t)((p / a.n) * a.n);
+            }
+            int32_t js[kK] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+            float q0[kK], q1[kK], q2[kK];
+#pragma unroll
+            for (int s2 = 0; s2 < kK; ++s2) {
+                js[s2] = v ? base + js[s2] : 0;
+                q0[s2] = v ? __ldg(a.loc + (int64_t)js[s2] * 3 + 0) : 0.f;
+                q1[s2] = v ? __ldg(a.loc + (int64_t)js[s2] * 3 + 1) : 0.f;
+                q2[s2] = v ? __ldg(a.loc + (int64_t)js[s2] * 3 + 2) : 0.f;
+            }
+            const int st = i & 1;
+            if (i >= 2) mbar_wait_sleep(e_empty + st, (uint32_t)(((i >> 1) + 1) & 1));
+            const uint32_t es = E0 + (uint32_t)(st * L::E_STAGE);
+#pragma unroll
+            for (int s2 = 0; s2 < kK; ++s2)
+                sts128f(es + (uint32_t)((s2 * kTile + t) * 16), __int_as_float(js[s2]), c0 - q0[s2], c1 - q1[s2], c2 - q2[s2]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(e_full + st);
+        };
+        if (T > 0) produce(0);
+        for (int i = 0; i < T; ++i) {
+            if (i + 1 < T) produce(i + 1);
+            if (warp == wCtlWarp0) {
+                if (lane == 0) issue_mma(i, 0);
+                __syncwarp();
+            }
+            if (i >= 1) epilogue(i - 1);
+            if (warp == wCtlWarp0) {
+                if (lane == 0) issue_mma(i, 1);
+                __syncwarp();
+            }
+        }
+        if (T > 0) epilogue(T - 1);
+    } else {
+        // ------------------------------------------------------------ gather warps
+        // warp w: rows 8w .. 8w+7 of every tile, channel half h = 0 then 1.  Lane (pt, cl):
+        // point row 8w + {0,4,1,5,2,6,3,7}[pt] (each quarter-warp's two rows store to disjoint
+        // chunk sets), channels 32h + 8cl .. +7.
+        const int pt = lane >> 2, cl = lane & 3;
+        const int row = 8 * warp + ((pt & 1) << 2) + (pt >> 1);
+        float v[4][8];
+        auto load4 = [&](int i, int h, int b0) {
+            const uint32_t es = E0 + (uint32_t)((i & 1) * L::E_STAGE + row * 16);
+            const float *src = a.feat + 32 * h + 8 * cl;
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+                const int32_t j = lds32(es + (uint32_t)((b0 + s2) * kTile * 16));
+                ldg_nc8(src + (int64_t)j * 64, v[s2]);
+            }
+        };
+        // x[t][c]: 4 components x 8 channels as float2 pairs
+        float2 x[4][4];
+        auto fma4 = [&](int i, int b0) {
+            const uint32_t es = E0 + (uint32_t)((i & 1) * L::E_STAGE + row * 16);
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2) {
+                const float4 e = lds128f(es + (uint32_t)((b0 + s2) * kTile * 16));
+                const float2 w0 = make_float2(e.y, e.y), w1 = make_float2(e.z, e.z), w2 = make_float2(e.w, e.w);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const float2 f = make_float2(v[s2][2 * c], v[s2][2 * c + 1]);
+                    x[0][c] = ffma2(f, w0, x[0][c]);
+                    x[1][c] = ffma2(f, w1, x[1][c]);
+                    x[2][c] = ffma2(f, w2, x[2][c]);
+                    x[3][c] = fadd2(x[3][c], f);
+                }
+            }
+        };
+        if (T > 0) {
+            mbar_wait(e_full + 0, 0u);
+            load4(0, 0, 0);
+        }
+        for (int i = 0; i < T; ++i) {
+            const int64_t lim = a.total - ((int64_t)blockIdx.x + (int64_t)i * gridDim.x) * kTile;
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                for (int tt = 0; tt < 4; ++tt)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) x[tt][c] = make_float2(0.f, 0.f);
+                fma4(i, 0);
+                load4(i, h, 4);
+                fma4(i, 4);
+                if (h == 1) {  // E(i) no longer read by this warp
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(e_empty + (i & 1));
+                }
+                // first batch of the next item
+                if (h == 0) {
+                    load4(i, 1, 0);
+                } else if (i + 1 < T) {
+                    mbar_wait(e_full + ((i + 1) & 1), (uint32_t)(((i + 1) >> 1) & 1));
+                    load4(i + 1, 0, 0);
+                }
+                // ---- scale, split, A-operand row
+                int e = 0;
+                float sc = 1.f;
+                if (SPLIT) {
+                    float m = 0.f;
+#pragma unroll
+                    for (int tt = 0; tt < 4; ++tt)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) m = fmaxf(m, fmaxf(fabsf(x[tt][c].x), fabsf(x[tt][c].y)));
+                    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+                    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+                    e = scale_exp(m);
+                    sc = exp2i(-e);
+                }
+                if ((int64_t)row >= lim) sc = 0.f;
+                if (i >= 1) mbar_wait(mma_done + h, (uint32_t)((i - 1) & 1));
+                if (h == 0 && i >= 2) mbar_wait(acc_free + (i & 1), (uint32_t)(((i >> 1) + 1) & 1));
+                // k = t*64 + 32h + 8cl .. +7: 16 bytes = chunk (4h + cl) of the row
+                const uint32_t rb = (uint32_t)(row >> 3) * 1024u + (uint32_t)(row & 7) * 128u +
+                                    ((uint32_t)(((4 * h + cl) ^ (row & 7))) << 4);
+#pragma unroll
+                for (int tt = 0; tt < 4; ++tt) {
+                    uint32_t hv[4], lv[4] = {0, 0, 0, 0};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        if (SPLIT) hv[c] = split2(x[tt][c], sc, lv[c]);
+                        else hv[c] = bf16x2(x[tt][c]);
+                    }
+                    const uint32_t off = (uint32_t)tt * (kTile * 128) + rb;
+                    sts128u(A_hi + off, hv[0], hv[1], hv[2], hv[3]);
+                    if (SPLIT) sts128u(A_lo + off, lv[0], lv[1], lv[2], lv[3]);
+                }
+                if (cl == 0) sts8(rs_s + (uint32_t)(((i & 1) * 2 + h) * kTile + row), e);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(a_full + h);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == wCtlWarp0) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 512);
+    }
+}
+
 }  // namespace fast
 
 // forward for c_in = c_out = 64, k = 8, d = 3 (the bench / C3 / C4 shape)
@@ -479,7 +757,28 @@ int tc_fast_forward(bool split, int64_t total, int64_t n, const float *feat, con
         a.trace = trace;
     }
     prof_begin("tc_forward", st);
-    if (split) {
+    static int narrow = -1;
+    if (narrow < 0) {
+        const char *e = getenv("FC_FWD_NARROW");
+        narrow = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (!narrow) {
+        if (split) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(tc_fwd64w_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdL<true>::SMEM_ALLOC);
+                attr = true;
+            }
+            tc_fwd64w_kernel<true><<<grid, wThreads, FwdL<true>::SMEM_ALLOC, st>>>(a);
+        } else {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(tc_fwd64w_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdL<false>::SMEM_ALLOC);
+                attr = true;
+            }
+            tc_fwd64w_kernel<false><<<grid, wThreads, FwdL<false>::SMEM_ALLOC, st>>>(a);
+        }
+    } else if (split) {
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(tc_fwd64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdL<true>::SMEM_ALLOC);
