@@ -39,6 +39,11 @@ constexpr int dWarps = 24;
 constexpr int dThreads = dWarps * 32;
 constexpr int dChunk = 16;     // points per chunk (= gather warps)
 constexpr int dK = 8;
+// register split (setmaxnreg): control warps (index, epilogue) give registers to the gather
+// warps, which hold a point's 8 rows and their offsets across the load latency;
+// 8 x 32 x kCtlRegs + 16 x 32 x kGatherRegs <= 768 x 80 (the launch allocation)
+constexpr int kCtlRegs = 64;
+constexpr int kGatherRegs = 88;
 
 struct DtL {
     static constexpr int XST = dChunk * 256 * 4;       // one tf32 X chunk image (16 KB)
@@ -170,6 +175,7 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
 
     if (warp >= dEpiWarp0) {
         // ------------------------------------------------------------ MMA issue + Z epilogue
+        setmaxnreg_dec<kCtlRegs>();
         // TMEM: d_theta D columns 0..255 (lanes: c' hi 0..63, c' lo 64..127), Z 256..447
         const int ew = warp - dEpiWarp0;
         const int row = ew * 32 + lane;
@@ -283,6 +289,7 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
         }
     } else if (warp >= dIdxWarp0) {
         // ------------------------------------------------------------ index producers
+        setmaxnreg_dec<kCtlRegs>();
         const int t = (warp - dIdxWarp0) * 32 + lane;
         struct Nb {
             int32_t j[dK];
@@ -350,9 +357,11 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
     } else {
         // ------------------------------------------------------------ gather warps
         // chunk c of tile i: warp w owns point 16c + w (tile row); lane owns channels 2L, 2L+1
+        setmaxnreg_inc<kGatherRegs>();
         const int cc = 2 * lane;
         const float *fsrc = a.feat + cc;
         float2 v[dK];
+        float dx[dK], dy[dK], dz[dK];  // offsets l_p - l_j of the rows in v
         float2 gn;  // upstream row of the point whose rows are in v
         auto issue_loads = [&](int i, int c) {
             if (c == 0) DT_CLK(0, mbar_wait(e_full + (i & 1), (uint32_t)((i >> 1) & 1)));
@@ -361,7 +370,11 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
             const uint32_t es = E0 + (uint32_t)((i & 1) * L::E_STAGE + row * 16);
             int32_t j[dK];
 #pragma unroll
-            for (int s2 = 0; s2 < dK; ++s2) j[s2] = lds32(es + (uint32_t)(s2 * kTile * 16));
+            for (int s2 = 0; s2 < dK; ++s2) {
+                const float4 e = lds128f(es + (uint32_t)(s2 * kTile * 16));
+                j[s2] = __float_as_int(e.x);
+                dx[s2] = e.y, dy[s2] = e.z, dz[s2] = e.w;
+            }
 #pragma unroll
             for (int s2 = 0; s2 < dK; ++s2) v[s2] = ldg_nc2(fsrc + (int64_t)j[s2] * 64);
             gn = p < a.total ? ldg_nc2(a.g + p * 64 + cc) : make_float2(0.f, 0.f);
@@ -384,15 +397,13 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
                 const int row = dChunk * c + warp;
                 const int64_t p = tile0 + row;
                 const bool pv = p < a.total;
-                const uint32_t es = E0 + (uint32_t)((i & 1) * L::E_STAGE + row * 16);
                 // moments: m[t] = (channel 2L, 2L+1) of component t
                 float2 m0 = make_float2(0.f, 0.f), m1 = m0, m2 = m0, m3 = m0;
 #pragma unroll
                 for (int s2 = 0; s2 < dK; ++s2) {
-                    const float4 e = lds128f(es + (uint32_t)(s2 * kTile * 16));
-                    m0 = ffma2(v[s2], make_float2(e.y, e.y), m0);
-                    m1 = ffma2(v[s2], make_float2(e.z, e.z), m1);
-                    m2 = ffma2(v[s2], make_float2(e.w, e.w), m2);
+                    m0 = ffma2(v[s2], make_float2(dx[s2], dx[s2]), m0);
+                    m1 = ffma2(v[s2], make_float2(dy[s2], dy[s2]), m1);
+                    m2 = ffma2(v[s2], make_float2(dz[s2], dz[s2]), m2);
                     m3 = fadd2(m3, v[s2]);
                 }
                 const float2 gv = gn;

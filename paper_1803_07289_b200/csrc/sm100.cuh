@@ -131,6 +131,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// warpgroup-wide register reallocation (all 4 warps of an aligned warpgroup execute it)
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 // Byte offset of element (row, k) of a K-major SW128 tile of 16-bit elements whose
 // K-blocks (64 elements = 128 B wide) are stacked `rows*128` bytes apart.
 __host__ __device__ __forceinline__ uint32_t sw128_offset(int row, int k, int rows) {
