@@ -389,8 +389,11 @@ def run_e2e(args, torch, _ops, feat, pos, nbr, g, theta, theta_b, n, k, world, d
     # Copies overlap where the data dependencies allow: the inputs of the forward go first on
     # a copy stream, the upstream gradient follows it while the forward runs, and the
     # forward's output returns to the host (D2H) while the upstream gradient arrives (H2D).
+    # The reverse-neighbourhood build validates the indices (host-synchronising, like the
+    # reference's range check), so it runs on its own stream: the host waits for this step's
+    # neighbour table only, not for the previous step's result copies queued on the main stream.
     main = torch.cuda.current_stream()
-    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    s_in, s_out, s_csr = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
 
     def one():
         with torch.cuda.stream(s_in):  # (no wait on main: overlaps the previous step's D2H)
@@ -402,8 +405,14 @@ def run_e2e(args, torch, _ops, feat, pos, nbr, g, theta, theta_b, n, k, world, d
             ev_g.record(s_in)
         for t in (f, p, nb, th, tb, gg):
             t.record_stream(main)
+        nb.record_stream(s_csr)
+        with torch.cuda.stream(s_csr):
+            s_csr.wait_event(ev_in)
+            csr = _ops.csr_build(nb, 1, n)
+        for t in csr:
+            t.record_stream(main)
+        main.wait_stream(s_csr)
         main.wait_event(ev_in)
-        csr = _ops.csr_build(nb, 1, n)
         out = _ops.conv_forward(f, p, nb, th, tb, 1, n, args.mode)
         with torch.cuda.stream(s_out):
             s_out.wait_stream(main)
@@ -434,7 +443,8 @@ def run_e2e(args, torch, _ops, feat, pos, nbr, g, theta, theta_b, n, k, world, d
             "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3), "steps": steps,
             "path": "C ABI (fc_csr_build + fc_conv_forward + fc_conv_backward), pinned host fp32 buffers; "
                     "forward-input H2D (overlapping the previous step's result D2H), then upstream-gradient H2D "
-                    "overlapped with the forward and its output D2H"}
+                    "overlapped with the forward and its output D2H; the index-validating reverse-CSR build "
+                    "on a side stream"}
 
 
 def run_reference(args, world, rank):

@@ -12,7 +12,8 @@ import os
 from . import errors
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libflexconv_b200.so")
+# FC_LIB_PATH: A/B timing of an alternative build (scripts/*_probe.py); defaults to the in-tree library
+LIB_PATH = os.environ.get("FC_LIB_PATH") or os.path.join(HERE, "libflexconv_b200.so")
 
 FC_F32, FC_F64 = 0, 1
 MODE_AUTO, MODE_SIMT, MODE_TC_SPLIT, MODE_TC_BF16 = 0, 1, 2, 3
