@@ -115,6 +115,11 @@ __device__ __forceinline__ void sts64u(uint32_t addr, uint32_t a, uint32_t b) {
 __device__ __forceinline__ void sts32u(uint32_t addr, uint32_t a) {
     asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(a) : "memory");
 }
+__device__ __forceinline__ void ldg_nc8f(const float *p, float (&v)[8]) {
+    asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(p));
+}
 __device__ __forceinline__ float2 ldg_nc2(const float *p) {
     float2 v;
     asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
@@ -203,8 +208,7 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
             tmem_ld8(tb + 128u, z2);
             float gv[8];
             if (pz < a.total) {
-                const float4 x = ldg_nc4(a.g + pz * 64 + 8 * s), y = ldg_nc4(a.g + pz * 64 + 8 * s + 4);
-                gv[0] = x.x, gv[1] = x.y, gv[2] = x.z, gv[3] = x.w, gv[4] = y.x, gv[5] = y.y, gv[6] = y.z, gv[7] = y.w;
+                ldg_nc8f(a.g + pz * 64 + 8 * s, gv);  // own row: one 32-byte load (one line touch)
             } else {
 #pragma unroll
                 for (int q = 0; q < 8; ++q) gv[q] = 0.f;

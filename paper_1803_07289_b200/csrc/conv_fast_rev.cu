@@ -220,11 +220,18 @@ __global__ void __launch_bounds__(rThreads, 1) tc_rev64_kernel(RevArgs a) {
                 float nb0 = 0.f, nb1 = 0.f, nb2 = 0.f;
 #pragma unroll 1
                 for (int c0 = 0; c0 < 64; c0 += 16) {
-                    float f[16];
+                    // own row, 32 bytes per lane per load (LDG.256): one line touch per 8 channels
+                    float f[16], f8[8];
+                    if (pv) {
+                        ldg_nc8r(a.feat + p * 64 + c0, f8);
 #pragma unroll
-                    for (int q = 0; q < 16; q += 4) {
-                        const float4 x = pv ? ldg_nc4(a.feat + p * 64 + c0 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-                        f[q] = x.x, f[q + 1] = x.y, f[q + 2] = x.z, f[q + 3] = x.w;
+                        for (int q = 0; q < 8; ++q) f[q] = f8[q];
+                        ldg_nc8r(a.feat + p * 64 + c0 + 8, f8);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) f[8 + q] = f8[q];
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) f[q] = 0.f;
                     }
 #pragma unroll
                     for (int tt = 0; tt < 3; ++tt) {
@@ -694,11 +701,18 @@ __global__ void __launch_bounds__(wrThreads, 1) tc_rev64w_kernel(RevArgs a) {
                 float nb0 = 0.f, nb1 = 0.f, nb2 = 0.f;
 #pragma unroll 1
                 for (int c0 = 0; c0 < 64; c0 += 16) {
-                    float f[16];
+                    // own row, 32 bytes per lane per load (LDG.256): one line touch per 8 channels
+                    float f[16], f8[8];
+                    if (pv) {
+                        ldg_nc8r(a.feat + p * 64 + c0, f8);
 #pragma unroll
-                    for (int q = 0; q < 16; q += 4) {
-                        const float4 x = pv ? ldg_nc4(a.feat + p * 64 + c0 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-                        f[q] = x.x, f[q + 1] = x.y, f[q + 2] = x.z, f[q + 3] = x.w;
+                        for (int q = 0; q < 8; ++q) f[q] = f8[q];
+                        ldg_nc8r(a.feat + p * 64 + c0 + 8, f8);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) f[8 + q] = f8[q];
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) f[q] = 0.f;
                     }
 #pragma unroll
                     for (int tt = 0; tt < 3; ++tt) {
