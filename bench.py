@@ -98,6 +98,21 @@ def ncu_traffic(name):
     return d.get("kernels", {}).get(name, {}).get("dram_bytes_per_point")
 
 
+def ncu_datapipe(name):
+    """The kernel's L1 data-pipe budget (profiles/ncu_datapipe.json, written by
+    scripts/ncu_datapipe.py from an ncu --set full capture of this workload), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_datapipe.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    k = d.get("kernels", {}).get(name)
+    if not k:
+        return None
+    return {"l1_data_pipe_frac": k["l1_data_pipe_frac"], "lsu_wavefronts_per_point": k["lsu_wavefronts_per_point"],
+            "tc_smem_wavefronts_per_point": k["tc_smem_wavefronts_per_point"]}
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
@@ -323,6 +338,9 @@ def main():
         kernels[name] = {"ms": round(ms, 4), "bytes_per_point": b,
                          "GBps": round(b * n / ms / 1e6, 1) if b else None,
                          "frac": round(b * n / ms / 1e6 / hbm, 4) if b else None}
+        dp = ncu_datapipe(name)
+        if dp:  # the binding on-chip limit (ncu), beside the HBM roofline
+            kernels[name]["limiter"] = dict(dp, source="profiles/ncu_datapipe.json")
     dom = max(kern, key=kern.get) if kern else None
     if dom is not None and kernel_bytes_per_point(dom, c, c, d, k):
         dom_b, dom_ms = kernel_bytes_per_point(dom, c, c, d, k), kern[dom]

@@ -20,11 +20,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def bench_name(kernel: str):
-    if "tc_fwd64_kernel" in kernel:
+    if "tc_fwd64_kernel" in kernel or "tc_fwd64w_kernel" in kernel:
         return "tc_forward"
     if "tc_dt64_kernel" in kernel:
         return "tc_dtheta"
-    m = re.search(r"tc_rev64_kernel<(?:\(bool\))?(\w+), (?:\(bool\))?(\w+)>", kernel)
+    m = re.search(r"tc_rev64w?_kernel<(?:\(bool\))?(\w+), (?:\(bool\))?(\w+)>", kernel)
     if m:
         return "tc_reverse_dloc" if m.group(2) in ("1", "true") else "tc_reverse"
     m = re.search(r"tc_gmc_kernel<\(?int\)?(\d+), \(?int\)?(\d+), \(?bool\)?(\d), \(?bool\)?(\d), \(?int\)?(\d+), \(?bool\)?(\d)>", kernel)
@@ -46,14 +46,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=7_000_000)
     ap.add_argument("--mode", default="auto")
+    ap.add_argument("--csv", default=None, help="parse an existing ncu CSV instead of running ncu")
     args = ap.parse_args()
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    log = os.path.join(ROOT, "gpurun_out", "ncu_traffic.csv")
+    log = args.csv or os.path.join(ROOT, "gpurun_out", "ncu_traffic.csv")
     cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
            "--clock-control", "none", "-k", "regex:tc_|gmc|dtheta|fwd64|rev64|dt64", "--csv", "--log-file", log,
            sys.executable, os.path.join(ROOT, "bench.py"), "--n", str(args.n), "--steps", "1", "--warmup", "1",
            "--no-cpu", "--no-e2e", "--mode", args.mode]
-    subprocess.run(cmd, check=True, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+    if not args.csv:
+        subprocess.run(cmd, check=True, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
     rows = list(csv.reader(open(log)))
     hdr = next(r for r in rows if r and r[0] == "ID")
     ik, im, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
