@@ -157,6 +157,12 @@ int fc_knn(int dtype, int64_t batch, int64_t n, int d, int k, const void *points
 int fc_spatial_order(int dtype, int64_t n, int d, const void *points, int32_t *order,
                      void *stream);
 
+/* Inverse density of the IDISS sampler: phi[i] = sum over neighbour row i of |l_i - l_j|
+ * (sampling.py:33-48), fp64 in the reference's numpy evaluation order (bitwise equal).
+ * points [n, d] fp64, neighbors [n, k] int32 (k <= 128), phi [n] fp64. */
+int fc_inverse_density(int64_t n, int d, int k, const double *points, const int32_t *neighbors,
+                       double *phi, void *stream);
+
 /* ---- row movement used by the pooling stage (flexops.py:168-203) --------------------- */
 /* out[r] = in[sel[r]] -- downsample_gather (flexops.py:168-175). */
 int fc_gather_rows(int dtype, int64_t rows_out, int c, const void *in, const int32_t *sel,

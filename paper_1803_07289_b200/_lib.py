@@ -50,6 +50,7 @@ SIGNATURES = {
     "fc_pool_backward_record": [_I, _I64, _I64, _I, _P, _P, _P, _P, _P],
     "fc_knn": [_I, _I64, _I64, _I, _I, _P, _P, _I, _P],
     "fc_spatial_order": [_I, _I64, _I, _P, _P, _P],
+    "fc_inverse_density": [_I64, _I, _I, _P, _P, _P, _P],
     "fc_gather_rows": [_I, _I64, _I, _P, _P, _P, _P],
     "fc_scatter_rows": [_I, _I64, _I64, _I, _P, _P, _P, _P],
     "fc_indices_to_i32": [_P, _P, _I64, _I64, _P, _P],

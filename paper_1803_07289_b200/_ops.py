@@ -170,6 +170,16 @@ def spatial_order(points):
     return order
 
 
+def inverse_density(points, nbr):
+    """phi [n] fp64 of the IDISS sampler (fc_inverse_density)."""
+    points = _need(points, "points", torch.float64)
+    nbr = _need(nbr, "neighbors", torch.int32)
+    n, d = points.shape
+    phi = torch.empty(n, dtype=torch.float64, device=points.device)
+    _lib.call("fc_inverse_density", n, d, nbr.shape[1], _p(points), _p(nbr), _p(phi), _stream(points))
+    return phi
+
+
 def gather_rows(x, sel):
     x = _need(x, "features")
     sel = _need(sel, "selection", torch.int32, x.device)

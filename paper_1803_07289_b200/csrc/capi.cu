@@ -131,6 +131,8 @@ template <typename PT>
 int launch_knn(int64_t batch, int64_t n, int d, int k, const PT *pts, int32_t *out, int algo, cudaStream_t st);
 template <typename PT>
 int launch_spatial_order(int64_t n, int d, const PT *pts, int32_t *order, cudaStream_t st);
+int launch_inverse_density(int64_t n, int d, int k, const double *pts, const int32_t *nbr, double *phi,
+                           cudaStream_t st);
 
 }  // namespace fc
 
@@ -395,6 +397,13 @@ int fc_spatial_order(int dtype, int64_t n, int d, const void *points, int32_t *o
     cudaStream_t st = ST(stream);
     if (dtype == FC_F32) return launch_spatial_order<float>(n, d, (const float *)points, order, st);
     return launch_spatial_order<double>(n, d, (const double *)points, order, st);
+}
+
+int fc_inverse_density(int64_t n, int d, int k, const double *points, const int32_t *neighbors, double *phi,
+                       void *stream) {
+    if (n < 1) return set_error(FC_ERR_EMPTY, "no points");
+    if (d < 1 || k < 1) return set_error(FC_ERR_SHAPE, "d and k must be >= 1");
+    return launch_inverse_density(n, d, k, points, neighbors, phi, ST(stream));
 }
 
 int fc_gather_rows(int dtype, int64_t rows_out, int c, const void *in, const int32_t *sel, void *out, void *stream) {

@@ -442,6 +442,50 @@ int launch_spatial_order(int64_t n, int d, const PT *pts, int32_t *order, cudaSt
     return check_launch("spatial_order");
 }
 
+// ---- inverse density (sampling.py:33-48): phi[i] = sum_j |l_i - l_j| over the neighbour
+// row, in the reference's numpy order: per pair ((0 + dx^2) + dy^2) + ..., sqrt, then the
+// row sum as numpy's pairwise reduction (n < 8: sequential from 0; 8 <= n <= 128: eight
+// running partials combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the tail).
+// Plain IEEE fp64 mul/add/sqrt (no FMA contraction): bitwise equal to the reference.
+__device__ __forceinline__ double pair_dist(const double *__restrict__ pts, int d, int64_t i, int64_t j) {
+    double s = 0.0;
+    for (int t = 0; t < d; ++t) {
+        const double df = __dsub_rn(pts[i * d + t], pts[j * d + t]);
+        s = __dadd_rn(s, __dmul_rn(df, df));
+    }
+    return __dsqrt_rn(s);
+}
+__global__ void inverse_density_kernel(int64_t n, int d, int k, const double *__restrict__ pts,
+                                       const int32_t *__restrict__ nbr, double *__restrict__ phi) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t *row = nbr + i * k;
+        double res;
+        if (k < 8) {
+            res = 0.0;
+            for (int q = 0; q < k; ++q) res = __dadd_rn(res, pair_dist(pts, d, i, row[q]));
+        } else {
+            double r[8];
+            for (int q = 0; q < 8; ++q) r[q] = pair_dist(pts, d, i, row[q]);
+            int q = 8;
+            for (; q + 8 <= k; q += 8)
+                for (int u = 0; u < 8; ++u) r[u] = __dadd_rn(r[u], pair_dist(pts, d, i, row[q + u]));
+            res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                            __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+            for (; q < k; ++q) res = __dadd_rn(res, pair_dist(pts, d, i, row[q]));
+        }
+        phi[i] = res;
+    }
+}
+
+int launch_inverse_density(int64_t n, int d, int k, const double *pts, const int32_t *nbr, double *phi,
+                           cudaStream_t st) {
+    if (k > 128) return set_error(FC_ERR_UNSUPPORTED, "inverse density: k > 128 (numpy pairwise blocks)");
+    const int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)num_sms() * 8);
+    inverse_density_kernel<<<grid, 256, 0, st>>>(n, d, k, pts, nbr, phi);
+    count_launch();
+    return check_launch("inverse_density");
+}
+
 template int launch_knn<float>(int64_t, int64_t, int, int, const float *, int32_t *, int, cudaStream_t);
 template int launch_knn<double>(int64_t, int64_t, int, int, const double *, int32_t *, int, cudaStream_t);
 template int launch_spatial_order<float>(int64_t, int, const float *, int32_t *, cudaStream_t);
