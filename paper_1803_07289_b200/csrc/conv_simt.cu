@@ -321,9 +321,30 @@ void launch_pack(int cin, int d, int cout, const T *theta, const T *theta_b, T *
 }
 
 template <typename T, int DP, bool REV>
+int launch_wide_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, const T *rows, const T *loc,
+                       const int32_t *nbr, Csr csr, const T *w, T *out, cudaStream_t st);
+template <typename T, int DP>
+int launch_dtheta_slice_dp(int64_t total, int64_t n, int cin, int k, int cout, const T *feat, const T *loc,
+                           const int32_t *nbr, const T *g, T *d_theta, T *d_theta_b, cudaStream_t st);
+
+// FC_NO_WIDE=1: keep the per-warp kernels below (A/B timing of conv_wide.cu)
+static bool wide_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("FC_NO_WIDE");
+        v = (e && e[0] == '1') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+template <typename T, int DP, bool REV>
 static int launch_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, const T *rows,
                          const T *loc, const int32_t *nbr, Csr csr, const T *w, T *out,
                          const T *feat, const T *theta, const T *centre, T *dloc, cudaStream_t st) {
+    if (dloc == nullptr && wide_enabled()) {  // conv_wide.cu: same sums, same order, CTA-tiled
+        const int rc = launch_wide_gmc_dp<T, DP, REV>(total, n, gc, k, cout, rows, loc, nbr, csr, w, out, st);
+        if (rc != FC_ERR_UNSUPPORTED) return rc;
+    }
     const int ktot = gc * (DP + 1);
     const size_t per_point = (size_t)ktot * sizeof(T);
     int ppw = 4;
@@ -396,6 +417,10 @@ template <typename T, int DP>
 static int launch_dtheta_dp(int64_t total, int64_t n, int cin, int k, int cout, const T *feat,
                             const T *loc, const int32_t *nbr, const T *g, T *d_theta,
                             T *d_theta_b, cudaStream_t st) {
+    if (wide_enabled()) {  // conv_wide.cu: one gather per 16-channel slice
+        const int rc = launch_dtheta_slice_dp<T, DP>(total, n, cin, k, cout, feat, loc, nbr, g, d_theta, d_theta_b, st);
+        if (rc != FC_ERR_UNSUPPORTED) return rc;
+    }
     constexpr int RPT = 8;
     const int ktot = cin * (DP + 1);
     const int64_t E = (int64_t)cout * ktot;
@@ -437,6 +462,7 @@ int launch_dtheta_reduce(int chunks, int cin, int d, int cout, const T *partial,
     return check_launch("dtheta_reduce_kernel");
 }
 template int launch_dtheta_reduce<float>(int, int, int, int, const float *, float *, float *, cudaStream_t);
+template int launch_dtheta_reduce<double>(int, int, int, int, const double *, double *, double *, cudaStream_t);
 
 #define FC_INST(T)                                                                                   \
     template void launch_pack<T>(int, int, int, const T *, const T *, T *, T *, cudaStream_t);      \

@@ -85,6 +85,17 @@ class FlexConvParams:
         if not finite:
             raise NonFiniteError("parameters contain NaN or Inf")
 
+    @classmethod
+    def _checked_views(cls, theta: torch.Tensor, theta_b: torch.Tensor) -> "FlexConvParams":
+        """Views into a parameter vector whose finiteness the caller has already checked
+        once for the whole vector (network.LayerGraph.forward): the shape checks of
+        __post_init__ without a per-layer device->host sync."""
+        self = cls.__new__(cls)
+        self.theta, self.theta_b = theta, theta_b
+        if theta.ndim != 3 or theta_b.ndim != 2 or tuple(theta.shape[:2]) != tuple(theta_b.shape):
+            raise ShapeMismatchError("theta must be C_out x C_in x d, theta_b C_out x C_in")
+        return self
+
     @property
     def c_out(self) -> int:
         return int(self.theta.shape[0])

@@ -21,7 +21,7 @@ import torch
 
 from . import _ops
 from .core import PointCloud, Rng, validate_cloud
-from .errors import ConfigInvalidError, ShapeMismatchError
+from .errors import ConfigInvalidError, IndexOutOfRangeError, ShapeMismatchError
 from .neighborhood import DEFAULT_LEAF_SIZE, NeighborIndex, build_kdtree, knn_query
 
 
@@ -82,6 +82,7 @@ class HierarchyLevel:
     cloud: PointCloud
     neighbors: NeighborIndex
     selection: np.ndarray | None
+    parent_n: int | None = None  # size of the level the selection indexes
     _dev: dict = field(default_factory=dict, repr=False)
 
     def device(self, dtype=torch.float64, device=None) -> dict:
@@ -95,6 +96,10 @@ class HierarchyLevel:
                    "table": self.neighbors.device_table(device, self.cloud.n)}
             if self.selection is not None:
                 hit["selection"] = torch.from_numpy(np.asarray(self.selection, dtype=np.int64)).to(device)
+                sel32, bad = _ops.narrow_indices(hit["selection"], self.parent_n if self.parent_n is not None else 2 ** 31 - 1)
+                if hit["selection"].numel() and int(bad.item()):
+                    raise IndexOutOfRangeError("selection index out of [0, n_parent)")
+                hit["selection32"] = sel32
             self._dev[key] = hit
         return hit
 
@@ -144,5 +149,6 @@ def build_hierarchy(cloud: PointCloud, k: int, factor: int, depth: int, rng: Rng
         else:
             selection = random_sample(parent.cloud.n, m, level_rng)
         sub = PointCloud(parent.cloud.locations[selection], parent.cloud.features[selection])
-        levels.append(HierarchyLevel(sub, _level_neighbors(sub.locations, k, num_threads, leaf_size), selection))
+        levels.append(HierarchyLevel(sub, _level_neighbors(sub.locations, k, num_threads, leaf_size), selection,
+                                     parent.cloud.n))
     return ResolutionHierarchy(levels, k=k, factor=factor, mode=mode)

@@ -1,0 +1,122 @@
+"""GPU parity of the wide-channel CUDA-core engines (conv_wide.cu: wide_gmc_kernel and
+dtheta_slice_kernel) -- the shapes the tensor-core kernels do not cover: the U-Net's
+128 -> 128 and 256 -> 256 levels, the classifier's 64 -> 128, odd channel counts and d != 3.
+
+Oracle: oracle/flexconv_oracle.c (pinned bitwise to the reference's _native kernels).
+Tolerances as tests/test_gpu_parity.py: fp64 forward bitwise (same operations, same order);
+fp64 backward / deconv 1e-12 relative; fp32 forward / deconv / d_features allclose(1e-4, 1e-5);
+fp32 N-long reductions (d_theta, d_theta_b, d_locations) with the stated floor + norm 1e-5.
+"""
+
+import numpy as np
+import pytest
+
+from paper_1803_07289_b200.core import synthetic_layer
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [  # (n, k, c_in, c_out, d)
+    (700, 8, 128, 128, 3),
+    (300, 8, 256, 256, 3),
+    (500, 16, 64, 128, 3),
+    (333, 7, 40, 72, 3),
+    (257, 5, 24, 200, 2),
+    (129, 6, 17, 33, 5),
+]
+
+
+def _case(shape, seed=11):
+    from oracle import oracle
+
+    n, k, cin, cout, d = shape
+    loc, feat, th, tb, up = synthetic_layer(seed, cin + cout, n, d, cin, cout)
+    nbr = oracle.knn_brute(loc, k)
+    return loc, feat, th, tb, up, nbr
+
+
+def _t(a, dtype):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda().to(dtype)
+
+
+def _np(t):
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def _red_close(got, ref, name):
+    floor = 1e-5 + 1e-6 * float(np.abs(ref).max())
+    np.testing.assert_allclose(got, ref, rtol=1e-4, atol=floor, err_msg=name)
+    assert np.linalg.norm(got - ref) <= 1e-5 * max(np.linalg.norm(ref), 1e-30), name
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_wide_forward_fp64_bitwise(fc, oracle_mod, shape):
+    loc, feat, th, tb, up, nbr = _case(shape)
+    got = fc.flex_conv_forward(feat, loc, fc.NeighborIndex(nbr), fc.FlexConvParams(th, tb))
+    np.testing.assert_array_equal(got, oracle_mod.conv_forward(feat, loc, nbr, th, tb))
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_wide_fp32_forward_backward_deconv(fc, oracle_mod, shape):
+    import torch
+
+    loc, feat, th, tb, up, nbr = _case(shape)
+    f32 = torch.float32
+    nb = fc.NeighborIndex(_t(nbr, torch.int64))
+    params = fc.FlexConvParams(_t(th, f32), _t(tb, f32))
+    out = fc.flex_conv_forward(_t(feat, f32), _t(loc, f32), nb, params)
+    np.testing.assert_allclose(_np(out), oracle_mod.conv_forward(feat, loc, nbr, th, tb), rtol=1e-4, atol=1e-5)
+    df, dth, dtb, dl = oracle_mod.conv_backward(up, feat, loc, nbr, th, tb)
+    for with_loc in (False, True):
+        gb = fc.flex_conv_backward(_t(up, f32), _t(feat, f32), _t(loc, f32), nb, params, with_locations=with_loc)
+        np.testing.assert_allclose(_np(gb.d_features), df, rtol=1e-4, atol=1e-5, err_msg="d_features")
+        _red_close(_np(gb.d_theta), dth, "d_theta")
+        _red_close(_np(gb.d_theta_b), dtb, "d_theta_b")
+        if with_loc:
+            _red_close(_np(gb.d_locations), dl, "d_locations")
+    y = fc.flex_deconv_forward(_t(up, f32), _t(loc, f32), nb, params)
+    np.testing.assert_allclose(_np(y), oracle_mod.deconv_forward(up, loc, nbr, th, tb), rtol=1e-4, atol=1e-5)
+
+
+@pytest.mark.parametrize("shape", SHAPES[:3])
+def test_wide_fp64_backward_and_deconv(fc, oracle_mod, shape):
+    loc, feat, th, tb, up, nbr = _case(shape)
+    nb = fc.NeighborIndex(nbr)
+    params = fc.FlexConvParams(th, tb)
+    gb = fc.flex_conv_backward(up, feat, loc, nb, params)
+    for got, ref in zip((gb.d_features, gb.d_theta, gb.d_theta_b, gb.d_locations),
+                        oracle_mod.conv_backward(up, feat, loc, nbr, th, tb)):
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12 * float(np.abs(ref).max()))
+    y = fc.flex_deconv_forward(up, loc, nb, params)
+    ref = oracle_mod.deconv_forward(up, loc, nbr, th, tb)
+    np.testing.assert_allclose(y, ref, rtol=1e-12, atol=1e-12 * float(np.abs(ref).max()))
+
+
+def test_wide_batched_and_deterministic(fc, oracle_mod):
+    """Batched clouds (cloud-local indices) through the [B, D, N] API; two runs bitwise equal."""
+    import torch
+
+    b, n, k, cin, cout = 3, 400, 8, 128, 128
+    g = np.random.default_rng(3)
+    loc = np.floor(g.random((b, n, 3)) * 2 ** 24) / 2 ** 24
+    feat = g.standard_normal((b, n, cin)).astype(np.float32).astype(np.float64)
+    th = (0.1 * g.standard_normal((cout, cin, 3))).astype(np.float32).astype(np.float64)
+    tb = (0.1 * g.standard_normal((cout, cin))).astype(np.float32).astype(np.float64)
+    pos = _t(loc, torch.float32).transpose(1, 2)
+    nbh = fc.knn(pos, k)
+    f = _t(feat, torch.float32).transpose(1, 2).requires_grad_(True)
+    theta = _t(th, torch.float32).requires_grad_(True)
+    theta_b = _t(tb, torch.float32).requires_grad_(True)
+    outs = []
+    for _ in range(2):
+        f.grad = theta.grad = theta_b.grad = None
+        out = fc.flex_conv(f, pos, nbh, theta, theta_b)
+        out.square().sum().backward()
+        outs.append([t.detach().clone() for t in (out, f.grad, theta.grad, theta_b.grad)])
+    for a, c in zip(*outs):
+        assert torch.equal(a, c)
+    for bi in range(b):
+        nbr = nbh.bkn[bi].t().cpu().numpy().astype(np.int64)
+        ref = oracle_mod.conv_forward(feat[bi], loc[bi], nbr, th, tb)
+        np.testing.assert_allclose(_np(outs[0][0][bi].t()), ref, rtol=1e-4, atol=1e-5)
