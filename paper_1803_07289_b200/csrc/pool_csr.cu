@@ -2,6 +2,8 @@
 // builder (a stable counting sort, no float atomics) and row gather/scatter.
 #include "fc_common.cuh"
 
+#include <initializer_list>
+
 namespace fc {
 
 static int grid_1d(int64_t items, int block = 256) {
@@ -63,6 +65,141 @@ __global__ void pool_bwd_kernel(int64_t total, int64_t n, int c, int k, const T 
         }
         df[idx] = acc;
     }
+}
+
+// ---------------------------------------------------------------- vectorised forms
+// A thread owns (point, V channels) with V = 16 / sizeof(T) (one 16-byte load per neighbour
+// row); the row's K indices are loaded first and up to 8 neighbour rows are in flight before
+// the first comparison.  Same comparisons in the same slot order as pool_fwd_kernel, same
+// additions in the same reverse-list order as pool_bwd_kernel -> identical results.
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+    using V = float4;
+    using I = int4;
+    static constexpr int N = 4;
+};
+template <>
+struct Vec16<double> {
+    using V = double2;
+    using I = int2;
+    static constexpr int N = 2;
+};
+
+template <typename T>
+__device__ __forceinline__ T vget(const typename Vec16<T>::V &v, int e) {
+    return reinterpret_cast<const T *>(&v)[e];
+}
+template <typename T>
+__device__ __forceinline__ int32_t iget(const typename Vec16<T>::I &v, int e) {
+    return reinterpret_cast<const int32_t *>(&v)[e];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    pool_fwd_vec_kernel(int64_t total, int64_t n, int c, int k, const T *__restrict__ feat,
+                        const int32_t *__restrict__ nbr, T *__restrict__ out, int32_t *__restrict__ argmax) {
+    using VT = typename Vec16<T>::V;
+    using IT = typename Vec16<T>::I;
+    constexpr int V = Vec16<T>::N;
+    const int cv = c / V;
+    const int64_t items = total * cv;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < items;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = idx / cv;
+        const int ch = (int)(idx - p * cv) * V;
+        const int64_t base = (p / n) * n;
+        const int32_t *row = nbr + p * k;
+        T bv[V];
+        int32_t bj[V];
+        for (int s0 = 0; s0 < k; s0 += 8) {
+            int32_t jj[8];
+            VT vv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) jj[u] = __ldg(row + min(s0 + u, k - 1));
+#pragma unroll
+            for (int u = 0; u < 8; ++u) vv[u] = __ldg(reinterpret_cast<const VT *>(feat + (base + jj[u]) * c + ch));
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int s = s0 + u;
+                if (s < k) {
+#pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        const T v = vget<T>(vv[u], e);
+                        if (s == 0 || v > bv[e] || (v == bv[e] && jj[u] < bj[e])) {
+                            bv[e] = v;
+                            bj[e] = jj[u];
+                        }
+                    }
+                }
+            }
+        }
+        VT o;
+        IT a;
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            reinterpret_cast<T *>(&o)[e] = bv[e];
+            reinterpret_cast<int32_t *>(&a)[e] = bj[e];
+        }
+        *reinterpret_cast<VT *>(out + p * c + ch) = o;
+        *reinterpret_cast<IT *>(argmax + p * c + ch) = a;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    pool_bwd_vec_kernel(int64_t total, int64_t n, int c, int k, const T *__restrict__ g,
+                        const int32_t *__restrict__ argmax, Csr csr, T *__restrict__ df) {
+    using VT = typename Vec16<T>::V;
+    using IT = typename Vec16<T>::I;
+    constexpr int V = Vec16<T>::N;
+    const int cv = c / V;
+    const int64_t items = total * cv;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < items;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = idx / cv;
+        const int ch = (int)(idx - j * cv) * V;
+        const int32_t jl = (int32_t)(j - (j / n) * n);
+        const int32_t q0 = __ldg(csr.off + j), q1 = __ldg(csr.off + j + 1);
+        T acc[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[e] = T(0);
+        int64_t prev = -1;
+        for (int32_t qb = q0; qb < q1; qb += 8) {
+            int64_t ii[8];
+            IT am[8];
+            VT gv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) ii[u] = (int64_t)__ldg(csr.ent + min(qb + u, q1 - 1)) / k;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                am[u] = __ldg(reinterpret_cast<const IT *>(argmax + ii[u] * c + ch));
+                gv[u] = __ldg(reinterpret_cast<const VT *>(g + ii[u] * c + ch));
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (qb + u < q1 && ii[u] != prev) {  // row i lists j twice: routed once
+                    prev = ii[u];
+#pragma unroll
+                    for (int e = 0; e < V; ++e)
+                        if (iget<T>(am[u], e) == jl) acc[e] = Ar<T>::add(acc[e], vget<T>(gv[u], e));
+                }
+            }
+        }
+        VT o;
+#pragma unroll
+        for (int e = 0; e < V; ++e) reinterpret_cast<T *>(&o)[e] = acc[e];
+        *reinterpret_cast<VT *>(df + j * c + ch) = o;
+    }
+}
+
+template <typename T>
+static bool vec16_ok(int c, std::initializer_list<const void *> ptrs) {
+    if (c % (16 / (int)sizeof(T)) != 0) return false;
+    for (const void *q : ptrs)
+        if (reinterpret_cast<uintptr_t>(q) % 16 != 0) return false;
+    return true;
 }
 
 // Record-only backward (flexops.py:154-165): buckets (row, channel) of the record.
@@ -279,14 +416,22 @@ __global__ void check_indices_kernel(const int32_t *__restrict__ in, int64_t cou
 template <typename T>
 int launch_pool_fwd(int64_t total, int64_t n, int c, int k, const T *feat, const int32_t *nbr,
                     T *out, int32_t *argmax, cudaStream_t st) {
-    pool_fwd_kernel<T><<<grid_1d(total * c), 256, 0, st>>>(total, n, c, k, feat, nbr, out, argmax);
+    if (vec16_ok<T>(c, {feat, out, argmax}))
+        pool_fwd_vec_kernel<T><<<grid_1d(total * (c / (16 / (int)sizeof(T)))), 256, 0, st>>>(total, n, c, k, feat, nbr,
+                                                                                          out, argmax);
+    else
+        pool_fwd_kernel<T><<<grid_1d(total * c), 256, 0, st>>>(total, n, c, k, feat, nbr, out, argmax);
     count_launch();
     return check_launch("pool_fwd_kernel");
 }
 template <typename T>
 int launch_pool_bwd(int64_t total, int64_t n, int c, int k, const T *g, const int32_t *argmax,
                     Csr csr, T *df, cudaStream_t st) {
-    pool_bwd_kernel<T><<<grid_1d(total * c), 256, 0, st>>>(total, n, c, k, g, argmax, csr, df);
+    if (vec16_ok<T>(c, {g, argmax, df}))
+        pool_bwd_vec_kernel<T><<<grid_1d(total * (c / (16 / (int)sizeof(T)))), 256, 0, st>>>(total, n, c, k, g, argmax,
+                                                                                          csr, df);
+    else
+        pool_bwd_kernel<T><<<grid_1d(total * c), 256, 0, st>>>(total, n, c, k, g, argmax, csr, df);
     count_launch();
     return check_launch("pool_bwd_kernel");
 }
