@@ -57,6 +57,39 @@ def fixed_order_allreduce(t: torch.Tensor, group=None) -> torch.Tensor:
     return acc.to(t.dtype)
 
 
+def ordered_allgather_sum(local: torch.Tensor, units: int, group=None) -> torch.Tensor:
+    """Sum of per-unit rows in GLOBAL unit order, whatever the world size.
+
+    `local` is [n_local, ...]: this rank's units, the block `shard_range(units, world, rank)`.
+    Every rank all-gathers the blocks (padded to the largest) and adds the rows one by one in
+    unit order, in `local`'s dtype -- the additions of the reference's sequential
+    accumulation loop (harness.py:589-595: grads += graph.backward(g) per scene), so the
+    result is bitwise identical for 1, 2, 4 or 8 ranks and to the single-process loop."""
+    import torch.distributed as dist
+
+    multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+    world = dist.get_world_size(group) if multi else 1
+    rank = dist.get_rank(group) if multi else 0
+    lo, hi = shard_range(units, world, rank)
+    if local.shape[0] != hi - lo:
+        raise ShapeMismatchError(f"rank {rank} holds {local.shape[0]} units, its shard is {hi - lo}")
+    if not multi:
+        blocks = [local]
+    else:
+        width = shard_range(units, world, 0)[1]  # the first block is the largest
+        pad = torch.zeros((width,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        pad[: local.shape[0]] = local
+        parts = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(parts, pad, group=group)
+        blocks = [parts[r][: shard_range(units, world, r)[1] - shard_range(units, world, r)[0]]
+                  for r in range(world)]
+    acc = torch.zeros(tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    for b in blocks:
+        for row in b:
+            acc += row
+    return acc
+
+
 # ---------------------------------------------------------------------------- transports
 class DistTransport:
     """Grouped point-to-point exchange over torch.distributed (one call per direction)."""

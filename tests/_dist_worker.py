@@ -76,6 +76,16 @@ def main():
     again = parallel.fixed_order_allreduce(parallel.sharded_backward_local(
         plan, t(up[lo:hi]), feat_l, loc_l, t(th), t(tb), comp)[1])
     res["allreduce_bitwise"] = bool(torch.equal(again, dth))
+    # batch-sharded gradient combination (network.train_step_batch): per-unit rows summed in
+    # global unit order must equal the single-process sequential loop bitwise
+    units = 5
+    rows = torch.from_numpy(np.random.default_rng(7).standard_normal((units, 33)) * 10.0 ** np.arange(-8, 25, 1))
+    lo_u, hi_u = parallel.shard_range(units, world, rank)
+    got = parallel.ordered_allgather_sum(rows[lo_u:hi_u].clone(), units)
+    seq = torch.zeros(33, dtype=torch.float64)
+    for r in rows:
+        seq += r
+    res["ordered_sum_bitwise"] = bool(torch.equal(got, seq))
     print("RESULT " + json.dumps(res), flush=True)
     dist.destroy_process_group()
 
