@@ -96,3 +96,7 @@ def synthetic_layer(seed: int, tag: int, n: int, d: int, c_in: int, c_out: int):
     theta_b = (g.standard_normal((c_out, c_in)) * 0.1).astype(np.float32).astype(np.float64)
     up = g.standard_normal((n, c_out)).astype(np.float32).astype(np.float64)
     return loc, feat, theta, theta_b, up
+
+
+# the reference keeps its file formats in these modules; same names here
+from .formats import read_cloud, write_cloud  # noqa: E402,F401  (core.py:148-219)

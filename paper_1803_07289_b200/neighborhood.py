@@ -195,3 +195,7 @@ def validate_neighbors(locations, neighbors: NeighborIndex) -> None:
         keys = list(zip(d2.tolist(), row[1:].tolist()))
         if keys != sorted(keys):
             raise IndexOutOfRangeError(f"row {i} not sorted by (distance, index)")
+
+
+# the reference keeps its file formats in these modules; same names here
+from .formats import read_neighbors, write_neighbors  # noqa: E402,F401  (neighborhood.py:211-252)

@@ -152,3 +152,7 @@ def build_hierarchy(cloud: PointCloud, k: int, factor: int, depth: int, rng: Rng
         levels.append(HierarchyLevel(sub, _level_neighbors(sub.locations, k, num_threads, leaf_size), selection,
                                      parent.cloud.n))
     return ResolutionHierarchy(levels, k=k, factor=factor, mode=mode)
+
+
+# the reference keeps its file formats in these modules; same names here
+from .formats import load_hierarchy, save_hierarchy  # noqa: E402,F401  (sampling.py:149-204)
