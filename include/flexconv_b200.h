@@ -172,6 +172,31 @@ int fc_gather_rows(int dtype, int64_t rows_out, int c, const void *in, const int
 int fc_scatter_rows(int dtype, int64_t rows_in, int64_t rows_out, int c, const void *in,
                     const int32_t *sel, void *out, void *stream);
 
+/* ---- fused downsample / upsample pooling (network.py:248-280 _PoolDown / _Upsample,
+ * flexops.py:168-203 downsample_gather / flex_upsample), one cloud, without the fine-level
+ * intermediates (the pooled map of every fine point, the zero-filled scattered map):
+ * fc_selection_owner     owner[0..n) = -1, then owner[sel[r]] = r (largest r on duplicate
+ *                        targets: scatter_to_fine's last-writer rule).
+ * fc_pool_select_forward out row r (of m) pools fine row p = rows ? rows[r] : r over its
+ *                        neighbours j = neighbors[p*k + s]; neighbour j's value is
+ *                        owner ? (owner[j] >= 0 ? features[owner[j]] : 0) : features[j];
+ *                        winners [m, c] = the fine index j, ties to the lower j (_native.pyx:151).
+ *                        PoolDown: rows = selection, owner = NULL.  Upsample: rows = NULL, owner = map.
+ * fc_pool_select_backward d_features row r (of m) is fine row j = rows ? rows[r] : r: the sum,
+ *                        over j's reverse entries (i, s) ascending (each i once), of
+ *                        upstream[q, ch] with q = owner ? owner[i] : i (none if q < 0) and
+ *                        winners[q, ch] == j -- flexops.flex_max_pool_backward's additions
+ *                        (_native.pyx:165-168) restricted to rows that can be non-zero.
+ *                        PoolDown: rows = NULL, owner = map.  Upsample: rows = selection, owner = NULL. */
+int fc_selection_owner(int64_t m, int64_t n, const int32_t *sel, int32_t *owner, void *stream);
+int fc_pool_select_forward(int dtype, int64_t m, int64_t n, int c, int k, const void *features,
+                           const int32_t *neighbors, const int32_t *rows, const int32_t *owner,
+                           void *out, int32_t *winners, void *stream);
+int fc_pool_select_backward(int dtype, int64_t m, int64_t n, int c, int k, const void *upstream,
+                            const int32_t *winners, const int32_t *rev_offsets,
+                            const int32_t *rev_entries, const int32_t *rows, const int32_t *owner,
+                            void *d_features, void *stream);
+
 /* ---- index plumbing --------------------------------------------------------------------
  * int64 -> int32 narrowing with a device-side range check: *bad (device int32) receives
  * the number of entries outside [0, hi) (the reference's idx.min()/max() scan,

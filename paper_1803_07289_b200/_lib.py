@@ -53,6 +53,9 @@ SIGNATURES = {
     "fc_inverse_density": [_I64, _I, _I, _P, _P, _P, _P],
     "fc_gather_rows": [_I, _I64, _I, _P, _P, _P, _P],
     "fc_scatter_rows": [_I, _I64, _I64, _I, _P, _P, _P, _P],
+    "fc_selection_owner": [_I64, _I64, _P, _P, _P],
+    "fc_pool_select_forward": [_I, _I64, _I64, _I, _I, _P, _P, _P, _P, _P, _P, _P],
+    "fc_pool_select_backward": [_I, _I64, _I64, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "fc_indices_to_i32": [_P, _P, _I64, _I64, _P, _P],
     "fc_check_indices": [_P, _I64, _I64, _P, _P],
 }

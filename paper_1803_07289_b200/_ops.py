@@ -197,6 +197,39 @@ def scatter_rows(x, sel, rows_out):
     return out
 
 
+def selection_owner(sel, n):
+    """owner [n] int32: owner[sel[r]] = r (largest r on duplicates), -1 elsewhere."""
+    sel = _need(sel, "selection", torch.int32)
+    owner = torch.empty(n, dtype=torch.int32, device=sel.device)
+    _lib.call("fc_selection_owner", sel.numel(), n, _p(sel), _p(owner), _stream(sel))
+    return owner
+
+
+def pool_select_forward(feat, nbr, m, rows=None, owner=None):
+    """Fused PoolDown (rows = selection) / Upsample (owner = selection_owner) pooling: m output
+    rows, winners = fine neighbour indices (fc_pool_select_forward)."""
+    feat = _need(feat, "features")
+    nbr = _need(nbr, "neighbors", torch.int32, feat.device)
+    n, k = nbr.shape
+    c = feat.shape[1]
+    out = torch.empty(m, c, dtype=feat.dtype, device=feat.device)
+    win = torch.empty(m, c, dtype=torch.int32, device=feat.device)
+    _lib.call("fc_pool_select_forward", _dtype(feat), m, n, c, k, _p(feat), _p(nbr), _p(rows), _p(owner), _p(out),
+              _p(win), _stream(feat))
+    return out, win
+
+
+def pool_select_backward(g, winners, csr, m, n, k, rows=None, owner=None):
+    """Backward of pool_select_forward: d_features for m fine rows (all n, or rows=selection)."""
+    g = _need(g, "upstream")
+    winners = _need(winners, "winners", torch.int32, g.device)
+    off, ent = csr
+    df = torch.empty(m, g.shape[1], dtype=g.dtype, device=g.device)
+    _lib.call("fc_pool_select_backward", _dtype(g), m, n, g.shape[1], k, _p(g), _p(winners), _p(off), _p(ent),
+              _p(rows), _p(owner), _p(df), _stream(g))
+    return df
+
+
 def narrow_indices(idx64, hi):
     """int64 -> int32 with the reference's [0, hi) range check; returns (idx32, bad_count)."""
     idx64 = _need(idx64, "indices", torch.int64)

@@ -123,6 +123,13 @@ int launch_gather_rows(int64_t rows_out, int c, const T *in, const int32_t *sel,
 template <typename T>
 int launch_scatter_rows(int64_t rows_in, int64_t rows_out, int c, const T *in, const int32_t *sel, T *out,
                         cudaStream_t st);
+int launch_selection_owner(int64_t m, int64_t n, const int32_t *sel, int32_t *owner, cudaStream_t st);
+template <typename T>
+int launch_pool_select_fwd(int64_t m, int c, int k, const T *feat, const int32_t *nbr, const int32_t *rows,
+                           const int32_t *owner, T *out, int32_t *winners, cudaStream_t st);
+template <typename T>
+int launch_pool_select_bwd(int64_t m, int c, int k, const T *g, const int32_t *winners, Csr csr,
+                           const int32_t *rows, const int32_t *owner, T *df, cudaStream_t st);
 int launch_narrow_indices(const int64_t *in, int32_t *out, int64_t count, int64_t hi, int32_t *bad,
                           cudaStream_t st);
 int launch_check_indices(const int32_t *in, int64_t count, int64_t hi, int32_t *bad, cudaStream_t st);
@@ -421,6 +428,44 @@ int fc_scatter_rows(int dtype, int64_t rows_in, int64_t rows_out, int c, const v
     cudaStream_t st = ST(stream);
     if (dtype == FC_F32) return launch_scatter_rows<float>(rows_in, rows_out, c, (const float *)in, sel, (float *)out, st);
     return launch_scatter_rows<double>(rows_in, rows_out, c, (const double *)in, sel, (double *)out, st);
+}
+
+int fc_selection_owner(int64_t m, int64_t n, const int32_t *sel, int32_t *owner, void *stream) {
+    if (n < 1) return set_error(FC_ERR_EMPTY, "empty fine level");
+    if (m < 0) return set_error(FC_ERR_SHAPE, "negative selection size");
+    return launch_selection_owner(m, n, sel, owner, ST(stream));
+}
+
+int fc_pool_select_forward(int dtype, int64_t m, int64_t n, int c, int k, const void *features,
+                           const int32_t *neighbors, const int32_t *rows, const int32_t *owner, void *out,
+                           int32_t *winners, void *stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (n < 1) return set_error(FC_ERR_EMPTY, "empty fine level");
+    if (c < 1 || k < 1 || m < 0) return set_error(FC_ERR_SHAPE, "c and k must be >= 1, m >= 0");
+    if (m == 0) return FC_OK;
+    cudaStream_t st = ST(stream);
+    if (dtype == FC_F32)
+        return launch_pool_select_fwd<float>(m, c, k, (const float *)features, neighbors, rows, owner, (float *)out,
+                                             winners, st);
+    return launch_pool_select_fwd<double>(m, c, k, (const double *)features, neighbors, rows, owner, (double *)out,
+                                          winners, st);
+}
+
+int fc_pool_select_backward(int dtype, int64_t m, int64_t n, int c, int k, const void *upstream,
+                            const int32_t *winners, const int32_t *rev_offsets, const int32_t *rev_entries,
+                            const int32_t *rows, const int32_t *owner, void *d_features, void *stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (n < 1) return set_error(FC_ERR_EMPTY, "empty fine level");
+    if (c < 1 || k < 1 || m < 0) return set_error(FC_ERR_SHAPE, "c and k must be >= 1, m >= 0");
+    if (!rev_offsets || !rev_entries) return set_error(FC_ERR_CONFIG, "pool backward needs the reverse neighbourhood");
+    if (m == 0) return FC_OK;
+    cudaStream_t st = ST(stream);
+    const Csr csr{rev_offsets, rev_entries};
+    if (dtype == FC_F32)
+        return launch_pool_select_bwd<float>(m, c, k, (const float *)upstream, winners, csr, rows, owner,
+                                             (float *)d_features, st);
+    return launch_pool_select_bwd<double>(m, c, k, (const double *)upstream, winners, csr, rows, owner,
+                                          (double *)d_features, st);
 }
 
 int fc_indices_to_i32(const int64_t *in, int32_t *out, int64_t count, int64_t hi, int32_t *bad, void *stream) {

@@ -202,6 +202,131 @@ static bool vec16_ok(int c, std::initializer_list<const void *> ptrs) {
     return true;
 }
 
+// ---------------------------------------------------------------- fused down/upsample pooling
+// (network.py:248-280, flexops.py:168-203) without the fine-level intermediate tensors.
+// V channels per thread (V = 16 / sizeof(T) when the rows are 16-byte aligned, else 1).
+template <typename T, int V>
+__device__ __forceinline__ void ldvec(const T *p, T (&v)[V]) {
+    if constexpr (V == 1) {
+        v[0] = __ldg(p);
+    } else {
+        using VT = typename Vec16<T>::V;
+        const VT x = __ldg(reinterpret_cast<const VT *>(p));
+#pragma unroll
+        for (int e = 0; e < V; ++e) v[e] = reinterpret_cast<const T *>(&x)[e];
+    }
+}
+
+// out row r pools fine row p = rows ? rows[r] : r; neighbour j's value is
+// owner ? (owner[j] >= 0 ? feat[owner[j]] : 0) : feat[j]; winners hold the fine index j.
+template <typename T, int V>
+__global__ void __launch_bounds__(256)
+    pool_select_fwd_kernel(int64_t m, int c, int k, const T *__restrict__ feat, const int32_t *__restrict__ nbr,
+                           const int32_t *__restrict__ rows, const int32_t *__restrict__ owner, T *__restrict__ out,
+                           int32_t *__restrict__ winners) {
+    const int cv = c / V;
+    const int64_t items = m * cv;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < items;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = idx / cv;
+        const int ch = (int)(idx - r * cv) * V;
+        const int64_t p = rows ? (int64_t)__ldg(rows + r) : r;
+        const int32_t *row = nbr + p * k;
+        T bv[V];
+        int32_t bj[V];
+        for (int s0 = 0; s0 < k; s0 += 8) {
+            int32_t jj[8];
+            T vv[8][V];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) jj[u] = __ldg(row + min(s0 + u, k - 1));
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t src = owner ? (int64_t)__ldg(owner + jj[u]) : (int64_t)jj[u];
+                if (src >= 0) {
+                    ldvec<T, V>(feat + src * c + ch, vv[u]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < V; ++e) vv[u][e] = T(0);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int sl = s0 + u;
+                if (sl < k) {
+#pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        const T v = vv[u][e];
+                        if (sl == 0 || v > bv[e] || (v == bv[e] && jj[u] < bj[e])) {
+                            bv[e] = v;
+                            bj[e] = jj[u];
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            out[r * c + ch + e] = bv[e];
+            winners[r * c + ch + e] = bj[e];
+        }
+    }
+}
+
+// out row r is fine row j = rows ? rows[r] : r; sums upstream[q, ch] over j's reverse entries
+// (i, s) ascending, each i once, with q = owner ? owner[i] : i (skipped when < 0) and
+// winners[q, ch] == j -- the additions of _native.pyx:165-168 restricted to the rows that can
+// be non-zero (dropping additions of +0.0 cannot change an accumulator that starts at +0.0).
+template <typename T, int V>
+__global__ void __launch_bounds__(256)
+    pool_select_bwd_kernel(int64_t m, int c, int k, const T *__restrict__ g, const int32_t *__restrict__ winners,
+                           Csr csr, const int32_t *__restrict__ rows, const int32_t *__restrict__ owner,
+                           T *__restrict__ df) {
+    const int cv = c / V;
+    const int64_t items = m * cv;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < items;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = idx / cv;
+        const int ch = (int)(idx - r * cv) * V;
+        const int32_t j = rows ? __ldg(rows + r) : (int32_t)r;
+        const int32_t q0 = __ldg(csr.off + j), q1 = __ldg(csr.off + j + 1);
+        T acc[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[e] = T(0);
+        int64_t prev = -1;
+        for (int32_t qb = q0; qb < q1; qb += 8) {
+            int64_t ii[8], src[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                ii[u] = (int64_t)__ldg(csr.ent + min(qb + u, q1 - 1)) / k;
+                src[u] = owner ? (int64_t)__ldg(owner + ii[u]) : ii[u];
+            }
+            int32_t am[8][V];
+            T gv[8][V];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (src[u] >= 0) {
+#pragma unroll
+                    for (int e = 0; e < V; ++e) am[u][e] = __ldg(winners + src[u] * c + ch + e);
+                    ldvec<T, V>(g + src[u] * c + ch, gv[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (qb + u < q1 && ii[u] != prev) {
+                    prev = ii[u];
+                    if (src[u] >= 0) {
+#pragma unroll
+                        for (int e = 0; e < V; ++e)
+                            if (am[u][e] == j) acc[e] = Ar<T>::add(acc[e], gv[u][e]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < V; ++e) df[r * c + ch + e] = acc[e];
+    }
+}
+
 // Record-only backward (flexops.py:154-165): buckets (row, channel) of the record.
 template <typename T>
 __global__ void pool_bwd_record_kernel(int64_t n_rows, int c, const T *__restrict__ g,
@@ -463,6 +588,40 @@ int launch_scatter_rows(int64_t rows_in, int64_t rows_out, int c, const T *in, c
     return check_launch("scatter_rows");
 }
 
+int launch_selection_owner(int64_t m, int64_t n, const int32_t *sel, int32_t *owner, cudaStream_t st) {
+    fill_i32_kernel<<<grid_1d(n), 256, 0, st>>>(owner, n, -1);
+    count_launch();
+    if (m > 0) {
+        scatter_owner_kernel<<<grid_1d(m), 256, 0, st>>>(m, sel, owner);
+        count_launch();
+    }
+    return check_launch("selection_owner");
+}
+
+template <typename T>
+int launch_pool_select_fwd(int64_t m, int c, int k, const T *feat, const int32_t *nbr, const int32_t *rows,
+                           const int32_t *owner, T *out, int32_t *winners, cudaStream_t st) {
+    constexpr int V = 16 / sizeof(T);
+    if (vec16_ok<T>(c, {feat, out, winners}))
+        pool_select_fwd_kernel<T, V><<<grid_1d(m * (c / V)), 256, 0, st>>>(m, c, k, feat, nbr, rows, owner, out, winners);
+    else
+        pool_select_fwd_kernel<T, 1><<<grid_1d(m * c), 256, 0, st>>>(m, c, k, feat, nbr, rows, owner, out, winners);
+    count_launch();
+    return check_launch("pool_select_fwd_kernel");
+}
+
+template <typename T>
+int launch_pool_select_bwd(int64_t m, int c, int k, const T *g, const int32_t *winners, Csr csr,
+                           const int32_t *rows, const int32_t *owner, T *df, cudaStream_t st) {
+    constexpr int V = 16 / sizeof(T);
+    if (vec16_ok<T>(c, {g, winners, df}))
+        pool_select_bwd_kernel<T, V><<<grid_1d(m * (c / V)), 256, 0, st>>>(m, c, k, g, winners, csr, rows, owner, df);
+    else
+        pool_select_bwd_kernel<T, 1><<<grid_1d(m * c), 256, 0, st>>>(m, c, k, g, winners, csr, rows, owner, df);
+    count_launch();
+    return check_launch("pool_select_bwd_kernel");
+}
+
 int launch_narrow_indices(const int64_t *in, int32_t *out, int64_t count, int64_t hi, int32_t *bad,
                           cudaStream_t st) {
     narrow_indices_kernel<<<grid_1d(count), 256, 0, st>>>(in, out, count, hi, bad);
@@ -485,7 +644,12 @@ int launch_check_indices(const int32_t *in, int64_t count, int64_t hi, int32_t *
     template int launch_gather_rows<T>(int64_t, int, const T *, const int32_t *, T *,            \
                                        cudaStream_t);                                            \
     template int launch_scatter_rows<T>(int64_t, int64_t, int, const T *, const int32_t *, T *,  \
-                                        cudaStream_t);
+                                        cudaStream_t);                                           \
+    template int launch_pool_select_fwd<T>(int64_t, int, int, const T *, const int32_t *,        \
+                                           const int32_t *, const int32_t *, T *, int32_t *,     \
+                                           cudaStream_t);                                        \
+    template int launch_pool_select_bwd<T>(int64_t, int, int, const T *, const int32_t *, Csr,   \
+                                           const int32_t *, const int32_t *, T *, cudaStream_t);
 FC_POOL_INST(float)
 FC_POOL_INST(double)
 

@@ -253,8 +253,19 @@ def flex_upsample(features_coarse, selection, fine_neighbors: NeighborIndex, n: 
                   num_threads: int = 1, with_record: bool = False):
     """Scatter coarse features to the fine level (zero fill) and flex-max-pool there
     (flexops.py:193-203)."""
-    full = scatter_to_fine(features_coarse, selection, n)
-    pooled, record = flex_max_pool(full, fine_neighbors, num_threads)
+    features_coarse = _f64_2d(features_coarse, "features_coarse")
+    kd = _Kind(features_coarse)
+    nsel = int(np.asarray(selection).shape[0]) if not isinstance(selection, torch.Tensor) else int(selection.shape[0])
+    if nsel != int(features_coarse.shape[0]):
+        raise ShapeMismatchError(f"{features_coarse.shape[0]} coarse rows but {nsel} selections")
+    if fine_neighbors.n != int(n):
+        raise ShapeMismatchError(f"neighbor index has {fine_neighbors.n} rows for {n} points")
+    s32 = _selection(selection, kd, int(n))
+    table = fine_neighbors.device_table(kd.device, int(n))
+    # fused scatter + pool (fc_pool_select_forward): no zero-filled fine-level intermediate
+    pooled, record = _ops.pool_select_forward(kd.dev(features_coarse), table, int(n),
+                                              owner=_ops.selection_owner(s32, int(n)))
+    pooled, record = kd.back(pooled), kd.back(record.to(torch.int64))
     return (pooled, record) if with_record else pooled
 
 
