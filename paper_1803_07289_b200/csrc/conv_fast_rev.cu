@@ -89,6 +89,17 @@ __device__ __forceinline__ void ldg_nc8r(const float *p, float (&v)[8]) {
                  : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
                  : "l"(p));
 }
+// predicated form: lanes whose slot is past their list's end issue no load (no L1 wavefronts)
+// and read zeros
+__device__ __forceinline__ void ldg_nc8r_if(const float *p, float (&v)[8], bool ok) {
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.b32 q, %9, 0;\n"
+        " mov.b32 %0, 0;\n mov.b32 %1, 0;\n mov.b32 %2, 0;\n mov.b32 %3, 0;\n"
+        " mov.b32 %4, 0;\n mov.b32 %5, 0;\n mov.b32 %6, 0;\n mov.b32 %7, 0;\n"
+        " @q ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n}"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+        : "l"(p), "r"((int)ok));
+}
 __device__ __forceinline__ void sts128r(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
@@ -887,8 +898,9 @@ __global__ void __launch_bounds__(wrThreads, 1) tc_rev64w_kernel(RevArgs a) {
 #pragma unroll
             for (int s2 = 0; s2 < 4; ++s2) {
                 const int sl = b0 + s2;
-                const int32_t j = lds32(sl < it.cnt ? it.eb + (uint32_t)(sl * 16) : it.ez);
-                ldg_nc8r(src + (int64_t)j * 64, v[s2]);
+                const bool ok = sl < it.cnt;
+                const int32_t j = lds32(ok ? it.eb + (uint32_t)(sl * 16) : it.ez);
+                ldg_nc8r_if(src + (int64_t)j * 64, v[s2], ok);
             }
         };
         auto fma4w = [&](const ItemW &it, int b0) {
