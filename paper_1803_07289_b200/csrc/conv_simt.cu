@@ -322,7 +322,8 @@ void launch_pack(int cin, int d, int cout, const T *theta, const T *theta_b, T *
 
 template <typename T, int DP, bool REV>
 int launch_wide_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, const T *rows, const T *loc,
-                       const int32_t *nbr, Csr csr, const T *w, T *out, cudaStream_t st);
+                       const int32_t *nbr, Csr csr, const T *w, T *out, const T *feat, const T *theta,
+                       const T *centre, T *dloc, cudaStream_t st);
 template <typename T, int DP>
 int launch_dtheta_slice_dp(int64_t total, int64_t n, int cin, int k, int cout, const T *feat, const T *loc,
                            const int32_t *nbr, const T *g, T *d_theta, T *d_theta_b, cudaStream_t st);
@@ -341,8 +342,9 @@ template <typename T, int DP, bool REV>
 static int launch_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, const T *rows,
                          const T *loc, const int32_t *nbr, Csr csr, const T *w, T *out,
                          const T *feat, const T *theta, const T *centre, T *dloc, cudaStream_t st) {
-    if (dloc == nullptr && wide_enabled()) {  // conv_wide.cu: same sums, same order, CTA-tiled
-        const int rc = launch_wide_gmc_dp<T, DP, REV>(total, n, gc, k, cout, rows, loc, nbr, csr, w, out, st);
+    if (wide_enabled()) {  // conv_wide.cu: same sums, same order, CTA-tiled (+ the d_loc neighbour term)
+        const int rc = launch_wide_gmc_dp<T, DP, REV>(total, n, gc, k, cout, rows, loc, nbr, csr, w, out, feat, theta,
+                                                      centre, dloc, st);
         if (rc != FC_ERR_UNSUPPORTED) return rc;
     }
     const int ktot = gc * (DP + 1);

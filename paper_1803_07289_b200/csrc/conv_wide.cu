@@ -153,11 +153,23 @@ __device__ __forceinline__ void wide_moments(const T *__restrict__ rows, int gc,
 }
 
 // out[p, cp] = sum_{c, t} w[(c*(DP+1)+t)*cout + cp] * M_p[c, t]   (w = forward or adjoint packing)
+// Neighbour role of the location gradient (REVERSE only; dloc == nullptr: skipped):
+//   dloc[j, t] = centre[j, t] - sum_c f[j, c] sum_c' theta[c', c, t] Y_j[DP, c']
+// (the -dt terms of _native.pyx:121-127 regrouped per j; Y_j[DP, :] = the bias moment row,
+// already in shared memory).  w3 = theta repacked as [DP][gc][cout].
+template <typename T>
+struct WideDloc {
+    const T *w3;
+    const T *feat;    // [total, cout]
+    const T *centre;  // [total, DP]
+    T *dloc;          // [total, DP] or null
+};
+
 template <typename T, int DP, bool REVERSE, int PPL, int VEC>
 __global__ void __launch_bounds__(kWideThreads)
     wide_gmc_kernel(int64_t total, int64_t n, int gc, int k, int cout, const T *__restrict__ rows,
                     const T *__restrict__ loc, const int32_t *__restrict__ nbr, Csr csr, const T *__restrict__ w,
-                    T *__restrict__ out) {
+                    T *__restrict__ out, WideDloc<T> dl) {
     constexpr int P = 32 * PPL;
     constexpr int KC = kChunkCh * (DP + 1);
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -245,7 +257,92 @@ __global__ void __launch_bounds__(kWideThreads)
                 }
             }
         }
+        if (REVERSE && dl.dloc != nullptr) {
+            // U_t[p, c] = sum_c' Yb_p[c'] theta[c', c, t] with the same chunked, double-buffered
+            // weight staging as above (weights = theta_t, [gc][cout]); then each thread dots its
+            // 16 channels with f[p, :] and the 8 warps' partials are added in warp order.
+            T *red = wc + 2 * KC * kPassCp;  // [8 warps][DP][P]
+            const bool async3 = (cout * sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(dl.w3) % 16) == 0;
+            T part[PPL][DP > 0 ? DP : 1];
+#pragma unroll
+            for (int a = 0; a < PPL; ++a)
+#pragma unroll
+                for (int t = 0; t < DP; ++t) part[a][t] = T(0);
+            for (int pass = 0; pass < passes; ++pass) {
+                const int cpw = pass * kPassCp + warp * kGroup;
+#pragma unroll 1
+                for (int t = 0; t < DP; ++t) {
+                    const T *wt = dl.w3 + (int64_t)t * gc * cout;
+                    T acc[PPL][kGroup];
+#pragma unroll
+                    for (int a = 0; a < PPL; ++a)
+#pragma unroll
+                        for (int j = 0; j < kGroup; ++j) acc[a][j] = T(0);
+                    const int nchunks = (gc + kChunkCh - 1) / kChunkCh;
+                    stage_weights<T, 0>(wc, wt, 0, pass, gc, cout, async3);
+                    cp_async_commit();
+                    for (int ci = 0; ci < nchunks; ++ci) {
+                        const int c0 = ci * kChunkCh;
+                        if (ci + 1 < nchunks)
+                            stage_weights<T, 0>(wc + ((ci + 1) & 1) * KC * kPassCp, wt, c0 + kChunkCh, pass, gc, cout,
+                                                async3);
+                        cp_async_commit();
+                        cp_async_wait1();
+                        __syncthreads();
+                        const T *wcur = wc + (ci & 1) * KC * kPassCp;
+                        const int nch = min(kChunkCh, gc - c0);
+                        for (int cl = 0; cl < nch; ++cl) {
+                            const T *wrow = wcur + cl * kPassCp + warp * kGroup;
+                            T wv[kGroup];
+#pragma unroll
+                            for (int j = 0; j < kGroup; ++j) wv[j] = wrow[j];
+#pragma unroll
+                            for (int a = 0; a < PPL; ++a) {
+                                const T yb = xs[(lane + 32 * a) * S + DP * gc + c0 + cl];
+#pragma unroll
+                                for (int j = 0; j < kGroup; ++j) acc[a][j] = Ar<T>::madd(acc[a][j], wv[j], yb);
+                            }
+                        }
+                        __syncthreads();
+                    }
+#pragma unroll
+                    for (int a = 0; a < PPL; ++a) {
+                        const int64_t p = p0 + lane + 32 * a;
+                        if (p < total && cpw < cout) {
+                            const T *fr = dl.feat + p * cout + cpw;
+#pragma unroll
+                            for (int j = 0; j < kGroup; ++j)
+                                if (cpw + j < cout) part[a][t] = Ar<T>::madd(part[a][t], __ldg(fr + j), acc[a][j]);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < PPL; ++a)
+#pragma unroll
+                for (int t = 0; t < DP; ++t) red[(warp * DP + t) * P + lane + 32 * a] = part[a][t];
+            __syncthreads();
+            for (int e = threadIdx.x; e < P * DP; e += kWideThreads) {
+                const int pl = e / DP, t = e - (e / DP) * DP;
+                const int64_t p = p0 + pl;
+                if (p < total) {
+                    T sum = T(0);
+                    for (int w8 = 0; w8 < kWideThreads / 32; ++w8) sum = Ar<T>::add(sum, red[(w8 * DP + t) * P + pl]);
+                    dl.dloc[p * DP + t] = Ar<T>::sub(dl.centre[p * DP + t], sum);
+                }
+            }
+        }
         __syncthreads();  // xs is rewritten by the next tile's gathers
+    }
+}
+
+template <typename T>
+__global__ void pack_theta_t_kernel(int gc, int cout, int d, const T *__restrict__ theta, T *__restrict__ w3) {
+    const int64_t total = (int64_t)gc * cout * d;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int t = (int)(e % d);
+        const int64_t r = e / d;  // = cp * cout + c
+        w3[(int64_t)t * gc * cout + r] = theta[e];
     }
 }
 
@@ -365,7 +462,8 @@ template <typename T, int DP>
 size_t wide_smem(int gc, int ppl) {
     const size_t ktot = (size_t)gc * (DP + 1);
     const size_t xs = (size_t)32 * ppl * (ktot | 1);
-    return (xs * sizeof(T) + 16) + (size_t)2 * kChunkCh * (DP + 1) * kPassCp * sizeof(T);
+    return (xs * sizeof(T) + 16) + (size_t)2 * kChunkCh * (DP + 1) * kPassCp * sizeof(T) +
+           (size_t)(kWideThreads / 32) * DP * 32 * ppl * sizeof(T);  // + the d_loc reduction buffer
 }
 
 }  // namespace
@@ -374,7 +472,8 @@ size_t wide_smem(int gc, int ppl) {
 // moment tile does not fit in shared memory; the caller then uses gmc_kernel.
 template <typename T, int DP, bool REV>
 int launch_wide_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, const T *rows, const T *loc,
-                       const int32_t *nbr, Csr csr, const T *w, T *out, cudaStream_t st) {
+                       const int32_t *nbr, Csr csr, const T *w, T *out, const T *feat, const T *theta,
+                       const T *centre, T *dloc, cudaStream_t st) {
     constexpr size_t kMax = 200 * 1024, kTwoPerSm = 110 * 1024;
     // two points per lane for fp32 (32 FMAs per 6 shared loads) where two CTAs still fit per
     // SM (one CTA's gathers overlap the other's contraction); fp64 keeps one (register budget)
@@ -388,12 +487,22 @@ int launch_wide_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, const 
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * per_sm));
     constexpr int V = 16 / sizeof(T);
     const bool vec = gc % V == 0 && (reinterpret_cast<uintptr_t>(rows) % 16) == 0;
-    prof_begin(REV ? "simt_reverse" : "simt_forward", st);
+    WideDloc<T> dl{nullptr, feat, centre, dloc};
+    T *w3 = nullptr;
+    if (REV && dloc) {
+        w3 = (T *)scratch_alloc(sizeof(T) * (size_t)gc * cout * DP, st);
+        if (!w3) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+        const int64_t e = (int64_t)gc * cout * DP;
+        pack_theta_t_kernel<T><<<(unsigned)std::min<int64_t>(ceil_div(e, 256), 4096), 256, 0, st>>>(gc, cout, DP, theta, w3);
+        count_launch();
+        dl.w3 = w3;
+    }
+    prof_begin(REV ? (dloc ? "simt_reverse_dloc" : "simt_reverse") : "simt_forward", st);
 #define FC_WIDE_LAUNCH(PPLV, VECV)                                                                              \
     do {                                                                                                        \
         set_smem_attr(wide_gmc_kernel<T, DP, REV, PPLV, VECV>, smem);                                           \
         wide_gmc_kernel<T, DP, REV, PPLV, VECV><<<grid, kWideThreads, smem, st>>>(total, n, gc, k, cout, rows, loc, \
-                                                                                 nbr, csr, w, out);              \
+                                                                                 nbr, csr, w, out, dl);          \
     } while (0)
     if (sizeof(T) == 4 && ppl == 2) {
         if (vec) FC_WIDE_LAUNCH(2, V); else FC_WIDE_LAUNCH(2, 1);
@@ -403,6 +512,7 @@ int launch_wide_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, const 
 #undef FC_WIDE_LAUNCH
     prof_end(st);
     count_launch();
+    scratch_free(w3, st);
     return check_launch("wide_gmc_kernel");
 }
 
@@ -444,9 +554,11 @@ int launch_dtheta_slice_dp(int64_t total, int64_t n, int cin, int k, int cout, c
 
 #define FC_WIDE_INST(T, DP)                                                                                       \
     template int launch_wide_gmc_dp<T, DP, false>(int64_t, int64_t, int, int, int, const T *, const T *,       \
-                                                  const int32_t *, Csr, const T *, T *, cudaStream_t);         \
+                                                  const int32_t *, Csr, const T *, T *, const T *, const T *,  \
+                                                  const T *, T *, cudaStream_t);                               \
     template int launch_wide_gmc_dp<T, DP, true>(int64_t, int64_t, int, int, int, const T *, const T *,        \
-                                                 const int32_t *, Csr, const T *, T *, cudaStream_t);          \
+                                                 const int32_t *, Csr, const T *, T *, const T *, const T *,   \
+                                                 const T *, T *, cudaStream_t);                                \
     template int launch_dtheta_slice_dp<T, DP>(int64_t, int64_t, int, int, int, const T *, const T *,          \
                                                const int32_t *, const T *, T *, T *, cudaStream_t);
 #define FC_WIDE_INST_T(T) \
