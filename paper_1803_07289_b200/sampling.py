@@ -119,6 +119,54 @@ class ResolutionHierarchy:
         return [lv.cloud.n for lv in self.levels]
 
 
+def spatially_ordered(cloud: PointCloud, *per_point):
+    """Data preparation: the cloud's points (and any per-point arrays, e.g. labels) permuted
+    into cell order (ops.spatial_order).  Flex-convolution is permutation equivariant
+    (reference tests/test_flexops.py:263-276), and idiss_sample returns sorted indices, so
+    every level of a hierarchy built from the reordered cloud is spatially ordered too: the
+    neighbour rows of consecutive points then share cache lines (the gathers hit L1/L2)
+    instead of landing anywhere in the cloud.  Returns (cloud, *per_point, perm)."""
+    pos = torch.from_numpy(np.ascontiguousarray(cloud.locations)).to(_device(), torch.float64)
+    perm = _ops.spatial_order(pos).to(torch.int64).cpu().numpy()
+    out = [PointCloud(cloud.locations[perm], cloud.features[perm])]
+    out += [np.asarray(a)[perm] for a in per_point]
+    return (*out, perm)
+
+
+def concat_hierarchies(hierarchies: list[ResolutionHierarchy]) -> ResolutionHierarchy:
+    """Several scenes' hierarchies as ONE hierarchy of disjoint clouds: level t holds the
+    scenes' level-t points back to back, neighbour rows and selections shifted by each
+    scene's offset.  No neighbourhood crosses a scene, so every operator of the network
+    computes exactly the per-scene results; one launch then covers all scenes (used by
+    network.train_step_batch(fused=True) for a GPU's share of the batch)."""
+    if not hierarchies:
+        raise ConfigInvalidError("no hierarchies to concatenate")
+    h0 = hierarchies[0]
+    depth = h0.depth
+    if any(h.depth != depth or h.k != h0.k for h in hierarchies):
+        raise ShapeMismatchError("hierarchies must share depth and k")
+    levels = []
+    for t in range(depth + 1):
+        locs, feats, nbrs, sels = [], [], [], []
+        off = par_off = 0
+        for h in hierarchies:
+            lv = h.levels[t]
+            locs.append(lv.cloud.locations)
+            feats.append(lv.cloud.features)
+            idx = lv.neighbors.indices
+            idx = idx.cpu().numpy() if isinstance(idx, torch.Tensor) else np.asarray(idx)
+            nbrs.append(idx.astype(np.int64) + off)
+            if t:
+                sels.append(np.asarray(lv.selection, dtype=np.int64) + par_off)
+                par_off += h.levels[t - 1].cloud.n
+            off += lv.cloud.n
+        cloud = PointCloud(np.concatenate(locs), np.concatenate(feats))
+        selection = np.concatenate(sels) if t else None
+        levels.append(HierarchyLevel(cloud, NeighborIndex(np.concatenate(nbrs)), selection,
+                                     par_off if t else None))
+    return ResolutionHierarchy(levels, k=h0.k, factor=h0.factor, mode=h0.mode)
+
+
 def _level_neighbors(locations, k: int, num_threads: int, leaf_size: int) -> NeighborIndex:
     tree = build_kdtree(locations, leaf_size)
     return knn_query(tree, tree.points, min(k, locations.shape[0]), num_threads)
