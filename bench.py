@@ -397,9 +397,22 @@ def run_e2e(args, torch, _ops, feat, pos, nbr, g, theta, theta_b, n, k, world, d
     """Same metric through the C ABI with pinned HOST buffers: every step copies the inputs
     H2D, rebuilds the reverse neighbourhood, runs fwd + bwd and copies the results D2H."""
     dev = feat.device
-    host_in = [t.cpu().pin_memory() for t in (feat, pos, nbr, g, theta, theta_b)]
+    # pinned host buffers filled straight from the device (no pageable intermediate: at N
+    # ranks per box this is N x 7.6 GB of page-locked memory, not 2x that transiently)
     outs_shape = [(n, theta.shape[0]), (n, feat.shape[1]), tuple(theta.shape), tuple(theta_b.shape), (n, 3)]
-    host_out = [torch.empty(s, dtype=torch.float32).pin_memory() for s in outs_shape]
+    ok, err = 1, ""
+    try:
+        host_in = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t)
+                   for t in (feat, pos, nbr, g, theta, theta_b)]
+        host_out = [torch.empty(s, dtype=torch.float32, pin_memory=True) for s in outs_shape]
+    except (RuntimeError, MemoryError) as exc:  # e.g. page-locking failed on a small host
+        ok, err = 0, f"{type(exc).__name__}: {str(exc)[:200]}"
+    if world > 1:  # every rank takes the same branch (no rank left waiting in a collective)
+        flag = torch.tensor([ok], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        ok = int(flag.item())
+    if not ok:
+        return {"value": None, "unit": UNIT, "error": err or "pinned host buffers unavailable on another rank"}
     h2d = sum(t.numel() * t.element_size() for t in host_in)
     d2h = sum(t.numel() * t.element_size() for t in host_out)
     steps = max(1, min(args.steps, 5))
