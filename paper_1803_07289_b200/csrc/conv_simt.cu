@@ -328,6 +328,13 @@ template <typename T, int DP>
 int launch_dtheta_slice_dp(int64_t total, int64_t n, int cin, int k, int cout, const T *feat, const T *loc,
                            const int32_t *nbr, const T *g, T *d_theta, T *d_theta_b, cudaStream_t st);
 
+template <int DP, bool REV>
+int launch_gemm_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, const float *rows, const float *loc,
+                       const int32_t *nbr, Csr csr, const float *w, float *out, cudaStream_t st);
+template <int DP>
+int launch_gemm_dtheta_dp(int64_t total, int64_t n, int cin, int k, int cout, const float *feat, const float *loc,
+                          const int32_t *nbr, const float *g, float *d_theta, float *d_theta_b, cudaStream_t st);
+
 // FC_NO_WIDE=1: keep the per-warp kernels below (A/B timing of conv_wide.cu)
 static bool wide_enabled() {
     static int v = -1;
@@ -342,6 +349,13 @@ template <typename T, int DP, bool REV>
 static int launch_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, const T *rows,
                          const T *loc, const int32_t *nbr, Csr csr, const T *w, T *out,
                          const T *feat, const T *theta, const T *centre, T *dloc, cudaStream_t st) {
+    if constexpr (sizeof(T) == 4) {  // fp32, >= 96 gathered channels: moments + cuBLAS GEMM (conv_wide.cu)
+        if (dloc == nullptr && wide_enabled()) {
+            const int rc = launch_gemm_gmc_dp<DP, REV>(total, n, gc, k, cout, (const float *)rows, (const float *)loc,
+                                                       nbr, csr, (const float *)w, (float *)out, st);
+            if (rc != FC_ERR_UNSUPPORTED) return rc;
+        }
+    }
     if (wide_enabled()) {  // conv_wide.cu: same sums, same order, CTA-tiled (+ the d_loc neighbour term)
         const int rc = launch_wide_gmc_dp<T, DP, REV>(total, n, gc, k, cout, rows, loc, nbr, csr, w, out, feat, theta,
                                                       centre, dloc, st);
@@ -419,6 +433,13 @@ template <typename T, int DP>
 static int launch_dtheta_dp(int64_t total, int64_t n, int cin, int k, int cout, const T *feat,
                             const T *loc, const int32_t *nbr, const T *g, T *d_theta,
                             T *d_theta_b, cudaStream_t st) {
+    if constexpr (sizeof(T) == 4) {
+        if (wide_enabled()) {
+            const int rc = launch_gemm_dtheta_dp<DP>(total, n, cin, k, cout, (const float *)feat, (const float *)loc,
+                                                     nbr, (const float *)g, (float *)d_theta, (float *)d_theta_b, st);
+            if (rc != FC_ERR_UNSUPPORTED) return rc;
+        }
+    }
     if (wide_enabled()) {  // conv_wide.cu: one gather per 16-channel slice
         const int rc = launch_dtheta_slice_dp<T, DP>(total, n, cin, k, cout, feat, loc, nbr, g, d_theta, d_theta_b, st);
         if (rc != FC_ERR_UNSUPPORTED) return rc;

@@ -19,6 +19,10 @@
 //                   Partials per chunk are reduced in fixed order by dtheta_reduce_kernel.
 #include "fc_common.cuh"
 
+#include <cublas_v2.h>
+
+#include <cstdlib>
+
 namespace fc {
 
 template <typename T>
@@ -551,6 +555,190 @@ int launch_dtheta_slice_dp(int64_t total, int64_t n, int cin, int k, int cout, c
     }
     return FC_ERR_UNSUPPORTED;
 }
+
+// ---------------------------------------------------------------------------------------
+// fp32 wide channel counts as moments + library GEMM.  The contraction of the gathered
+// moments with the packed weights (and d_theta = G^T X) is a plain dense GEMM once the moment
+// rows X [points, ktot] are materialised; it goes to cuBLAS (FP32, no TF32: default math
+// mode), which runs it at several times the CTA-tiled FFMA rate.  The gather stays here.
+namespace {
+
+// X[p, c*(DP+1) + t] for points [p0, p0 + m): one warp per point, lanes over 4 channels,
+// 8 neighbour rows in flight, slot order per (c, t) (_native.pyx:52-59).
+template <int DP, bool REVERSE>
+__global__ void __launch_bounds__(256)
+    moments_rows_kernel(int64_t p0, int64_t m, int64_t n, int gc, int k, const float *__restrict__ rows,
+                        const float *__restrict__ loc, const int32_t *__restrict__ nbr, Csr csr,
+                        float *__restrict__ X) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int ktot = gc * (DP + 1);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < m; r += nw) {
+        const int64_t p = p0 + r;
+        const int64_t base = (p / n) * n;
+        float lp[DP];
+#pragma unroll
+        for (int t = 0; t < DP; ++t) lp[t] = loc[p * DP + t];
+        int64_t q0 = 0, q1 = k;
+        if (REVERSE) {
+            q0 = csr.off[p];
+            q1 = csr.off[p + 1];
+        }
+        float *xr = X + r * ktot;
+        for (int c0 = 0; c0 < gc; c0 += 128) {
+            const int c = c0 + lane * 4;
+            const bool ok = c < gc;
+            float acc[4][DP + 1];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+#pragma unroll
+                for (int t = 0; t <= DP; ++t) acc[e][t] = 0.f;
+            for (int64_t qb = q0; qb < q1; qb += 8) {
+                int64_t jj[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int64_t q = qb + u < q1 ? qb + u : q1 - 1;
+                    jj[u] = REVERSE ? (int64_t)csr.ent[q] / k : base + nbr[p * k + q];
+                }
+                float4 v[8];
+                float o[8][DP];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    v[u] = ok ? __ldg(reinterpret_cast<const float4 *>(rows + jj[u] * gc + c)) : make_float4(0, 0, 0, 0);
+#pragma unroll
+                    for (int t = 0; t < DP; ++t)
+                        o[u][t] = REVERSE ? loc[jj[u] * DP + t] - lp[t] : lp[t] - loc[jj[u] * DP + t];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (qb + u < q1) {
+                        const float ve[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+#pragma unroll
+                            for (int t = 0; t < DP; ++t) acc[e][t] = fmaf(ve[e], o[u][t], acc[e][t]);
+                            acc[e][DP] += ve[e];
+                        }
+                    }
+                }
+            }
+            if (ok) {  // 4 channels x (DP+1) consecutive floats
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+#pragma unroll
+                    for (int t = 0; t <= DP; ++t) xr[(c + e) * (DP + 1) + t] = acc[e][t];
+            }
+        }
+    }
+}
+
+cublasHandle_t cublas_handle() {
+    static cublasHandle_t h[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!h[dev & 63]) {
+        if (cublasCreate(&h[dev & 63]) != CUBLAS_STATUS_SUCCESS) return nullptr;
+        cublasSetMathMode(h[dev & 63], CUBLAS_DEFAULT_MATH);  // FP32 FMA, no TF32
+    }
+    return h[dev & 63];
+}
+
+bool gemm_route_enabled(int gc) {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("FC_NO_GEMM");
+        v = (e && e[0] == '1') ? 0 : 1;
+    }
+    return v == 1 && gc >= 96 && gc % 4 == 0;
+}
+
+int64_t gemm_chunk(int64_t total, int ktot) {
+    const int64_t cap = std::max<int64_t>(1024, ((int64_t)256 << 20) / ((int64_t)ktot * 4));
+    return std::min<int64_t>(total, cap);
+}
+
+}  // namespace
+
+// out [total, cout] = X [total, ktot] . w [ktot, cout]   (w: forward or adjoint packing)
+template <int DP, bool REV>
+int launch_gemm_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, const float *rows, const float *loc,
+                       const int32_t *nbr, Csr csr, const float *w, float *out, cudaStream_t st) {
+    if (!gemm_route_enabled(gc) || (reinterpret_cast<uintptr_t>(rows) % 16) != 0) return FC_ERR_UNSUPPORTED;
+    cublasHandle_t h = cublas_handle();
+    if (!h) return FC_ERR_UNSUPPORTED;
+    const int ktot = gc * (DP + 1);
+    const int64_t chunk = gemm_chunk(total, ktot);
+    float *X = (float *)scratch_alloc(sizeof(float) * chunk * ktot, st);
+    if (!X) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+    cublasSetStream(h, st);
+    prof_begin(REV ? "gemm_reverse" : "gemm_forward", st);
+    int rc = FC_OK;
+    for (int64_t p0 = 0; p0 < total && rc == FC_OK; p0 += chunk) {
+        const int64_t m = std::min(chunk, total - p0);
+        const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)num_sms() * 8);
+        moments_rows_kernel<DP, REV><<<grid, 256, 0, st>>>(p0, m, n, gc, k, rows, loc, nbr, csr, X);
+        count_launch();
+        const float one = 1.f, zero = 0.f;
+        if (cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, cout, (int)m, ktot, &one, w, cout, X, ktot, &zero,
+                        out + p0 * cout, cout) != CUBLAS_STATUS_SUCCESS)
+            rc = set_error(FC_ERR_CUDA, "cublasSgemm failed");
+    }
+    prof_end(st);
+    scratch_free(X, st);
+    if (rc) return rc;
+    return check_launch("moments + GEMM");
+}
+
+// d_theta via P [cout, ktot] = sum over point chunks (fixed order) of G^T X, then the fp64
+// fixed-order reduce kernel converts P into d_theta / d_theta_b.
+template <int DP>
+int launch_gemm_dtheta_dp(int64_t total, int64_t n, int cin, int k, int cout, const float *feat, const float *loc,
+                          const int32_t *nbr, const float *g, float *d_theta, float *d_theta_b, cudaStream_t st) {
+    if (!gemm_route_enabled(cin) || (reinterpret_cast<uintptr_t>(feat) % 16) != 0) return FC_ERR_UNSUPPORTED;
+    cublasHandle_t h = cublas_handle();
+    if (!h) return FC_ERR_UNSUPPORTED;
+    const int ktot = cin * (DP + 1);
+    const int64_t chunk = gemm_chunk(total, ktot);
+    float *X = (float *)scratch_alloc(sizeof(float) * chunk * ktot, st);
+    float *P = (float *)scratch_alloc(sizeof(float) * (size_t)cout * ktot, st);
+    if (!X || !P) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+    cublasSetStream(h, st);
+    prof_begin("gemm_dtheta", st);
+    int rc = FC_OK;
+    for (int64_t p0 = 0; p0 < total && rc == FC_OK; p0 += chunk) {
+        const int64_t m = std::min(chunk, total - p0);
+        const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)num_sms() * 8);
+        moments_rows_kernel<DP, false><<<grid, 256, 0, st>>>(p0, m, n, cin, k, feat, loc, nbr, Csr{nullptr, nullptr}, X);
+        count_launch();
+        const float one = 1.f, beta = p0 == 0 ? 0.f : 1.f;
+        // column-major: P_cm (ktot x cout) = X_cm (ktot x m) . G_cm^T (m x cout)
+        if (cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, ktot, cout, (int)m, &one, X, ktot, g + p0 * cout, cout, &beta,
+                        P, ktot) != CUBLAS_STATUS_SUCCESS)
+            rc = set_error(FC_ERR_CUDA, "cublasSgemm failed");
+    }
+    if (rc == FC_OK) rc = launch_dtheta_reduce<float>(1, cin, DP, cout, P, d_theta, d_theta_b, st);
+    prof_end(st);
+    scratch_free(X, st);
+    scratch_free(P, st);
+    if (rc) return rc;
+    return check_launch("moments + GEMM (d_theta)");
+}
+
+#define FC_GEMM_INST(DP)                                                                                          \
+    template int launch_gemm_gmc_dp<DP, false>(int64_t, int64_t, int, int, int, const float *, const float *,     \
+                                               const int32_t *, Csr, const float *, float *, cudaStream_t);       \
+    template int launch_gemm_gmc_dp<DP, true>(int64_t, int64_t, int, int, int, const float *, const float *,      \
+                                              const int32_t *, Csr, const float *, float *, cudaStream_t);        \
+    template int launch_gemm_dtheta_dp<DP>(int64_t, int64_t, int, int, int, const float *, const float *,         \
+                                           const int32_t *, const float *, float *, float *, cudaStream_t);
+FC_GEMM_INST(1)
+FC_GEMM_INST(2)
+FC_GEMM_INST(3)
+FC_GEMM_INST(4)
+FC_GEMM_INST(5)
+FC_GEMM_INST(6)
+FC_GEMM_INST(7)
+FC_GEMM_INST(8)
 
 #define FC_WIDE_INST(T, DP)                                                                                       \
     template int launch_wide_gmc_dp<T, DP, false>(int64_t, int64_t, int, int, int, const T *, const T *,       \
