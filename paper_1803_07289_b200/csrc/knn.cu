@@ -227,6 +227,17 @@ __global__ void sorted_points_kernel(int64_t n, int d, const PT *__restrict__ pt
     }
 }
 
+// squared gap between coordinate x and cell c of axis t (0 inside; the first / last cell of
+// an axis extends to infinity outward, since cell_coord clamps)
+__device__ __forceinline__ double cell_gap2(const GridParams &gp, double x, int c, int t) {
+    if (t >= gp.d) return 0.0;
+    const double lo = gp.lo[t] + (double)c * gp.h, hi = lo + gp.h;
+    double g = 0.0;
+    if (c > 0 && x < lo) g = lo - x;
+    else if (c < gp.G[t] - 1 && x > hi) g = x - hi;
+    return g * g;
+}
+
 template <int KK>
 __global__ void __launch_bounds__(128)
     knn_grid_query_kernel(int64_t n, int k, const double4 *__restrict__ sp,
@@ -249,6 +260,7 @@ __global__ void __launch_bounds__(128)
     const int kk = k - 1;
     const int rmax = max(gp.G[0], max(gp.G[1], gp.G[2]));
     const double margin = gp.h * 1e-7;
+    const double prune_margin = gp.h * gp.h * 1e-6;
     for (int r = 0;; ++r) {
         for (int dz = -r; dz <= r; ++dz) {
             const int z = c[2] + dz;
@@ -258,9 +270,18 @@ __global__ void __launch_bounds__(128)
                 if (y < 0 || y >= gp.G[1]) continue;
                 const bool full = (dz == -r || dz == r || dy == -r || dy == r);
                 const int step = full ? 1 : (r > 0 ? 2 * r : 1);
+                // lower bound of the squared distance to any point of the cell row (y, z):
+                // cells farther than the current k-1-th distance cannot contribute (exact:
+                // boundary cells are unbounded outward, and a small margin covers rounding)
+                double worst = DBL_MAX;
+#pragma unroll
+                for (int a = 0; a < KK; ++a)
+                    if (a == kk - 1) worst = bd[a];
+                const double gyz = cell_gap2(gp, px[1], y, 1) + cell_gap2(gp, px[2], z, 2);
                 for (int dx = -r; dx <= r; dx += step) {
                     const int x = c[0] + dx;
                     if (x < 0 || x >= gp.G[0]) continue;
+                    if (worst < DBL_MAX && gyz + cell_gap2(gp, px[0], x, 0) - prune_margin > worst) continue;
                     const int64_t b = interleave_cell(gp, x, y, z);
                     const int32_t s1 = off[b + 1];
                     for (int32_t s = off[b]; s < s1; ++s) {
