@@ -163,17 +163,22 @@ __device__ __forceinline__ int cell_coord(const GridParams &gp, double x, int t)
     return c;
 }
 
+// Bounding box in two passes: each block reduces a grid-stride share to partial[block][6]
+// (min x,y,z, max x,y,z); bbox_final_kernel (one block) reduces the partials.
 template <typename PT>
-__global__ void bbox_kernel(int64_t n, int d, const PT *__restrict__ pts, double *__restrict__ box) {
-    // one block, 1024 threads: box[t] = min, box[3+t] = max
-    __shared__ double smin[3][32], smax[3][32];
+__global__ void __launch_bounds__(256)
+    bbox_partial_kernel(int64_t n, int d, const PT *__restrict__ pts, double *__restrict__ partial) {
+    __shared__ double smin[3][8], smax[3][8];
     double mn[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, mx[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
-        for (int t = 0; t < d && t < 3; ++t) {
-            const double v = coord(pts, i, d, t);
-            mn[t] = fmin(mn[t], v);
-            mx[t] = fmax(mx[t], v);
-        }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+        for (int t = 0; t < 3; ++t)
+            if (t < d) {
+                const double v = coord(pts, i, d, t);
+                mn[t] = fmin(mn[t], v);
+                mx[t] = fmax(mx[t], v);
+            }
+#pragma unroll
     for (int t = 0; t < 3; ++t) {
         for (int o = 16; o > 0; o >>= 1) {
             mn[t] = fmin(mn[t], __shfl_xor_sync(0xffffffffu, mn[t], o));
@@ -185,19 +190,24 @@ __global__ void bbox_kernel(int64_t n, int d, const PT *__restrict__ pts, double
         }
     }
     __syncthreads();
-    if (threadIdx.x < 32) {
-        for (int t = 0; t < 3; ++t) {
-            double a = threadIdx.x < (blockDim.x >> 5) ? smin[t][threadIdx.x] : DBL_MAX;
-            double b = threadIdx.x < (blockDim.x >> 5) ? smax[t][threadIdx.x] : -DBL_MAX;
-            for (int o = 16; o > 0; o >>= 1) {
-                a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
-                b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
-            }
-            if (threadIdx.x == 0) {
-                box[t] = a;
-                box[3 + t] = b;
-            }
+    if (threadIdx.x < 3) {
+        const int t = threadIdx.x;
+        double a = DBL_MAX, b = -DBL_MAX;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a = fmin(a, smin[t][w]);
+            b = fmax(b, smax[t][w]);
         }
+        partial[(int64_t)blockIdx.x * 6 + t] = a;
+        partial[(int64_t)blockIdx.x * 6 + 3 + t] = b;
+    }
+}
+
+__global__ void bbox_final_kernel(int parts, const double *__restrict__ partial, double *__restrict__ box) {
+    if (threadIdx.x < 6) {
+        const int t = threadIdx.x;
+        double v = t < 3 ? DBL_MAX : -DBL_MAX;
+        for (int q = 0; q < parts; ++q) v = t < 3 ? fmin(v, partial[q * 6 + t]) : fmax(v, partial[q * 6 + t]);
+        box[t] = v;
     }
 }
 
@@ -358,8 +368,16 @@ template <typename PT>
 static int cell_csr(int64_t n, int d, const PT *pts, GridParams *gp_out, int32_t **off_out,
                     int32_t **ent_out, int64_t *buckets_out, cudaStream_t st, double ppc_default = 2.0) {
     double *box_d = (double *)scratch_alloc(6 * sizeof(double), st);
-    bbox_kernel<PT><<<1, 1024, 0, st>>>(n, d, pts, box_d);
-    count_launch();
+    {
+        const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)num_sms() * 4));
+        double *partial = (double *)scratch_alloc(sizeof(double) * 6 * parts, st);
+        if (!partial) return set_error(FC_ERR_CUDA, "scratch allocation failed (bbox)");
+        bbox_partial_kernel<PT><<<parts, 256, 0, st>>>(n, d, pts, partial);
+        bbox_final_kernel<<<1, 32, 0, st>>>(parts, partial, box_d);
+        count_launch();
+        count_launch();
+        scratch_free(partial, st);
+    }
     double box[6];
     cudaMemcpyAsync(box, box_d, sizeof(box), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
