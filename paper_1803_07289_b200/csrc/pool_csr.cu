@@ -375,6 +375,25 @@ __global__ void csr_sort_segments_kernel(int64_t buckets, const int32_t *__restr
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < buckets;
          b += (int64_t)gridDim.x * blockDim.x) {
         const int32_t lo = off[b], hi = off[b + 1];
+        if (hi - lo <= 16) {  // the usual case: sort in registers (bounded insertion sort)
+            constexpr int32_t kBig = 0x7fffffff;
+            int32_t v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = lo + q < hi ? ent[lo + q] : kBig;
+#pragma unroll
+            for (int a = 1; a < 16; ++a) {
+#pragma unroll
+                for (int q = a; q > 0; --q) {
+                    const int32_t x = v[q - 1], y = v[q];
+                    v[q - 1] = min(x, y);
+                    v[q] = max(x, y);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                if (lo + q < hi) ent[lo + q] = v[q];
+            continue;
+        }
         for (int32_t a = lo + 1; a < hi; ++a) {
             const int32_t v = ent[a];
             int32_t q = a;
