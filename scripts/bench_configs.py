@@ -161,6 +161,19 @@ def c2(reps):
         dbw()
     out["step_all"] = row(timed(step, reps), P)
     out["step_all"]["what"] = "conv fwd+bwd, pool fwd+bwd, deconv fwd+bwd back to back"
+    # the same step captured once as a CUDA graph and replayed (launch-bound at 8 K points)
+    try:
+        s_cap = torch.cuda.Stream()
+        s_cap.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s_cap):
+            step()  # warm the allocator / kernel attributes outside the capture
+        torch.cuda.current_stream().wait_stream(s_cap)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        out["step_all_cuda_graph"] = row(timed(graph.replay, reps), P)
+    except Exception as exc:  # noqa: BLE001 -- report, do not fail the suite
+        out["step_all_cuda_graph"] = {"error": f"{type(exc).__name__}: {str(exc)[:160]}"}
     return {"shape": "B=8, N=1024, K=16, 64->128 (pool on 128 ch, deconv 128->64), fp32", **out}
 
 
