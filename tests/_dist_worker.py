@@ -86,7 +86,12 @@ def main():
     for r in rows:
         seq += r
     res["ordered_sum_bitwise"] = bool(torch.equal(got, seq))
-    print("RESULT " + json.dumps(res), flush=True)
+    out_dir = os.environ.get("FC_RESULT_DIR")
+    if out_dir:  # one file per rank: the two ranks' stdout lines can interleave
+        with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fh:
+            json.dump(res, fh)
+    else:
+        print("RESULT " + json.dumps(res), flush=True)
     dist.destroy_process_group()
 
 

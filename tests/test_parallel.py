@@ -50,8 +50,8 @@ def test_halo_plan_invariants(oracle_mod):
 
 
 @pytest.mark.timeout(300)
-def test_point_chunk_sharding_gloo_world2(oracle_mod):
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1")
+def test_point_chunk_sharding_gloo_world2(oracle_mod, tmp_path):
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1", FC_RESULT_DIR=str(tmp_path))
     for attempt in range(3):  # retries only guard against a rendezvous-port race
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
                "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
@@ -60,7 +60,7 @@ def test_point_chunk_sharding_gloo_world2(oracle_mod):
         if proc.returncode == 0:
             break
     assert proc.returncode == 0, proc.stderr[-3000:]
-    res = [json.loads(line[7:]) for line in proc.stdout.splitlines() if line.startswith("RESULT ")]
+    res = [json.loads((tmp_path / f"rank{r}.json").read_text()) for r in range(2)]
     assert len(res) == 2
     for r in res:
         assert r["halo"] > 0
