@@ -332,6 +332,10 @@ template <int DP, bool REV>
 int launch_gemm_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, const float *rows, const float *loc,
                        const int32_t *nbr, Csr csr, const float *w, float *out, cudaStream_t st);
 template <int DP>
+int launch_gemm_rev_dloc_dp(int64_t total, int64_t n, int gc, int k, int cout, const float *rows, const float *loc,
+                            Csr csr, const float *w, float *out, const float *feat, const float *theta,
+                            const float *centre, float *dloc, cudaStream_t st);
+template <int DP>
 int launch_gemm_dtheta_dp(int64_t total, int64_t n, int cin, int k, int cout, const float *feat, const float *loc,
                           const int32_t *nbr, const float *g, float *d_theta, float *d_theta_b, cudaStream_t st);
 
@@ -354,6 +358,15 @@ static int launch_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, cons
             const int rc = launch_gemm_gmc_dp<DP, REV>(total, n, gc, k, cout, (const float *)rows, (const float *)loc,
                                                        nbr, csr, (const float *)w, (float *)out, st);
             if (rc != FC_ERR_UNSUPPORTED) return rc;
+        }
+        if constexpr (REV) {
+            if (dloc != nullptr && wide_enabled()) {
+                const int rc = launch_gemm_rev_dloc_dp<DP>(total, n, gc, k, cout, (const float *)rows,
+                                                           (const float *)loc, csr, (const float *)w, (float *)out,
+                                                           (const float *)feat, (const float *)theta,
+                                                           (const float *)centre, (float *)dloc, st);
+                if (rc != FC_ERR_UNSUPPORTED) return rc;
+            }
         }
     }
     if (wide_enabled()) {  // conv_wide.cu: same sums, same order, CTA-tiled (+ the d_loc neighbour term)

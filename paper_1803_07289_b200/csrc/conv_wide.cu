@@ -565,7 +565,7 @@ namespace {
 
 // X[p, c*(DP+1) + t] for points [p0, p0 + m): one warp per point, lanes over 4 channels,
 // 8 neighbour rows in flight, slot order per (c, t) (_native.pyx:52-59).
-template <int DP, bool REVERSE>
+template <int DP, bool REVERSE, bool TMAJOR = false>
 __global__ void __launch_bounds__(256)
     moments_rows_kernel(int64_t p0, int64_t m, int64_t n, int gc, int k, const float *__restrict__ rows,
                         const float *__restrict__ loc, const int32_t *__restrict__ nbr, Csr csr,
@@ -622,11 +622,17 @@ __global__ void __launch_bounds__(256)
                     }
                 }
             }
-            if (ok) {  // 4 channels x (DP+1) consecutive floats
+            if (ok) {
+                if constexpr (TMAJOR) {  // X[p, t*gc + c]: one float4 per t
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
+                    for (int t = 0; t <= DP; ++t)
+                        *reinterpret_cast<float4 *>(xr + t * gc + c) = make_float4(acc[0][t], acc[1][t], acc[2][t], acc[3][t]);
+                } else {  // X[p, c*(DP+1) + t]: 4 channels x (DP+1) consecutive floats
 #pragma unroll
-                    for (int t = 0; t <= DP; ++t) xr[(c + e) * (DP + 1) + t] = acc[e][t];
+                    for (int e = 0; e < 4; ++e)
+#pragma unroll
+                        for (int t = 0; t <= DP; ++t) xr[(c + e) * (DP + 1) + t] = acc[e][t];
+                }
             }
         }
     }
@@ -724,13 +730,118 @@ int launch_gemm_dtheta_dp(int64_t total, int64_t n, int cin, int k, int cout, co
     return check_launch("moments + GEMM (d_theta)");
 }
 
+namespace {
+
+// w_t[(t*gc + c)*cout + o] = w[(c*(DP+1) + t)*cout + o]   (c-major -> t-major packing)
+__global__ void repack_tmajor_kernel(int gc, int dp1, int cout, const float *__restrict__ w, float *__restrict__ wt) {
+    const int64_t total = (int64_t)gc * dp1 * cout;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int o = (int)(e % cout);
+        const int64_t r = e / cout;  // = c*dp1 + t
+        const int t = (int)(r % dp1), c = (int)(r / dp1);
+        wt[((int64_t)t * gc + c) * cout + o] = w[e];
+    }
+}
+
+// theta [gc][cout][d] -> tcat [gc][d*cout]: tcat[c'][t*cout + c] = theta[c', c, t]
+__global__ void pack_theta_cat_kernel(int gc, int cout, int d, const float *__restrict__ theta,
+                                      float *__restrict__ tcat) {
+    const int64_t total = (int64_t)gc * cout * d;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int t = (int)(e % d);
+        const int64_t r = e / d;  // = c' * cout + c
+        const int c = (int)(r % cout), cp = (int)(r / cout);
+        tcat[(int64_t)cp * d * cout + (int64_t)t * cout + c] = theta[e];
+    }
+}
+
+// dloc[p, t] = centre[p, t] - sum_c f[p, c] U[p, t*cout + c]   (warp per point)
+template <int DP>
+__global__ void __launch_bounds__(256)
+    dloc_nbr_kernel(int64_t p0, int64_t m, int cout, const float *__restrict__ feat, const float *__restrict__ U,
+                    const float *__restrict__ centre, float *__restrict__ dloc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < m; r += nw) {
+        const int64_t p = p0 + r;
+        float part[DP];
+#pragma unroll
+        for (int t = 0; t < DP; ++t) part[t] = 0.f;
+        for (int c = lane; c < cout; c += 32) {
+            const float f = feat[p * cout + c];
+#pragma unroll
+            for (int t = 0; t < DP; ++t) part[t] = fmaf(f, U[r * DP * cout + t * cout + c], part[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < DP; ++t) {
+            float v = part[t];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) dloc[p * DP + t] = centre[p * DP + t] - v;
+        }
+    }
+}
+
+}  // namespace
+
+// Reverse role with the location gradient: d_f = Y . W (t-major), U = Yb . [theta_0 .. theta_{d-1}]
+// (one GEMM, N = d*cout), then the neighbour-role term dotted with f (dloc_nbr_kernel).
+template <int DP>
+int launch_gemm_rev_dloc_dp(int64_t total, int64_t n, int gc, int k, int cout, const float *rows, const float *loc,
+                            Csr csr, const float *w, float *out, const float *feat, const float *theta,
+                            const float *centre, float *dloc, cudaStream_t st) {
+    if (!gemm_route_enabled(gc) || (reinterpret_cast<uintptr_t>(rows) % 16) != 0) return FC_ERR_UNSUPPORTED;
+    cublasHandle_t h = cublas_handle();
+    if (!h) return FC_ERR_UNSUPPORTED;
+    const int ktot = gc * (DP + 1);
+    const int64_t chunk = gemm_chunk(total, ktot + DP * cout);
+    float *X = (float *)scratch_alloc(sizeof(float) * chunk * ktot, st);
+    float *U = (float *)scratch_alloc(sizeof(float) * chunk * DP * cout, st);
+    float *wt = (float *)scratch_alloc(sizeof(float) * (size_t)ktot * cout, st);
+    float *tcat = (float *)scratch_alloc(sizeof(float) * (size_t)gc * DP * cout, st);
+    if (!X || !U || !wt || !tcat) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+    const unsigned pg = (unsigned)std::min<int64_t>(ceil_div((int64_t)ktot * cout, 256), 4096);
+    repack_tmajor_kernel<<<pg, 256, 0, st>>>(gc, DP + 1, cout, w, wt);
+    pack_theta_cat_kernel<<<pg, 256, 0, st>>>(gc, cout, DP, theta, tcat);
+    count_launch();
+    count_launch();
+    cublasSetStream(h, st);
+    prof_begin("gemm_reverse_dloc", st);
+    int rc = FC_OK;
+    for (int64_t p0 = 0; p0 < total && rc == FC_OK; p0 += chunk) {
+        const int64_t m = std::min(chunk, total - p0);
+        const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)num_sms() * 8);
+        moments_rows_kernel<DP, true, true><<<grid, 256, 0, st>>>(p0, m, n, gc, k, rows, loc, nullptr, csr, X);
+        count_launch();
+        const float one = 1.f, zero = 0.f;
+        if (cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, cout, (int)m, ktot, &one, wt, cout, X, ktot, &zero,
+                        out + p0 * cout, cout) != CUBLAS_STATUS_SUCCESS ||
+            cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, DP * cout, (int)m, gc, &one, tcat, DP * cout, X + DP * gc, ktot,
+                        &zero, U, DP * cout) != CUBLAS_STATUS_SUCCESS) {
+            rc = set_error(FC_ERR_CUDA, "cublasSgemm failed");
+            break;
+        }
+        dloc_nbr_kernel<DP><<<grid, 256, 0, st>>>(p0, m, cout, feat, U, centre, dloc);
+        count_launch();
+    }
+    prof_end(st);
+    scratch_free(X, st);
+    scratch_free(U, st);
+    scratch_free(wt, st);
+    scratch_free(tcat, st);
+    if (rc) return rc;
+    return check_launch("moments + GEMM (reverse, d_loc)");
+}
+
 #define FC_GEMM_INST(DP)                                                                                          \
     template int launch_gemm_gmc_dp<DP, false>(int64_t, int64_t, int, int, int, const float *, const float *,     \
                                                const int32_t *, Csr, const float *, float *, cudaStream_t);       \
     template int launch_gemm_gmc_dp<DP, true>(int64_t, int64_t, int, int, int, const float *, const float *,      \
                                               const int32_t *, Csr, const float *, float *, cudaStream_t);        \
     template int launch_gemm_dtheta_dp<DP>(int64_t, int64_t, int, int, int, const float *, const float *,         \
-                                           const int32_t *, const float *, float *, float *, cudaStream_t);
+                                           const int32_t *, const float *, float *, float *, cudaStream_t);       \
+    template int launch_gemm_rev_dloc_dp<DP>(int64_t, int64_t, int, int, int, const float *, const float *, Csr,  \
+                                             const float *, float *, const float *, const float *, const float *, \
+                                             float *, cudaStream_t);
 FC_GEMM_INST(1)
 FC_GEMM_INST(2)
 FC_GEMM_INST(3)
