@@ -332,6 +332,9 @@ template <int DP, bool REV>
 int launch_gemm_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, const float *rows, const float *loc,
                        const int32_t *nbr, Csr csr, const float *w, float *out, cudaStream_t st);
 template <int DP>
+int launch_gemm_centre_dp(int64_t total, int64_t n, int cin, int k, int cout, const float *feat, const int32_t *nbr,
+                          const float *g, const float *theta, float *centre, cudaStream_t st);
+template <int DP>
 int launch_gemm_rev_dloc_dp(int64_t total, int64_t n, int gc, int k, int cout, const float *rows, const float *loc,
                             Csr csr, const float *w, float *out, const float *feat, const float *theta,
                             const float *centre, float *dloc, cudaStream_t st);
@@ -429,6 +432,11 @@ template <typename T, int DP>
 static int launch_dloc_centre_dp(int64_t total, int64_t n, int cin, int k, int cout, const T *feat,
                                  const int32_t *nbr, const T *g, const T *theta, T *centre,
                                  cudaStream_t st) {
+    if constexpr (sizeof(T) == 4) {  // fp32: Z = G . theta as one SGEMM + a row dot (conv_wide.cu)
+        const int rc = launch_gemm_centre_dp<DP>(total, n, cin, k, cout, (const float *)feat, nbr, (const float *)g,
+                                                 (const float *)theta, (float *)centre, st);
+        if (rc != FC_ERR_UNSUPPORTED) return rc;
+    }
     const size_t smem = (size_t)8 * cout * sizeof(T);
     set_smem(dloc_centre_kernel<T, DP>, smem);
     dloc_centre_kernel<T, DP><<<grid_for(ceil_div(total, 8), 1), 256, smem, st>>>(total, n, cin, k, cout, feat, nbr, g, theta, centre);

@@ -832,6 +832,78 @@ int launch_gemm_rev_dloc_dp(int64_t total, int64_t n, int gc, int k, int cout, c
     return check_launch("moments + GEMM (reverse, d_loc)");
 }
 
+namespace {
+
+// centre[p, t] = sum_c xbar[p, c] Z[p, t*cin + c],  xbar = sum_s f[j_s]  (warp per point)
+template <int DP>
+__global__ void __launch_bounds__(256)
+    centre_dot_kernel(int64_t p0, int64_t m, int64_t n, int cin, int k, const float *__restrict__ feat,
+                      const int32_t *__restrict__ nbr, const float *__restrict__ Z, float *__restrict__ centre) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < m; r += nw) {
+        const int64_t p = p0 + r, base = (p / n) * n;
+        float part[DP];
+#pragma unroll
+        for (int t = 0; t < DP; ++t) part[t] = 0.f;
+        for (int c = lane; c < cin; c += 32) {
+            float xb = 0.f;
+            for (int s = 0; s < k; ++s) xb += feat[(base + nbr[p * k + s]) * cin + c];
+#pragma unroll
+            for (int t = 0; t < DP; ++t) part[t] = fmaf(xb, Z[r * DP * cin + t * cin + c], part[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < DP; ++t) {
+            float v = part[t];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) centre[p * DP + t] = v;
+        }
+    }
+}
+
+}  // namespace
+
+// Centre role of the location gradient: Z = G . [theta_0 .. theta_{d-1}] (one SGEMM,
+// N = d*cin; theta_t is [cout][cin]), then centre = rowdot(xbar, Z_t).
+template <int DP>
+int launch_gemm_centre_dp(int64_t total, int64_t n, int cin, int k, int cout, const float *feat, const int32_t *nbr,
+                          const float *g, const float *theta, float *centre, cudaStream_t st) {
+    static const bool off = [] {
+        const char *e = getenv("FC_NO_GEMM");
+        return e && e[0] == '1';
+    }();
+    if (off || cout < 32) return FC_ERR_UNSUPPORTED;
+    cublasHandle_t h = cublas_handle();
+    if (!h) return FC_ERR_UNSUPPORTED;
+    const int64_t chunk = gemm_chunk(total, DP * cin);
+    float *Z = (float *)scratch_alloc(sizeof(float) * chunk * DP * cin, st);
+    float *tcat = (float *)scratch_alloc(sizeof(float) * (size_t)cout * DP * cin, st);
+    if (!Z || !tcat) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+    const unsigned pg = (unsigned)std::min<int64_t>(ceil_div((int64_t)cout * cin * DP, 256), 4096);
+    pack_theta_cat_kernel<<<pg, 256, 0, st>>>(cout, cin, DP, theta, tcat);  // tcat[c'][t*cin + c]
+    count_launch();
+    cublasSetStream(h, st);
+    prof_begin("gemm_centre", st);
+    int rc = FC_OK;
+    for (int64_t p0 = 0; p0 < total && rc == FC_OK; p0 += chunk) {
+        const int64_t m = std::min(chunk, total - p0);
+        const float one = 1.f, zero = 0.f;
+        if (cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, DP * cin, (int)m, cout, &one, tcat, DP * cin, g + p0 * cout, cout,
+                        &zero, Z, DP * cin) != CUBLAS_STATUS_SUCCESS) {
+            rc = set_error(FC_ERR_CUDA, "cublasSgemm failed");
+            break;
+        }
+        const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)num_sms() * 8);
+        centre_dot_kernel<DP><<<grid, 256, 0, st>>>(p0, m, n, cin, k, feat, nbr, Z, centre);
+        count_launch();
+    }
+    prof_end(st);
+    scratch_free(Z, st);
+    scratch_free(tcat, st);
+    if (rc) return rc;
+    return check_launch("GEMM (d_loc centre)");
+}
+
 #define FC_GEMM_INST(DP)                                                                                          \
     template int launch_gemm_gmc_dp<DP, false>(int64_t, int64_t, int, int, int, const float *, const float *,     \
                                                const int32_t *, Csr, const float *, float *, cudaStream_t);       \
@@ -841,7 +913,9 @@ int launch_gemm_rev_dloc_dp(int64_t total, int64_t n, int gc, int k, int cout, c
                                            const int32_t *, const float *, float *, float *, cudaStream_t);       \
     template int launch_gemm_rev_dloc_dp<DP>(int64_t, int64_t, int, int, int, const float *, const float *, Csr,  \
                                              const float *, float *, const float *, const float *, const float *, \
-                                             float *, cudaStream_t);
+                                             float *, cudaStream_t);                                              \
+    template int launch_gemm_centre_dp<DP>(int64_t, int64_t, int, int, int, const float *, const int32_t *,      \
+                                           const float *, const float *, float *, cudaStream_t);
 FC_GEMM_INST(1)
 FC_GEMM_INST(2)
 FC_GEMM_INST(3)
