@@ -650,12 +650,14 @@ cublasHandle_t cublas_handle() {
 }
 
 bool gemm_route_enabled(int gc) {
-    static int v = -1;
+    static int v = -1, gmin = 32;
     if (v < 0) {
         const char *e = getenv("FC_NO_GEMM");
         v = (e && e[0] == '1') ? 0 : 1;
+        const char *m = getenv("FC_GEMM_MIN");  // smallest gathered channel count on the GEMM route
+        if (m && atoi(m) > 0) gmin = atoi(m);
     }
-    return v == 1 && gc >= 96 && gc % 4 == 0;
+    return v == 1 && gc >= gmin && gc % 4 == 0;
 }
 
 int64_t gemm_chunk(int64_t total, int ktot) {
