@@ -204,6 +204,9 @@ int fc_pool_select_backward(int dtype, int64_t m, int64_t n, int c, int k, const
  * the bound is per cloud: entry e belongs to cloud e / (n_per_cloud*row_len). */
 int fc_indices_to_i32(const int64_t *in, int32_t *out, int64_t count, int64_t hi,
                       int32_t *bad, void *stream);
+/* *bad (device int32, caller-zeroed) += number of NaN / +-inf entries of x[0..count): the
+ * reference's np.isfinite(...).all() checks (network.py:391-396, flexops.py:38-39) on the device. */
+int fc_count_nonfinite(int dtype, const void *x, int64_t count, int32_t *bad, void *stream);
 int fc_check_indices(const int32_t *idx, int64_t count, int64_t hi, int32_t *bad,
                      void *stream);
 

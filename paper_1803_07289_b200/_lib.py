@@ -58,6 +58,7 @@ SIGNATURES = {
     "fc_pool_select_backward": [_I, _I64, _I64, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "fc_indices_to_i32": [_P, _P, _I64, _I64, _P, _P],
     "fc_check_indices": [_P, _I64, _I64, _P, _P],
+    "fc_count_nonfinite": [_I, _P, _I64, _P, _P],
 }
 _RESTYPE = {"fc_last_error": ctypes.c_char_p, "fc_launch_count": ctypes.c_uint64, "fc_profile_enable": None,
             "fc_profile_reset": None, "fc_profile_name": ctypes.c_char_p, "fc_profile_ms": ctypes.c_float}

@@ -244,3 +244,12 @@ def check_indices(idx32, hi):
     bad = torch.zeros(1, dtype=torch.int32, device=idx32.device)
     _lib.call("fc_check_indices", _p(idx32), idx32.numel(), int(hi), _p(bad), _stream(idx32))
     return bad
+
+
+def count_nonfinite(x, bad=None):
+    """Device int32 [1]: number of NaN / inf entries of x (added into `bad` if given)."""
+    x = _need(x, "tensor")
+    if bad is None:
+        bad = torch.zeros(1, dtype=torch.int32, device=x.device)
+    _lib.call("fc_count_nonfinite", _dtype(x), _p(x), x.numel(), _p(bad), _stream(x))
+    return bad

@@ -124,6 +124,7 @@ template <typename T>
 int launch_scatter_rows(int64_t rows_in, int64_t rows_out, int c, const T *in, const int32_t *sel, T *out,
                         cudaStream_t st);
 int launch_selection_owner(int64_t m, int64_t n, const int32_t *sel, int32_t *owner, cudaStream_t st);
+int launch_count_nonfinite(int dtype, const void *x, int64_t count, int32_t *bad, cudaStream_t st);
 template <typename T>
 int launch_pool_select_fwd(int64_t m, int c, int k, const T *feat, const int32_t *nbr, const int32_t *rows,
                            const int32_t *owner, T *out, int32_t *winners, cudaStream_t st);
@@ -471,6 +472,12 @@ int fc_pool_select_backward(int dtype, int64_t m, int64_t n, int c, int k, const
 int fc_indices_to_i32(const int64_t *in, int32_t *out, int64_t count, int64_t hi, int32_t *bad, void *stream) {
     if (count == 0) return FC_OK;
     return launch_narrow_indices(in, out, count, hi, bad, ST(stream));
+}
+
+int fc_count_nonfinite(int dtype, const void *x, int64_t count, int32_t *bad, void *stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (count == 0) return FC_OK;
+    return fc::launch_count_nonfinite(dtype, x, count, bad, ST(stream));
 }
 
 int fc_check_indices(const int32_t *idx, int64_t count, int64_t hi, int32_t *bad, void *stream) {

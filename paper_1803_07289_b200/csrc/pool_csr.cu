@@ -556,6 +556,29 @@ __global__ void check_indices_kernel(const int32_t *__restrict__ in, int64_t cou
     if (local_bad) atomicAdd(bad, local_bad);
 }
 
+// Non-finite entries of a float tensor: *bad += count (16-byte loads where aligned).  Used for
+// the network's per-layer gradient checks (network.py:391-392) without a reduction library.
+template <typename T>
+__global__ void __launch_bounds__(256) count_nonfinite_kernel(const T *__restrict__ x, int64_t count,
+                                                              int32_t *__restrict__ bad) {
+    int32_t local = 0;
+    constexpr int V = 16 / sizeof(T);
+    const bool vec = (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+    const int64_t nv = vec ? count / V : 0;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nv; e += (int64_t)gridDim.x * blockDim.x) {
+        typename Vec16<T>::V v = __ldg(reinterpret_cast<const typename Vec16<T>::V *>(x) + e);
+#pragma unroll
+        for (int q = 0; q < V; ++q) local += isfinite(reinterpret_cast<const T *>(&v)[q]) ? 0 : 1;
+    }
+    for (int64_t e = nv * V + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+         e += (int64_t)gridDim.x * blockDim.x)
+        local += isfinite(x[e]) ? 0 : 1;
+    if (__any_sync(0xffffffffu, local != 0)) {
+        for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+        if ((threadIdx.x & 31) == 0 && local) atomicAdd(bad, local);
+    }
+}
+
 // ---------------------------------------------------------------- launchers
 template <typename T>
 int launch_pool_fwd(int64_t total, int64_t n, int c, int k, const T *feat, const int32_t *nbr,
@@ -646,6 +669,13 @@ int launch_narrow_indices(const int64_t *in, int32_t *out, int64_t count, int64_
     narrow_indices_kernel<<<grid_1d(count), 256, 0, st>>>(in, out, count, hi, bad);
     count_launch();
     return check_launch("narrow_indices_kernel");
+}
+int launch_count_nonfinite(int dtype, const void *x, int64_t count, int32_t *bad, cudaStream_t st) {
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(count, 256 * 4), (int64_t)num_sms() * 8));
+    if (dtype == FC_F32) count_nonfinite_kernel<float><<<g, 256, 0, st>>>((const float *)x, count, bad);
+    else count_nonfinite_kernel<double><<<g, 256, 0, st>>>((const double *)x, count, bad);
+    count_launch();
+    return check_launch("count_nonfinite_kernel");
 }
 int launch_check_indices(const int32_t *in, int64_t count, int64_t hi, int32_t *bad, cudaStream_t st) {
     check_indices_kernel<<<grid_1d(count), 256, 0, st>>>(in, count, hi, bad);
