@@ -2,6 +2,7 @@
 // builder (a stable counting sort, no float atomics) and row gather/scatter.
 #include "fc_common.cuh"
 
+#include <cstdlib>
 #include <initializer_list>
 
 namespace fc {
@@ -144,6 +145,58 @@ __global__ void __launch_bounds__(256)
         }
         *reinterpret_cast<VT *>(out + p * c + ch) = o;
         *reinterpret_cast<IT *>(argmax + p * c + ch) = a;
+    }
+}
+
+// fp32, 8 channels per thread: one 32-byte load per neighbour row (ld.global.nc.v8), twice
+// the bytes in flight per thread of pool_fwd_vec_kernel; same comparisons in the same order.
+__device__ __forceinline__ void ldg8f(const float *p, float (&v)[8]) {
+    asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(p));
+}
+
+__global__ void __launch_bounds__(256)
+    pool_fwd_w8_kernel(int64_t total, int64_t n, int c, int k, const float *__restrict__ feat,
+                       const int32_t *__restrict__ nbr, float *__restrict__ out, int32_t *__restrict__ argmax) {
+    const int cv = c / 8;
+    const int64_t items = total * cv;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < items;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = idx / cv;
+        const int ch = (int)(idx - p * cv) * 8;
+        const int64_t base = (p / n) * n;
+        const int32_t *row = nbr + p * k;
+        float bv[8];
+        int32_t bj[8];
+        for (int s0 = 0; s0 < k; s0 += 8) {
+            int32_t jj[8];
+            float vv[8][8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) jj[u] = __ldg(row + min(s0 + u, k - 1));
+#pragma unroll
+            for (int u = 0; u < 8; ++u) ldg8f(feat + (base + jj[u]) * c + ch, vv[u]);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int s = s0 + u;
+                if (s < k) {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const float v = vv[u][e];
+                        if (s == 0 || v > bv[e] || (v == bv[e] && jj[u] < bj[e])) {
+                            bv[e] = v;
+                            bj[e] = jj[u];
+                        }
+                    }
+                }
+            }
+        }
+        float4 *o = reinterpret_cast<float4 *>(out + p * c + ch);
+        int4 *a = reinterpret_cast<int4 *>(argmax + p * c + ch);
+        o[0] = make_float4(bv[0], bv[1], bv[2], bv[3]);
+        o[1] = make_float4(bv[4], bv[5], bv[6], bv[7]);
+        a[0] = make_int4(bj[0], bj[1], bj[2], bj[3]);
+        a[1] = make_int4(bj[4], bj[5], bj[6], bj[7]);
     }
 }
 
@@ -584,8 +637,22 @@ template <typename T>
 int launch_pool_fwd(int64_t total, int64_t n, int c, int k, const T *feat, const int32_t *nbr,
                     T *out, int32_t *argmax, cudaStream_t st) {
     if (vec16_ok<T>(c, {feat, out, argmax}))
+    {
+        static const bool v4 = [] {  // FC_POOL_V4=1: 4-channel lanes (A/B)
+            const char *e = getenv("FC_POOL_V4");
+            return e && e[0] == '1';
+        }();
+        if constexpr (sizeof(T) == 4) {
+            if (!v4 && c % 8 == 0 && reinterpret_cast<uintptr_t>(feat) % 32 == 0) {
+                pool_fwd_w8_kernel<<<grid_1d(total * (c / 8)), 256, 0, st>>>(total, n, c, k, (const float *)feat, nbr,
+                                                                              (float *)out, argmax);
+                count_launch();
+                return check_launch("pool_fwd_w8_kernel");
+            }
+        }
         pool_fwd_vec_kernel<T><<<grid_1d(total * (c / (16 / (int)sizeof(T)))), 256, 0, st>>>(total, n, c, k, feat, nbr,
                                                                                           out, argmax);
+    }
     else
         pool_fwd_kernel<T><<<grid_1d(total * c), 256, 0, st>>>(total, n, c, k, feat, nbr, out, argmax);
     count_launch();
