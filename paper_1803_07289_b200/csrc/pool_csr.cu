@@ -247,6 +247,56 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// fp32 backward, 8 channels per thread, 4 reverse entries in flight (32-byte argmax and
+// upstream loads); same additions in the same order as pool_bwd_vec_kernel.
+__device__ __forceinline__ void ldg8i(const int32_t *p, int32_t (&v)[8]) {
+    asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "l"(p));
+}
+
+__global__ void __launch_bounds__(256)
+    pool_bwd_w8_kernel(int64_t total, int64_t n, int c, int k, const float *__restrict__ g,
+                       const int32_t *__restrict__ argmax, Csr csr, float *__restrict__ df) {
+    const int cv = c / 8;
+    const int64_t items = total * cv;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < items;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = idx / cv;
+        const int ch = (int)(idx - j * cv) * 8;
+        const int32_t jl = (int32_t)(j - (j / n) * n);
+        const int32_t q0 = __ldg(csr.off + j), q1 = __ldg(csr.off + j + 1);
+        float acc[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+        int64_t prev = -1;
+        for (int32_t qb = q0; qb < q1; qb += 4) {
+            int64_t ii[4];
+            int32_t am[4][8];
+            float gv[4][8];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) ii[u] = (int64_t)__ldg(csr.ent + min(qb + u, q1 - 1)) / k;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                ldg8i(argmax + ii[u] * c + ch, am[u]);
+                ldg8f(g + ii[u] * c + ch, gv[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (qb + u < q1 && ii[u] != prev) {  // row i lists j twice: routed once
+                    prev = ii[u];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        if (am[u][e] == jl) acc[e] += gv[u][e];
+                }
+            }
+        }
+        float4 *o = reinterpret_cast<float4 *>(df + j * c + ch);
+        o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+}
+
 template <typename T>
 static bool vec16_ok(int c, std::initializer_list<const void *> ptrs) {
     if (c % (16 / (int)sizeof(T)) != 0) return false;
@@ -661,6 +711,19 @@ int launch_pool_fwd(int64_t total, int64_t n, int c, int k, const T *feat, const
 template <typename T>
 int launch_pool_bwd(int64_t total, int64_t n, int c, int k, const T *g, const int32_t *argmax,
                     Csr csr, T *df, cudaStream_t st) {
+    if constexpr (sizeof(T) == 4) {
+        static const bool v4 = [] {
+            const char *e = getenv("FC_POOL_V4");
+            return e && e[0] == '1';
+        }();
+        if (!v4 && c % 8 == 0 && reinterpret_cast<uintptr_t>(g) % 32 == 0 &&
+            reinterpret_cast<uintptr_t>(argmax) % 32 == 0 && reinterpret_cast<uintptr_t>(df) % 16 == 0) {
+            pool_bwd_w8_kernel<<<grid_1d(total * (c / 8)), 256, 0, st>>>(total, n, c, k, (const float *)g, argmax, csr,
+                                                                          (float *)df);
+            count_launch();
+            return check_launch("pool_bwd_w8_kernel");
+        }
+    }
     if (vec16_ok<T>(c, {g, argmax, df}))
         pool_bwd_vec_kernel<T><<<grid_1d(total * (c / (16 / (int)sizeof(T)))), 256, 0, st>>>(total, n, c, k, g, argmax,
                                                                                           csr, df);
