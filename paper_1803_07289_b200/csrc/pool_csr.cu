@@ -312,6 +312,10 @@ template <typename T, int V>
 __device__ __forceinline__ void ldvec(const T *p, T (&v)[V]) {
     if constexpr (V == 1) {
         v[0] = __ldg(p);
+    } else if constexpr (V == 8 && sizeof(T) == 4) {  // fp32, 32-byte load
+        asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                     : "l"(p));
     } else {
         using VT = typename Vec16<T>::V;
         const VT x = __ldg(reinterpret_cast<const VT *>(p));
@@ -409,7 +413,15 @@ __global__ void __launch_bounds__(256)
             for (int u = 0; u < 8; ++u) {
                 if (src[u] >= 0) {
 #pragma unroll
-                    for (int e = 0; e < V; ++e) am[u][e] = __ldg(winners + src[u] * c + ch + e);
+                    if constexpr (V == 8) {
+                        asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                                     : "=r"(am[u][0]), "=r"(am[u][1]), "=r"(am[u][2]), "=r"(am[u][3]), "=r"(am[u][4]),
+                                       "=r"(am[u][5]), "=r"(am[u][6]), "=r"(am[u][7])
+                                     : "l"(winners + src[u] * c + ch));
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < V; ++e) am[u][e] = __ldg(winners + src[u] * c + ch + e);
+                    }
                     ldvec<T, V>(g + src[u] * c + ch, gv[u]);
                 }
             }
@@ -774,6 +786,15 @@ template <typename T>
 int launch_pool_select_fwd(int64_t m, int c, int k, const T *feat, const int32_t *nbr, const int32_t *rows,
                            const int32_t *owner, T *out, int32_t *winners, cudaStream_t st) {
     constexpr int V = 16 / sizeof(T);
+    if constexpr (sizeof(T) == 4) {  // fp32: 8 channels per thread, 32-byte loads
+        if (c % 8 == 0 && reinterpret_cast<uintptr_t>(feat) % 32 == 0 && reinterpret_cast<uintptr_t>(out) % 32 == 0 &&
+            reinterpret_cast<uintptr_t>(winners) % 32 == 0) {
+            pool_select_fwd_kernel<T, 8><<<grid_1d(m * (c / 8)), 256, 0, st>>>(m, c, k, feat, nbr, rows, owner, out,
+                                                                                winners);
+            count_launch();
+            return check_launch("pool_select_fwd_kernel");
+        }
+    }
     if (vec16_ok<T>(c, {feat, out, winners}))
         pool_select_fwd_kernel<T, V><<<grid_1d(m * (c / V)), 256, 0, st>>>(m, c, k, feat, nbr, rows, owner, out, winners);
     else
@@ -786,6 +807,15 @@ template <typename T>
 int launch_pool_select_bwd(int64_t m, int c, int k, const T *g, const int32_t *winners, Csr csr,
                            const int32_t *rows, const int32_t *owner, T *df, cudaStream_t st) {
     constexpr int V = 16 / sizeof(T);
+    if constexpr (sizeof(T) == 4) {
+        if (c % 8 == 0 && reinterpret_cast<uintptr_t>(g) % 32 == 0 && reinterpret_cast<uintptr_t>(winners) % 32 == 0 &&
+            reinterpret_cast<uintptr_t>(df) % 32 == 0) {
+            pool_select_bwd_kernel<T, 8><<<grid_1d(m * (c / 8)), 256, 0, st>>>(m, c, k, g, winners, csr, rows, owner,
+                                                                                df);
+            count_launch();
+            return check_launch("pool_select_bwd_kernel");
+        }
+    }
     if (vec16_ok<T>(c, {g, winners, df}))
         pool_select_bwd_kernel<T, V><<<grid_1d(m * (c / V)), 256, 0, st>>>(m, c, k, g, winners, csr, rows, owner, df);
     else
