@@ -338,6 +338,11 @@ def main():
         kernels[name] = {"ms": round(ms, 4), "bytes_per_point": b,
                          "GBps": round(b * n / ms / 1e6, 1) if b else None,
                          "frac": round(b * n / ms / 1e6 / hbm, 4) if b else None}
+        # the gathered bytes (K neighbour rows + positions per point, read
+        # through L1/L2) beside the compulsory ones -- the traffic the gathers actually move
+        gb = k * (4 * c + 4 * d)
+        kernels[name]["gathered_bytes_per_point"] = gb
+        kernels[name]["gathered_GBps"] = round(gb * n / ms / 1e6, 1)
         dp = ncu_datapipe(name)
         if dp:  # the binding on-chip limit (ncu), beside the HBM roofline
             kernels[name]["limiter"] = dict(dp, source="profiles/ncu_datapipe.json")
