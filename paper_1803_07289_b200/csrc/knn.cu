@@ -232,7 +232,7 @@ __global__ void sorted_points_kernel(int64_t n, int d, const PT *__restrict__ pt
         v.x = coord(pts, i, d, 0);
         v.y = d > 1 ? coord(pts, i, d, 1) : 0.0;
         v.z = d > 2 ? coord(pts, i, d, 2) : 0.0;
-        v.w = 0.0;
+        v.w = (double)i;  // the point's index rides along (one 32-byte load per candidate)
         sp[q] = v;
     }
 }
@@ -295,9 +295,9 @@ __global__ void __launch_bounds__(128)
                     const int64_t b = interleave_cell(gp, x, y, z);
                     const int32_t s1 = off[b + 1];
                     for (int32_t s = off[b]; s < s1; ++s) {
-                        const int32_t j = ent[s];
-                        if (j == i) continue;
                         const double4 pj = sp[s];
+                        const int32_t j = (int32_t)pj.w;
+                        if (j == i) continue;
                         double dist = 0.0, dv;
                         dv = __dsub_rn(pi.x, pj.x);
                         dist = __dadd_rn(dist, __dmul_rn(dv, dv));
