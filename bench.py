@@ -253,6 +253,8 @@ def main():
     pos = torch.floor(torch.rand(n, d, generator=gen, device=dev, dtype=torch.float64) * 2 ** 24) / 2 ** 24
     pos = pos.to(torch.float32)
     torch.cuda.synchronize()
+    _ops.spatial_order(pos)  # first call: module load + memory-pool growth (not reported)
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     order = _ops.spatial_order(pos)
     pos = pos[order.long()].contiguous()

@@ -203,12 +203,16 @@ __global__ void __launch_bounds__(256)
 }
 
 __global__ void bbox_final_kernel(int parts, const double *__restrict__ partial, double *__restrict__ box) {
-    if (threadIdx.x < 6) {
-        const int t = threadIdx.x;
-        double v = t < 3 ? DBL_MAX : -DBL_MAX;
-        for (int q = 0; q < parts; ++q) v = t < 3 ? fmin(v, partial[q * 6 + t]) : fmax(v, partial[q * 6 + t]);
-        box[t] = v;
+    // warp t reduces component t (0..2: min, 3..5: max) over the block partials
+    const int t = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (t >= 6) return;
+    double v = t < 3 ? DBL_MAX : -DBL_MAX;
+    for (int q = lane; q < parts; q += 32) v = t < 3 ? fmin(v, partial[q * 6 + t]) : fmax(v, partial[q * 6 + t]);
+    for (int o = 16; o > 0; o >>= 1) {
+        const double w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = t < 3 ? fmin(v, w) : fmax(v, w);
     }
+    if (lane == 0) box[t] = v;
 }
 
 template <typename PT>
@@ -373,7 +377,7 @@ static int cell_csr(int64_t n, int d, const PT *pts, GridParams *gp_out, int32_t
         double *partial = (double *)scratch_alloc(sizeof(double) * 6 * parts, st);
         if (!partial) return set_error(FC_ERR_CUDA, "scratch allocation failed (bbox)");
         bbox_partial_kernel<PT><<<parts, 256, 0, st>>>(n, d, pts, partial);
-        bbox_final_kernel<<<1, 32, 0, st>>>(parts, partial, box_d);
+        bbox_final_kernel<<<1, 192, 0, st>>>(parts, partial, box_d);
         count_launch();
         count_launch();
         scratch_free(partial, st);

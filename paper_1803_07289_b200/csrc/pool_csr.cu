@@ -490,6 +490,15 @@ __global__ void csr_sort_segments_kernel(int64_t buckets, const int32_t *__restr
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < buckets;
          b += (int64_t)gridDim.x * blockDim.x) {
         const int32_t lo = off[b], hi = off[b + 1];
+        if (hi - lo <= 1) continue;
+        if (hi - lo == 2) {
+            const int32_t x = ent[lo], y = ent[lo + 1];
+            if (x > y) {
+                ent[lo] = y;
+                ent[lo + 1] = x;
+            }
+            continue;
+        }
         if (hi - lo <= 16) {  // the usual case: sort in registers (bounded insertion sort)
             constexpr int32_t kBig = 0x7fffffff;
             int32_t v[16];
