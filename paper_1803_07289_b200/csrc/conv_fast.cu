@@ -95,10 +95,11 @@ __global__ void __launch_bounds__(1024) fwd_pack_b_kernel(const float *__restric
     __syncthreads();
     int e = 0;
     if (SPLIT) e = scale_exp(red[0]);
-    if (threadIdx.x == 0) binv[0] = exp2i(e);
+    if (blockIdx.x == 0 && threadIdx.x == 0) binv[0] = exp2i(e);
     const float sc = exp2i(-e);
     constexpr int BN = FwdL<SPLIT>::BN;
-    for (int idx = threadIdx.x; idx < BN * 256; idx += blockDim.x) {
+    // every block reduces the (L2-resident) max itself and packs its slice of the image
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < BN * 256; idx += gridDim.x * blockDim.x) {
         const int nn = idx >> 8, k = idx & 255;
         const int t = k >> 6, c = k & 63, cp = nn & 63;
         const float v = ((t < 3) ? theta[(cp * 64 + c) * 3 + t] : theta_b[cp * 64 + c]) * sc;
@@ -732,8 +733,8 @@ int tc_fast_forward(bool split, int64_t total, int64_t n, const float *feat, con
     uint8_t *img = (uint8_t *)scratch_alloc(bbytes + 256, st);
     if (!img) return set_error(FC_ERR_CUDA, "scratch allocation failed (fast forward)");
     float *binv = reinterpret_cast<float *>(img + bbytes);
-    if (split) fwd_pack_b_kernel<true><<<1, 1024, 0, st>>>(theta, theta_b, img, binv);
-    else fwd_pack_b_kernel<false><<<1, 1024, 0, st>>>(theta, theta_b, img, binv);
+    if (split) fwd_pack_b_kernel<true><<<FwdL<true>::BN * 256 / 1024, 1024, 0, st>>>(theta, theta_b, img, binv);
+    else fwd_pack_b_kernel<false><<<FwdL<false>::BN * 256 / 1024, 1024, 0, st>>>(theta, theta_b, img, binv);
     count_launch();
     FwdArgs a{};
     a.total = total;

@@ -121,10 +121,11 @@ __global__ void __launch_bounds__(1024)
     __syncthreads();
     float inv = 1.f, s = 1.f;
     if (SPLIT) s = split_scale(red[0], inv);
-    if (threadIdx.x == 0) binv[0] = inv;
+    if (blockIdx.x == 0 && threadIdx.x == 0) binv[0] = inv;
     const int KT = 4 * gc;
     const int bbytes = nout * KT * 2;
-    for (int idx = threadIdx.x; idx < nout * KT; idx += blockDim.x) {
+    // every block reduces the (L2-resident) max itself and packs its slice of the image
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nout * KT; idx += gridDim.x * blockDim.x) {
         const int nn = idx / KT, k = idx % KT;
         const int t = k / gc, c = k % gc;
         const int cp = reverse ? c : nn;
@@ -1229,7 +1230,8 @@ static int launch_tc(const TcArgs &a0, int cin, int cout, const float *theta, co
     uint8_t *img = (uint8_t *)scratch_alloc((size_t)L::B_BYTES * L::NSPLIT + 256, st);
     if (!img) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc)");
     float *binv = reinterpret_cast<float *>(img + (size_t)L::B_BYTES * L::NSPLIT);
-    tc_pack_b_kernel<SPLIT><<<1, 1024, 0, st>>>(cin, cout, theta, theta_b, REVERSE ? 1 : 0, NOUT, GC, img, binv);
+    tc_pack_b_kernel<SPLIT><<<(unsigned)ceil_div(NOUT * 4 * GC, 1024), 1024, 0, st>>>(cin, cout, theta, theta_b,
+                                                                                    REVERSE ? 1 : 0, NOUT, GC, img, binv);
     count_launch();
     a.bimg = img;
     a.binv = binv;
@@ -1298,8 +1300,9 @@ int tc_conv_forward_supported(int mode, int c_in, int d, int k, int c_out) {
 
 void launch_pack_b(bool split, int cin, int cout, const float *theta, const float *theta_b, int reverse, int nout,
                    int gc, uint8_t *img, float *binv, cudaStream_t st) {
-    if (split) tc_pack_b_kernel<true><<<1, 1024, 0, st>>>(cin, cout, theta, theta_b, reverse, nout, gc, img, binv);
-    else tc_pack_b_kernel<false><<<1, 1024, 0, st>>>(cin, cout, theta, theta_b, reverse, nout, gc, img, binv);
+    const unsigned g = (unsigned)ceil_div((int64_t)nout * 4 * gc, 1024);
+    if (split) tc_pack_b_kernel<true><<<g, 1024, 0, st>>>(cin, cout, theta, theta_b, reverse, nout, gc, img, binv);
+    else tc_pack_b_kernel<false><<<g, 1024, 0, st>>>(cin, cout, theta, theta_b, reverse, nout, gc, img, binv);
     count_launch();
 }
 
@@ -1378,7 +1381,7 @@ int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int c
         centre = (float *)scratch_alloc(sizeof(float) * total * 3, st);
         if (!img || !partial || !centre) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc backward)");
         float *binv = reinterpret_cast<float *>(img + img_bytes);
-        tc_pack_b_kernel<true><<<1, 1024, 0, st>>>(cin, cout, theta, theta_b, 0, cout, cin, img, binv);
+        tc_pack_b_kernel<true><<<(unsigned)ceil_div((int64_t)cout * 4 * cin, 1024), 1024, 0, st>>>(cin, cout, theta, theta_b, 0, cout, cin, img, binv);
         count_launch();
         DtArgs a{};
         a.total = total;
