@@ -279,18 +279,30 @@ template <typename T>
 __global__ void dtheta_reduce_kernel(int chunks, int cin, int d, int cout,
                                      const T *__restrict__ partial, T *__restrict__ d_theta,
                                      T *__restrict__ d_theta_b) {
+    // 8 lanes per output element: lane g adds the chunks of its contiguous block in ascending
+    // order (fp64), the 8 block sums are combined by a fixed xor tree -- a fixed order
+    // (deterministic), with 8x the loads in flight of one thread per element.
+    constexpr int G = 8;
     const int64_t E = (int64_t)cout * cin * (d + 1);
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E;
-         e += (int64_t)gridDim.x * blockDim.x) {
+    const int g = threadIdx.x % G;
+    const int per = (chunks + G - 1) / G;
+    const int c0 = g * per, c1 = min(chunks, c0 + per);
+    for (int64_t e0 = (int64_t)blockIdx.x * (blockDim.x / G); e0 < E; e0 += (int64_t)gridDim.x * (blockDim.x / G)) {
+        const int64_t e = e0 + threadIdx.x / G;
         double s = 0.0;
-        for (int ch = 0; ch < chunks; ++ch) s = __dadd_rn(s, (double)partial[(int64_t)ch * E + e]);
-        const int cp = (int)(e / (cin * (d + 1)));
-        const int kk = (int)(e % (cin * (d + 1)));
-        const int c = kk / (d + 1), t = kk % (d + 1);
-        if (t < d) {
-            if (d_theta) d_theta[((int64_t)cp * cin + c) * d + t] = (T)s;
-        } else if (d_theta_b) {
-            d_theta_b[(int64_t)cp * cin + c] = (T)s;
+        if (e < E)
+            for (int ch = c0; ch < c1; ++ch) s = __dadd_rn(s, (double)partial[(int64_t)ch * E + e]);
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+        if (g == 0 && e < E) {
+            const int cp = (int)(e / (cin * (d + 1)));
+            const int kk = (int)(e % (cin * (d + 1)));
+            const int c = kk / (d + 1), t = kk % (d + 1);
+            if (t < d) {
+                if (d_theta) d_theta[((int64_t)cp * cin + c) * d + t] = (T)s;
+            } else if (d_theta_b) {
+                d_theta_b[(int64_t)cp * cin + c] = (T)s;
+            }
         }
     }
 }
@@ -484,7 +496,7 @@ static int launch_dtheta_dp(int64_t total, int64_t n, int cin, int k, int cout, 
     dtheta_partial_kernel<T, DP, RPT><<<dim3((unsigned)chunks, (unsigned)slices), 256, smem, st>>>(
         total, n, cin, k, cout, feat, loc, nbr, g, partial, chunk_pts, tile);
     count_launch();
-    dtheta_reduce_kernel<T><<<grid_for(E, 256), 256, 0, st>>>((int)chunks, cin, DP, cout, partial, d_theta, d_theta_b);
+    dtheta_reduce_kernel<T><<<grid_for(E * 8, 256), 256, 0, st>>>((int)chunks, cin, DP, cout, partial, d_theta, d_theta_b);
     count_launch();
     scratch_free(partial, st);
     return check_launch("dtheta kernels");
@@ -501,7 +513,7 @@ template <typename T>
 int launch_dtheta_reduce(int chunks, int cin, int d, int cout, const T *partial, T *d_theta, T *d_theta_b,
                          cudaStream_t st) {
     const int64_t E = (int64_t)cout * cin * (d + 1);
-    dtheta_reduce_kernel<T><<<grid_for(E, 256), 256, 0, st>>>(chunks, cin, d, cout, partial, d_theta, d_theta_b);
+    dtheta_reduce_kernel<T><<<grid_for(E * 8, 256), 256, 0, st>>>(chunks, cin, d, cout, partial, d_theta, d_theta_b);
     count_launch();
     return check_launch("dtheta_reduce_kernel");
 }
