@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=131072)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fp64", action="store_true")
     return ap.parse_args()
 
 
@@ -111,6 +112,54 @@ def ncu_datapipe(name):
         return None
     return {"l1_data_pipe_frac": k["l1_data_pipe_frac"], "lsu_wavefronts_per_point": k["lsu_wavefronts_per_point"],
             "tc_smem_wavefronts_per_point": k["tc_smem_wavefronts_per_point"]}
+
+
+def tensor_pipe(kern, c_in, c_out, d, n, bf16_peak):
+    """Tensor-pipe side of the roofline for the contraction kernels: algorithmic contraction
+    flops per point (2*Din*(Dp+1)*Dout for the forward / d_features, the same
+    for d_theta) over the measured kernel time, against the measured dense bf16 peak, beside
+    ncu's sm__pipe_tensor_cycles_active for the same kernel (profiles/ncu_datapipe.json)."""
+    flops = 2 * c_in * (d + 1) * c_out
+    per_kernel = {"tc_forward": flops, "tc_dtheta": flops, "tc_reverse_dloc": 2 * flops, "tc_reverse": flops,
+                  "tc_reverse_dtheta": 2 * flops}
+    out = {"unit": "TFLOP/s", "peak": bf16_peak, "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense, burst)",
+           "flops_per_point": "2*Din*(Dp+1)*Dout per contraction (d_features + d_theta in the reverse kernel)",
+           "kernels": {}}
+    p = os.path.join(ROOT, "profiles", "ncu_datapipe.json")
+    ncu = {}
+    if os.path.exists(p):
+        with open(p) as fh:
+            ncu = json.load(fh).get("kernels", {})
+    for name, ms in kern.items():
+        if name not in per_kernel:
+            continue
+        tf = per_kernel[name] * n / (ms / 1e3) / 1e12
+        out["kernels"][name] = {"achieved": round(tf, 2), "frac": round(tf / bf16_peak, 4),
+                                "ncu_pipe_tensor_active_frac": ncu.get(name, {}).get("tensor_pipe_frac")}
+    return out
+
+
+def run_fp64(args, torch, _ops, feat, pos, nbr, csr, g, theta, theta_b, n, steps=2):
+    f64 = [t.double() for t in (feat, pos, g, theta, theta_b)]
+    torch.cuda.synchronize()
+
+    def step():
+        _ops.conv_forward(f64[0], f64[1], nbr, f64[3], f64[4], 1, n)
+        _ops.conv_backward(f64[2], f64[0], f64[1], nbr, csr, f64[3], f64[4], 1, n, need=(True, True, True, True))
+
+    step()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        step()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    del f64
+    return {"value": round(n / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 3), "steps": steps,
+            "dtype": "f64", "note": "reported only: the reference's fp64 arithmetic on the GPU (SIMT fp64, forward "
+                                    "bitwise equal to _native); the headline is the fp32-accurate engine"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -189,15 +238,14 @@ def cpu_kernels():
 
 
 def cpu_sample(n_sample, k, c, seed=4):
-    """A bounded sample of the workload: an n_sample-point cloud of the same construction."""
-    import torch
+    """A bounded sample of the workload: an n_sample-point cloud of the same construction.
+    Nothing from the product package is loaded on this leg: the inputs come from numpy
+    (paper_1803_07289_b200/core.py's generator is mirrored by oracle.synthetic_layer) and
+    the neighbour table from the oracle's OpenMP brute-force kNN."""
+    from oracle import oracle
 
-    from paper_1803_07289_b200 import _ops
-    from paper_1803_07289_b200.core import synthetic_layer
-
-    loc, feat, th, tb, up = synthetic_layer(seed, 0, n_sample, 3, c, c)
-    pts = torch.from_numpy(loc).cuda()
-    nbr = _ops.knn(pts, 1, n_sample, k).to(torch.int64).cpu().numpy()
+    loc, feat, th, tb, up = oracle.synthetic_layer(seed, 0, n_sample, 3, c, c)
+    nbr = oracle.knn_brute(loc, k)
     return loc, feat, th, tb, up, nbr
 
 
@@ -220,6 +268,48 @@ def time_cpu_step(kind, nat, sample):
         oracle.conv_backward(up, feat, loc, nbr, th, tb, True)
     t2 = time.perf_counter()
     return t1 - t0, t2 - t1
+
+
+# ------------------------------------------------------------------ workload
+def make_workload(n, k, c, rank, dev, d=3):
+    """The bench's synthetic layer on `dev` (tests/test_gpu_scale.py checks this exact
+    workload against the oracle): positions on the 2^-24 lattice (exact in fp32), spatially
+    ordered once, exact kNN table and reverse CSR; features / upstream N(0,1), theta /
+    theta_b 0.1 N(0,1).  Setup costs are timed with CUDA events and returned."""
+    import torch
+
+    from paper_1803_07289_b200 import _ops
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    pos = torch.floor(torch.rand(n, d, generator=gen, device=dev, dtype=torch.float64) * 2 ** 24) / 2 ** 24
+    pos = pos.to(torch.float32)
+    torch.cuda.synchronize()
+    _ops.spatial_order(pos)  # first call: module load + memory-pool growth (not reported)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    order = _ops.spatial_order(pos)
+    pos = pos[order.long()].contiguous()
+    torch.cuda.synchronize()
+    sort_ms = (time.perf_counter() - t0) * 1e3
+    feat = torch.randn(n, c, generator=gen, device=dev)
+    g = torch.randn(n, c, generator=gen, device=dev)
+    theta = 0.1 * torch.randn(c, c, d, generator=gen, device=dev)
+    theta_b = 0.1 * torch.randn(c, c, generator=gen, device=dev)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    nbr = _ops.knn(pos, 1, n, k)
+    e1.record()
+    torch.cuda.synchronize()
+    knn_ms = e0.elapsed_time(e1)
+    e0.record()
+    csr = _ops.csr_build(nbr, 1, n)
+    e1.record()
+    torch.cuda.synchronize()
+    csr_ms = e0.elapsed_time(e1)
+    return {"pos": pos, "feat": feat, "g": g, "theta": theta, "theta_b": theta_b, "nbr": nbr, "csr": csr,
+            "sort_ms": sort_ms, "knn_ms": knn_ms, "csr_ms": csr_ms}
 
 
 # ------------------------------------------------------------------ distributed
@@ -247,36 +337,9 @@ def main():
     from paper_1803_07289_b200 import _lib, _ops
 
     n, k, c, d = args.n, args.k, args.c, 3
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1234 + rank)
-    # positions on the 2^-24 lattice (exact in fp32), spatially ordered once
-    pos = torch.floor(torch.rand(n, d, generator=gen, device=dev, dtype=torch.float64) * 2 ** 24) / 2 ** 24
-    pos = pos.to(torch.float32)
-    torch.cuda.synchronize()
-    _ops.spatial_order(pos)  # first call: module load + memory-pool growth (not reported)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    order = _ops.spatial_order(pos)
-    pos = pos[order.long()].contiguous()
-    torch.cuda.synchronize()
-    sort_ms = (time.perf_counter() - t0) * 1e3
-    feat = torch.randn(n, c, generator=gen, device=dev)
-    g = torch.randn(n, c, generator=gen, device=dev)
-    theta = 0.1 * torch.randn(c, c, d, generator=gen, device=dev)
-    theta_b = 0.1 * torch.randn(c, c, generator=gen, device=dev)
-
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    nbr = _ops.knn(pos, 1, n, k)
-    e1.record()
-    torch.cuda.synchronize()
-    knn_ms = e0.elapsed_time(e1)
-    e0.record()
-    csr = _ops.csr_build(nbr, 1, n)
-    e1.record()
-    torch.cuda.synchronize()
-    csr_ms = e0.elapsed_time(e1)
+    w = make_workload(n, k, c, rank, dev)
+    pos, feat, g, theta, theta_b, nbr, csr = (w[x] for x in ("pos", "feat", "g", "theta", "theta_b", "nbr", "csr"))
+    sort_ms, knn_ms, csr_ms = w["sort_ms"], w["knn_ms"], w["csr_ms"]
 
     def step(phase_events=None):
         if phase_events:
@@ -332,6 +395,12 @@ def main():
             step()
     kern = {name: statistics.mean(v) for name, v in kt.times.items() if v and min(v) >= 0}
 
+    # ---------------- the reference's own arithmetic (fp64 engine, bitwise forward), reported
+    # only: the same workload cast to fp64, CUDA events, a few steps after the timed region
+    fp64 = None
+    if not args.no_fp64:
+        fp64 = run_fp64(args, torch, _ops, feat, pos, nbr, csr, g, theta, theta_b, n)
+
     hbm, bf16, src = peaks()
     fwd_b, bwd_b = algo_bytes_per_point(c, c, d, k)
     kernels = {}
@@ -366,6 +435,8 @@ def main():
                            "backward": {"ms": round(bwd_ms, 4), "bytes_per_point": bwd_b,
                                         "GBps": round(bwd_b * n / bwd_ms / 1e6, 1)}}}
 
+    roofline["tensor"] = tensor_pipe(kern, c, c, d, n, bf16)
+
     cpu = None
     if rank == 0 and not args.no_cpu:
         kind, nat = cpu_kernels()
@@ -392,6 +463,7 @@ def main():
             "gpu_launches": launches,
             "roofline": roofline,
             "cpu_baseline": cpu,
+            "fp64_engine": fp64,
             "e2e": e2e,
             "clocks": clk.summary(),
         }

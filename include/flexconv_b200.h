@@ -23,8 +23,9 @@
  *  - Outputs are OVERWRITTEN (the reference zero-fills then accumulates,
  *    flexops.py:123-126 -- same result).  Nullable outputs are skipped.
  *  - Work is enqueued on `stream` (cudaStream_t; NULL = legacy default stream);
- *    no entry point synchronises the host except fc_knn's grid path (reads a
- *    48-byte bounding box) and the *_check helpers documented as such.
+ *    no entry point synchronises the host except the validating reverse-CSR builders
+ *    (fc_csr_build, fc_record_csr_build: they report bad indices as a status code, like the
+ *    reference's range checks); fc_csr_build_async is their stream-ordered form.
  *  - Return FC_OK or an FC_ERR_* code; fc_last_error() holds the message (thread-local).
  */
 #ifndef FLEXCONV_B200_H
@@ -118,6 +119,12 @@ int fc_deconv_forward(int dtype, int mode, int64_t batch, int64_t n, int c_in, i
  * offsets [B*N + 1], entries [B*N*k].  Validates indices (FC_ERR_INDEX). */
 int fc_csr_build(int64_t batch, int64_t n, int k, const int32_t *neighbors,
                  int32_t *offsets, int32_t *entries, void *stream);
+/* The same build without the host synchronisation of the index check: *bad (device int32,
+ * caller-zeroed) receives the number of out-of-range entries.  Stream-ordered and
+ * CUDA-graph capturable; used where the table is valid by construction (fc_knn output) or
+ * was range-checked already (fc_check_indices when the neighbourhood was created). */
+int fc_csr_build_async(int64_t batch, int64_t n, int k, const int32_t *neighbors,
+                       int32_t *offsets, int32_t *entries, int32_t *bad, void *stream);
 
 /* ---- flex_pool (neighbourhood max-pool) --------------------------------------------
  * Replaces _native.max_pool_forward (_native.pyx:130-155) behind flexops.flex_max_pool

@@ -77,6 +77,9 @@ def _load():
         lib.fco_pool_backward.argtypes = [I, I, P, P, P]
         lib.fco_knn_brute.argtypes = [I, I, I, P, P, ctypes.c_int]
         lib.fco_knn_rows.argtypes = [I, I, I, P, P, I, P, ctypes.c_int]
+        lib.fco_conv_forward_rows.argtypes = [I, I, I, I, I, P, P, P, P, P, P, I, P, ctypes.c_int]
+        lib.fco_conv_backward_rows.argtypes = [I, I, I, I, I, P, P, P, P, P, P, P, I, P, P, ctypes.c_int]
+        lib.fco_conv_param_grads.argtypes = [I, I, I, I, I, P, P, P, P, P, P, ctypes.c_int]
         _lib = lib
     return _lib
 
@@ -175,3 +178,73 @@ def knn_rows(points, rows, k, num_threads=None):
     nt = num_threads or os.cpu_count() or 1
     _load().fco_knn_rows(n, d, k, _p(p), _p(r), r.shape[0], _p(out), nt)
     return out
+
+
+# ---------------------------------------------------------------- large-n checkers
+def conv_forward_rows(features, locations, neighbors, theta, theta_b, rows, num_threads=None):
+    """conv_forward restricted to the query rows (bitwise equal to those rows of conv_forward)."""
+    f, l, nb, th, tb, r = (_f64(features), _f64(locations), _i64(neighbors), _f64(theta), _f64(theta_b),
+                           _i64(rows))
+    n, C = f.shape
+    d = l.shape[1]
+    k = nb.shape[1]
+    cout = th.shape[0]
+    out = np.empty((r.shape[0], cout))
+    nt = num_threads or os.cpu_count() or 1
+    _load().fco_conv_forward_rows(n, C, d, k, cout, _p(f), _p(l), _p(nb), _p(th), _p(tb), _p(r), r.shape[0],
+                                  _p(out), nt)
+    return out
+
+
+def conv_backward_rows(upstream, features, locations, neighbors, theta, theta_b, rows, with_locations=True,
+                       num_threads=None):
+    """(d_features[rows], d_locations[rows] | None) of conv_backward, in the reference's
+    ascending-i addition order (bitwise equal to those rows of the serial conv_backward)."""
+    g, f, l, nb, th, tb = (_f64(upstream), _f64(features), _f64(locations), _i64(neighbors), _f64(theta),
+                           _f64(theta_b))
+    uniq, inv = np.unique(_i64(rows), return_inverse=True)  # the C routine wants distinct rows
+    r = _i64(uniq)
+    n, C = f.shape
+    d = l.shape[1]
+    k = nb.shape[1]
+    cout = th.shape[0]
+    df = np.empty((r.shape[0], C))
+    dl = np.empty((r.shape[0], d)) if with_locations else None
+    nt = num_threads or os.cpu_count() or 1
+    _load().fco_conv_backward_rows(n, C, d, k, cout, _p(g), _p(f), _p(l), _p(nb), _p(th), _p(tb), _p(r),
+                                   r.shape[0], _p(df), _p(dl), nt)
+    return df[inv], (dl[inv] if with_locations else None)
+
+
+def conv_param_grads(upstream, features, locations, neighbors, c_out=None, num_threads=None):
+    """(d_theta, d_theta_b) over all points: fp64, thread-parallel, per-thread partials added
+    in thread order (differs from the serial reference by fp64 regrouping only)."""
+    g, f, l, nb = _f64(upstream), _f64(features), _f64(locations), _i64(neighbors)
+    n, C = f.shape
+    d = l.shape[1]
+    k = nb.shape[1]
+    cout = g.shape[1] if c_out is None else int(c_out)
+    dth = np.empty((cout, C, d))
+    dtb = np.empty((cout, C))
+    nt = num_threads or os.cpu_count() or 1
+    _load().fco_conv_param_grads(n, C, d, k, cout, _p(g), _p(f), _p(l), _p(nb), _p(dth), _p(dtb), nt)
+    return dth, dtb
+
+
+# ---------------------------------------------------------------- synthetic inputs (numpy only)
+_MIX = 0x9E3779B97F4A7C15
+
+
+def synthetic_layer(seed, tag, n, d, c_in, c_out):
+    """The synthetic layer of SURVEY.md §8(d), drawn exactly as
+    paper_1803_07289_b200.core.synthetic_layer draws it (the reference's Philox Rng with
+    spawned substreams, /root/reference/pkg/src/flexconv/core.py:86-112), restated here with
+    numpy alone so the CPU-baseline legs of bench.py load nothing from the product package."""
+    stream = (0 * _MIX + int(tag) + 1) % 2 ** 64
+    g = np.random.Generator(np.random.Philox(key=[int(seed) % 2 ** 64, stream]))
+    loc = np.floor(g.uniform(0.0, 1.0, size=(n, d)) * 2.0 ** 24) / 2.0 ** 24
+    feat = g.standard_normal((n, c_in)).astype(np.float32).astype(np.float64)
+    theta = (g.standard_normal((c_out, c_in, d)) * 0.1).astype(np.float32).astype(np.float64)
+    theta_b = (g.standard_normal((c_out, c_in)) * 0.1).astype(np.float32).astype(np.float64)
+    up = g.standard_normal((n, c_out)).astype(np.float32).astype(np.float64)
+    return loc, feat, theta, theta_b, up

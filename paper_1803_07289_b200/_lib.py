@@ -44,6 +44,7 @@ SIGNATURES = {
     "fc_conv_backward": [_I, _I, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "fc_deconv_forward": [_I, _I, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "fc_csr_build": [_I64, _I64, _I, _P, _P, _P, _P],
+    "fc_csr_build_async": [_I64, _I64, _I, _P, _P, _P, _P, _P],
     "fc_pool_forward": [_I, _I64, _I64, _I, _I, _P, _P, _P, _P, _P],
     "fc_pool_backward": [_I, _I64, _I64, _I, _I, _P, _P, _P, _P, _P, _P],
     "fc_record_csr_build": [_I64, _I64, _I, _P, _P, _P, _P],

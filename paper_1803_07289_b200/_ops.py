@@ -41,6 +41,30 @@ def _p(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
 
+def _call(dev: torch.device, name: str, *args) -> None:
+    """One C-ABI call with `dev` as the current CUDA device: the library launches on the
+    current device, and the stream passed in belongs to `dev` (a tensor on cuda:1 while
+    cuda:0 is current would otherwise be launched into the wrong device's stream)."""
+    if dev.index is None or dev.index == torch.cuda.current_device():
+        _lib.call(name, *args)
+    else:
+        with torch.cuda.device(dev):
+            _lib.call(name, *args)
+
+
+def _shape(t: torch.Tensor, want: tuple, name: str) -> None:
+    if tuple(t.shape) != tuple(want):
+        raise ShapeMismatchError(f"{name} has shape {tuple(t.shape)}, expected {tuple(want)}")
+
+
+def _conv_shapes(theta, theta_b):
+    if theta.dim() != 3:
+        raise ShapeMismatchError(f"theta must be [C_out, C_in, d], got {tuple(theta.shape)}")
+    c_out, c_in, d = theta.shape
+    _shape(theta_b, (c_out, c_in), "theta_b")
+    return c_out, c_in, d
+
+
 def _stream(t: torch.Tensor):
     return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
 
@@ -55,13 +79,21 @@ def _need(t: torch.Tensor, name: str, dtype=None, device=None):
     return t.contiguous()
 
 
-def csr_build(nbr: torch.Tensor, batch: int, n: int):
-    """Reverse neighbourhood (stable counting sort): offsets [B*N+1], entries [B*N*K]."""
+def csr_build(nbr: torch.Tensor, batch: int, n: int, validate: bool = True):
+    """Reverse neighbourhood (stable counting sort): offsets [B*N+1], entries [B*N*K].
+    validate=True checks the indices and raises IndexOutOfRangeError (one host sync, like
+    the reference's range check); validate=False is the stream-ordered, graph-capturable
+    build for tables that are valid by construction or were checked already."""
     nbr = _need(nbr, "neighbors", torch.int32)
     k = nbr.shape[-1]
+    _shape(nbr, (batch * n, k), "neighbors")
     off = torch.empty(batch * n + 1, dtype=torch.int32, device=nbr.device)
     ent = torch.empty(batch * n * k, dtype=torch.int32, device=nbr.device)
-    _lib.call("fc_csr_build", batch, n, k, _p(nbr), _p(off), _p(ent), _stream(nbr))
+    if validate:
+        _call(nbr.device, "fc_csr_build", batch, n, k, _p(nbr), _p(off), _p(ent), _stream(nbr))
+    else:
+        bad = torch.zeros(1, dtype=torch.int32, device=nbr.device)
+        _call(nbr.device, "fc_csr_build_async", batch, n, k, _p(nbr), _p(off), _p(ent), _p(bad), _stream(nbr))
     return off, ent
 
 
@@ -72,10 +104,13 @@ def conv_forward(feat, loc, nbr, theta, theta_b, batch, n, mode="auto"):
     nbr = _need(nbr, "neighbors", torch.int32, dev)
     theta = _need(theta, "theta", dt, dev)
     theta_b = _need(theta_b, "theta_b", dt, dev)
-    c_out, c_in, d = theta.shape
+    c_out, c_in, d = _conv_shapes(theta, theta_b)
     k = nbr.shape[-1]
+    _shape(feat, (batch * n, c_in), "features")
+    _shape(loc, (batch * n, d), "locations")
+    _shape(nbr, (batch * n, k), "neighbors")
     out = torch.empty(batch * n, c_out, dtype=dt, device=dev)
-    _lib.call("fc_conv_forward", _dtype(feat), _mode(mode), batch, n, c_in, d, k, c_out, _p(feat), _p(loc),
+    _call(feat.device, "fc_conv_forward", _dtype(feat), _mode(mode), batch, n, c_in, d, k, c_out, _p(feat), _p(loc),
               _p(nbr), _p(theta), _p(theta_b), _p(out), _stream(feat))
     return out
 
@@ -90,15 +125,22 @@ def conv_backward(g, feat, loc, nbr, csr, theta, theta_b, batch, n, need=(True, 
     nbr = _need(nbr, "neighbors", torch.int32, dev)
     theta = _need(theta, "theta", dt, dev)
     theta_b = _need(theta_b, "theta_b", dt, dev)
-    c_out, c_in, d = theta.shape
+    c_out, c_in, d = _conv_shapes(theta, theta_b)
     k = nbr.shape[-1]
+    _shape(g, (batch * n, c_out), "upstream")
+    _shape(feat, (batch * n, c_in), "features")
+    _shape(loc, (batch * n, d), "locations")
+    _shape(nbr, (batch * n, k), "neighbors")
+    if csr is not None:
+        _shape(csr[0], (batch * n + 1,), "reverse offsets")
+        _shape(csr[1], (batch * n * k,), "reverse entries")
     want_df, want_dth, want_dtb, want_dl = need
     df = torch.empty(batch * n, c_in, dtype=dt, device=dev) if want_df else None
     dl = torch.empty(batch * n, d, dtype=dt, device=dev) if want_dl else None
     dth = torch.empty(c_out, c_in, d, dtype=dt, device=dev) if want_dth else None
     dtb = torch.empty(c_out, c_in, dtype=dt, device=dev) if want_dtb else None
     off, ent = csr if csr is not None else (None, None)
-    _lib.call("fc_conv_backward", _dtype(feat), _mode(mode), batch, n, c_in, d, k, c_out, _p(g), _p(feat),
+    _call(feat.device, "fc_conv_backward", _dtype(feat), _mode(mode), batch, n, c_in, d, k, c_out, _p(g), _p(feat),
               _p(loc), _p(nbr), _p(off), _p(ent), _p(theta), _p(theta_b), _p(df), _p(dl), _p(dth), _p(dtb),
               _stream(feat))
     return df, dth, dtb, dl
@@ -111,10 +153,14 @@ def deconv_forward(x, loc, csr, theta, theta_b, batch, n, k, mode="auto"):
     loc = _need(loc, "locations", dt, dev)
     theta = _need(theta, "theta", dt, dev)
     theta_b = _need(theta_b, "theta_b", dt, dev)
-    c_out, c_in, d = theta.shape
+    c_out, c_in, d = _conv_shapes(theta, theta_b)
+    _shape(x, (batch * n, c_out), "x")
+    _shape(loc, (batch * n, d), "locations")
     off, ent = csr
+    _shape(off, (batch * n + 1,), "reverse offsets")
+    _shape(ent, (batch * n * k,), "reverse entries")
     y = torch.empty(batch * n, c_in, dtype=dt, device=dev)
-    _lib.call("fc_deconv_forward", _dtype(x), _mode(mode), batch, n, c_in, d, k, c_out, _p(x), _p(loc),
+    _call(x.device, "fc_deconv_forward", _dtype(x), _mode(mode), batch, n, c_in, d, k, c_out, _p(x), _p(loc),
               _p(off), _p(ent), _p(theta), _p(theta_b), _p(y), _stream(x))
     return y
 
@@ -124,9 +170,11 @@ def pool_forward(feat, nbr, batch, n):
     nbr = _need(nbr, "neighbors", torch.int32, feat.device)
     c = feat.shape[-1]
     k = nbr.shape[-1]
+    _shape(feat, (batch * n, c), "features")
+    _shape(nbr, (batch * n, k), "neighbors")
     out = torch.empty_like(feat)
     am = torch.empty(feat.shape, dtype=torch.int32, device=feat.device)
-    _lib.call("fc_pool_forward", _dtype(feat), batch, n, c, k, _p(feat), _p(nbr), _p(out), _p(am),
+    _call(feat.device, "fc_pool_forward", _dtype(feat), batch, n, c, k, _p(feat), _p(nbr), _p(out), _p(am),
               _stream(feat))
     return out, am
 
@@ -135,9 +183,13 @@ def pool_backward(g, argmax, csr, batch, n, k):
     g = _need(g, "upstream")
     argmax = _need(argmax, "argmax", torch.int32, g.device)
     c = g.shape[-1]
+    _shape(g, (batch * n, c), "upstream")
+    _shape(argmax, (batch * n, c), "argmax")
     df = torch.empty_like(g)
     off, ent = csr
-    _lib.call("fc_pool_backward", _dtype(g), batch, n, c, k, _p(g), _p(argmax), _p(off), _p(ent), _p(df),
+    _shape(off, (batch * n + 1,), "reverse offsets")
+    _shape(ent, (batch * n * k,), "reverse entries")
+    _call(g.device, "fc_pool_backward", _dtype(g), batch, n, c, k, _p(g), _p(argmax), _p(off), _p(ent), _p(df),
               _stream(g))
     return df
 
@@ -148,9 +200,9 @@ def pool_backward_record(g, record, n_rows):
     n_up, c = g.shape
     off = torch.empty(n_rows * c + 1, dtype=torch.int32, device=g.device)
     ent = torch.empty(max(n_up * c, 1), dtype=torch.int32, device=g.device)
-    _lib.call("fc_record_csr_build", n_up, n_rows, c, _p(record), _p(off), _p(ent), _stream(g))
+    _call(g.device, "fc_record_csr_build", n_up, n_rows, c, _p(record), _p(off), _p(ent), _stream(g))
     df = torch.empty(n_rows, c, dtype=g.dtype, device=g.device)
-    _lib.call("fc_pool_backward_record", _dtype(g), n_up, n_rows, c, _p(g), _p(off), _p(ent), _p(df), _stream(g))
+    _call(g.device, "fc_pool_backward_record", _dtype(g), n_up, n_rows, c, _p(g), _p(off), _p(ent), _p(df), _stream(g))
     return df
 
 
@@ -158,7 +210,7 @@ def knn(points, batch, n, k, algo=_lib.KNN_AUTO):
     points = _need(points, "points")
     d = points.shape[-1]
     out = torch.empty(batch * n, k, dtype=torch.int32, device=points.device)
-    _lib.call("fc_knn", _dtype(points), batch, n, d, k, _p(points), _p(out), int(algo), _stream(points))
+    _call(points.device, "fc_knn", _dtype(points), batch, n, d, k, _p(points), _p(out), int(algo), _stream(points))
     return out
 
 
@@ -166,7 +218,7 @@ def spatial_order(points):
     points = _need(points, "points")
     n, d = points.shape
     order = torch.empty(n, dtype=torch.int32, device=points.device)
-    _lib.call("fc_spatial_order", _dtype(points), n, d, _p(points), _p(order), _stream(points))
+    _call(points.device, "fc_spatial_order", _dtype(points), n, d, _p(points), _p(order), _stream(points))
     return order
 
 
@@ -176,7 +228,7 @@ def inverse_density(points, nbr):
     nbr = _need(nbr, "neighbors", torch.int32)
     n, d = points.shape
     phi = torch.empty(n, dtype=torch.float64, device=points.device)
-    _lib.call("fc_inverse_density", n, d, nbr.shape[1], _p(points), _p(nbr), _p(phi), _stream(points))
+    _call(points.device, "fc_inverse_density", n, d, nbr.shape[1], _p(points), _p(nbr), _p(phi), _stream(points))
     return phi
 
 
@@ -184,7 +236,7 @@ def gather_rows(x, sel):
     x = _need(x, "features")
     sel = _need(sel, "selection", torch.int32, x.device)
     out = torch.empty(sel.numel(), x.shape[1], dtype=x.dtype, device=x.device)
-    _lib.call("fc_gather_rows", _dtype(x), sel.numel(), x.shape[1], _p(x), _p(sel), _p(out), _stream(x))
+    _call(x.device, "fc_gather_rows", _dtype(x), sel.numel(), x.shape[1], _p(x), _p(sel), _p(out), _stream(x))
     return out
 
 
@@ -192,7 +244,7 @@ def scatter_rows(x, sel, rows_out):
     x = _need(x, "features")
     sel = _need(sel, "selection", torch.int32, x.device)
     out = torch.empty(rows_out, x.shape[1], dtype=x.dtype, device=x.device)
-    _lib.call("fc_scatter_rows", _dtype(x), x.shape[0], rows_out, x.shape[1], _p(x), _p(sel), _p(out),
+    _call(x.device, "fc_scatter_rows", _dtype(x), x.shape[0], rows_out, x.shape[1], _p(x), _p(sel), _p(out),
               _stream(x))
     return out
 
@@ -201,7 +253,7 @@ def selection_owner(sel, n):
     """owner [n] int32: owner[sel[r]] = r (largest r on duplicates), -1 elsewhere."""
     sel = _need(sel, "selection", torch.int32)
     owner = torch.empty(n, dtype=torch.int32, device=sel.device)
-    _lib.call("fc_selection_owner", sel.numel(), n, _p(sel), _p(owner), _stream(sel))
+    _call(sel.device, "fc_selection_owner", sel.numel(), n, _p(sel), _p(owner), _stream(sel))
     return owner
 
 
@@ -214,7 +266,7 @@ def pool_select_forward(feat, nbr, m, rows=None, owner=None):
     c = feat.shape[1]
     out = torch.empty(m, c, dtype=feat.dtype, device=feat.device)
     win = torch.empty(m, c, dtype=torch.int32, device=feat.device)
-    _lib.call("fc_pool_select_forward", _dtype(feat), m, n, c, k, _p(feat), _p(nbr), _p(rows), _p(owner), _p(out),
+    _call(feat.device, "fc_pool_select_forward", _dtype(feat), m, n, c, k, _p(feat), _p(nbr), _p(rows), _p(owner), _p(out),
               _p(win), _stream(feat))
     return out, win
 
@@ -225,7 +277,7 @@ def pool_select_backward(g, winners, csr, m, n, k, rows=None, owner=None):
     winners = _need(winners, "winners", torch.int32, g.device)
     off, ent = csr
     df = torch.empty(m, g.shape[1], dtype=g.dtype, device=g.device)
-    _lib.call("fc_pool_select_backward", _dtype(g), m, n, g.shape[1], k, _p(g), _p(winners), _p(off), _p(ent),
+    _call(g.device, "fc_pool_select_backward", _dtype(g), m, n, g.shape[1], k, _p(g), _p(winners), _p(off), _p(ent),
               _p(rows), _p(owner), _p(df), _stream(g))
     return df
 
@@ -235,14 +287,14 @@ def narrow_indices(idx64, hi):
     idx64 = _need(idx64, "indices", torch.int64)
     out = torch.empty(idx64.shape, dtype=torch.int32, device=idx64.device)
     bad = torch.zeros(1, dtype=torch.int32, device=idx64.device)
-    _lib.call("fc_indices_to_i32", _p(idx64), _p(out), idx64.numel(), int(hi), _p(bad), _stream(idx64))
+    _call(idx64.device, "fc_indices_to_i32", _p(idx64), _p(out), idx64.numel(), int(hi), _p(bad), _stream(idx64))
     return out, bad
 
 
 def check_indices(idx32, hi):
     idx32 = _need(idx32, "indices", torch.int32)
     bad = torch.zeros(1, dtype=torch.int32, device=idx32.device)
-    _lib.call("fc_check_indices", _p(idx32), idx32.numel(), int(hi), _p(bad), _stream(idx32))
+    _call(idx32.device, "fc_check_indices", _p(idx32), idx32.numel(), int(hi), _p(bad), _stream(idx32))
     return bad
 
 
@@ -251,5 +303,5 @@ def count_nonfinite(x, bad=None):
     x = _need(x, "tensor")
     if bad is None:
         bad = torch.zeros(1, dtype=torch.int32, device=x.device)
-    _lib.call("fc_count_nonfinite", _dtype(x), _p(x), x.numel(), _p(bad), _stream(x))
+    _call(x.device, "fc_count_nonfinite", _dtype(x), _p(x), x.numel(), _p(bad), _stream(x))
     return bad

@@ -58,16 +58,13 @@ void prof_end(cudaStream_t st) {
 // Stream-ordered scratch from the device's default memory pool (kept resident: the
 // release threshold is raised once so repeated calls do not return memory to the OS).
 void *scratch_alloc(size_t bytes, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        int dev = 0;
-        cudaGetDevice(&dev);
+    static uint64_t configured = 0;
+    if (first_use_on_device(configured)) {
         cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        if (cudaDeviceGetDefaultMemPool(&pool, current_device()) == cudaSuccess) {
             uint64_t thr = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
-        configured = true;
     }
     void *p = nullptr;
     if (bytes == 0) bytes = 16;
@@ -246,16 +243,21 @@ int fc_conv_backward(int dtype, int mode, int64_t batch, int64_t n, int c_in, in
             if (rc) return rc;
         }
         if (d_features || d_locations) {
-            T *centre = nullptr;
+            Scratch centre_buf;
             if (d_locations) {
-                centre = (T *)scratch_alloc(sizeof(T) * total * d, st);
-                if (!centre) return set_error(FC_ERR_CUDA, "scratch allocation failed");
-                rc = launch_dloc_centre<T>(total, n, d, c_in, k, c_out, f, neighbors, g, th, centre, st);
+                centre_buf.alloc(sizeof(T) * total * d, st);
+                if (!centre_buf.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+                rc = launch_dloc_centre<T>(total, n, d, c_in, k, c_out, f, neighbors, g, th, centre_buf.as<T>(), st);
                 if (rc) return rc;
             }
+            T *centre = centre_buf.as<T>();
             T *df = (T *)d_features;
-            T *df_scratch = nullptr;
-            if (!df) df = df_scratch = (T *)scratch_alloc(sizeof(T) * total * c_in, st);
+            Scratch df_buf;
+            if (!df) {
+                df_buf.alloc(sizeof(T) * total * c_in, st);
+                if (!df_buf.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+                df = df_buf.as<T>();
+            }
             const bool tc = dtype == FC_F32 && mode != FC_MODE_SIMT && !d_locations &&
                             tc_reverse_supported(mode, c_out, d, c_in);
             if (tc) {
@@ -263,14 +265,12 @@ int fc_conv_backward(int dtype, int mode, int64_t batch, int64_t n, int c_in, in
                                     Csr{rev_offsets, rev_entries}, (const float *)th, (const float *)theta_b,
                                     (float *)df, st);
             } else {
-                T *wr = (T *)scratch_alloc((size_t)c_out * c_in * (d + 1) * sizeof(T), st);
-                launch_pack<T>(c_in, d, c_out, th, (const T *)theta_b, nullptr, wr, st);
+                Scratch wr((size_t)c_out * c_in * (d + 1) * sizeof(T), st);
+                if (!wr.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+                launch_pack<T>(c_in, d, c_out, th, (const T *)theta_b, nullptr, wr.as<T>(), st);
                 rc = launch_gmc<T>(true, total, n, d, c_out, k, c_in, g, l, neighbors, Csr{rev_offsets, rev_entries},
-                                   wr, df, f, th, centre, (T *)d_locations, st);
-                scratch_free(wr, st);
+                                   wr.as<T>(), df, f, th, centre, (T *)d_locations, st);
             }
-            scratch_free(df_scratch, st);
-            scratch_free(centre, st);
         }
         return rc;
     };
@@ -312,17 +312,25 @@ int fc_csr_build(int64_t batch, int64_t n, int k, const int32_t *neighbors, int3
     if (batch < 1 || n < 1 || k < 1) return set_error(FC_ERR_EMPTY, "empty neighbourhood");
     if (batch * n * (int64_t)k >= (int64_t)INT32_MAX) return set_error(FC_ERR_UNSUPPORTED, "B*N*k exceeds int32");
     cudaStream_t st = ST(stream);
-    int32_t *bad = (int32_t *)scratch_alloc(sizeof(int32_t), st);
-    cudaMemsetAsync(bad, 0, sizeof(int32_t), st);
-    int rc = build_csr(neighbors, batch * n * k, BucketFn{0, n, k}, batch * n, offsets, entries, bad, st);
+    Scratch bad(sizeof(int32_t), st);
+    if (!bad.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (csr)");
+    cudaMemsetAsync(bad.p, 0, sizeof(int32_t), st);
+    int rc = build_csr(neighbors, batch * n * k, BucketFn{0, n, k}, batch * n, offsets, entries, bad.as<int32_t>(), st);
     int32_t bad_h = 0;
-    cudaMemcpyAsync(&bad_h, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
-    scratch_free(bad, st);
+    cudaMemcpyAsync(&bad_h, bad.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     if (rc) return rc;
     if (int rc2 = check_launch("fc_csr_build")) return rc2;
     if (bad_h) return set_error(FC_ERR_INDEX, "neighbor index out of [0, n) (%d entries)", bad_h);
     return FC_OK;
+}
+
+int fc_csr_build_async(int64_t batch, int64_t n, int k, const int32_t *neighbors, int32_t *offsets,
+                       int32_t *entries, int32_t *bad, void *stream) {
+    if (batch < 1 || n < 1 || k < 1) return set_error(FC_ERR_EMPTY, "empty neighbourhood");
+    if (batch * n * (int64_t)k >= (int64_t)INT32_MAX) return set_error(FC_ERR_UNSUPPORTED, "B*N*k exceeds int32");
+    if (!bad) return set_error(FC_ERR_CONFIG, "fc_csr_build_async needs a device counter for bad indices");
+    return build_csr(neighbors, batch * n * k, BucketFn{0, n, k}, batch * n, offsets, entries, bad, ST(stream));
 }
 
 int fc_pool_forward(int dtype, int64_t batch, int64_t n, int c, int k, const void *features,
@@ -355,12 +363,12 @@ int fc_record_csr_build(int64_t n_up, int64_t n_rows, int c, const int32_t *reco
     if (n_up * (int64_t)c >= (int64_t)INT32_MAX || n_rows * (int64_t)c >= (int64_t)INT32_MAX)
         return set_error(FC_ERR_UNSUPPORTED, "record too large for int32 slots");
     cudaStream_t st = ST(stream);
-    int32_t *bad = (int32_t *)scratch_alloc(sizeof(int32_t), st);
-    cudaMemsetAsync(bad, 0, sizeof(int32_t), st);
-    int rc = build_csr(record, n_up * c, BucketFn{1, n_rows, c}, n_rows * c, offsets, entries, bad, st);
+    Scratch bad(sizeof(int32_t), st);
+    if (!bad.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (record csr)");
+    cudaMemsetAsync(bad.p, 0, sizeof(int32_t), st);
+    int rc = build_csr(record, n_up * c, BucketFn{1, n_rows, c}, n_rows * c, offsets, entries, bad.as<int32_t>(), st);
     int32_t bad_h = 0;
-    cudaMemcpyAsync(&bad_h, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
-    scratch_free(bad, st);
+    cudaMemcpyAsync(&bad_h, bad.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     if (rc) return rc;
     if (bad_h) return set_error(FC_ERR_INDEX, "corrupt pool record: winner index out of range");

@@ -765,32 +765,28 @@ int tc_fast_forward(bool split, int64_t total, int64_t n, const float *feat, con
     }
     if (!narrow) {
         if (split) {
-            static bool attr = false;
-            if (!attr) {
+            static uint64_t attr = 0;
+            if (first_use_on_device(attr)) {
                 cudaFuncSetAttribute(tc_fwd64w_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdL<true>::SMEM_ALLOC);
-                attr = true;
             }
             tc_fwd64w_kernel<true><<<grid, wThreads, FwdL<true>::SMEM_ALLOC, st>>>(a);
         } else {
-            static bool attr = false;
-            if (!attr) {
+            static uint64_t attr = 0;
+            if (first_use_on_device(attr)) {
                 cudaFuncSetAttribute(tc_fwd64w_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdL<false>::SMEM_ALLOC);
-                attr = true;
             }
             tc_fwd64w_kernel<false><<<grid, wThreads, FwdL<false>::SMEM_ALLOC, st>>>(a);
         }
     } else if (split) {
-        static bool attr = false;
-        if (!attr) {
+        static uint64_t attr = 0;
+        if (first_use_on_device(attr)) {
             cudaFuncSetAttribute(tc_fwd64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdL<true>::SMEM_ALLOC);
-            attr = true;
         }
         tc_fwd64_kernel<true><<<grid, kThreads, FwdL<true>::SMEM_ALLOC, st>>>(a);
     } else {
-        static bool attr = false;
-        if (!attr) {
+        static uint64_t attr = 0;
+        if (first_use_on_device(attr)) {
             cudaFuncSetAttribute(tc_fwd64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdL<false>::SMEM_ALLOC);
-            attr = true;
         }
         tc_fwd64_kernel<false><<<grid, kThreads, FwdL<false>::SMEM_ALLOC, st>>>(a);
     }

@@ -519,10 +519,9 @@ int tc_fast_dtheta(int64_t total, int64_t n, const float *feat, const float *loc
         if (!clk) cudaMalloc(&clk, sizeof(unsigned long long) * 148 * 24 * 4);
         a.clk = clk;
     }
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr = 0;
+    if (first_use_on_device(attr)) {
         cudaFuncSetAttribute(tc_dt64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DtL::SMEM_ALLOC);
-        attr = true;
     }
     prof_begin("tc_dtheta", st);
     tc_dt64_kernel<<<grid, dThreads, DtL::SMEM_ALLOC, st>>>(a);

@@ -1085,17 +1085,15 @@ int tc_fast_reverse(bool split, int64_t total, int k, const float *rows, const f
 #define FC_LAUNCH_REV(S, D)                                                                                     \
     do {                                                                                                        \
         if (narrow) {                                                                                           \
-            static bool attr = false;                                                                           \
-            if (!attr) {                                                                                        \
+            static uint64_t attr = 0;                                                                           \
+            if (first_use_on_device(attr)) {                                                                                        \
                 cudaFuncSetAttribute(tc_rev64_kernel<S, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, RevL<S>::SMEM_ALLOC); \
-                attr = true;                                                                                    \
             }                                                                                                   \
             tc_rev64_kernel<S, D><<<grid, rThreads, RevL<S>::SMEM_ALLOC, st>>>(a);                              \
         } else {                                                                                                \
-            static bool attr = false;                                                                           \
-            if (!attr) {                                                                                        \
+            static uint64_t attr = 0;                                                                           \
+            if (first_use_on_device(attr)) {                                                                                        \
                 cudaFuncSetAttribute(tc_rev64w_kernel<S, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, RevL<S>::SMEM_ALLOC); \
-                attr = true;                                                                                    \
             }                                                                                                   \
             tc_rev64w_kernel<S, D><<<grid, wrThreads, RevL<S>::SMEM_ALLOC, st>>>(a);                            \
         }                                                                                                       \

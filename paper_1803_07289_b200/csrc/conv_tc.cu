@@ -1236,11 +1236,10 @@ static int launch_tc(const TcArgs &a0, int cin, int cout, const float *theta, co
     a.bimg = img;
     a.binv = binv;
     a.num_tiles = ceil_div(a.total, kTcM);
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr = 0;
+    if (first_use_on_device(attr)) {
         cudaFuncSetAttribute(tc_gmc_kernel<GC, NOUT, SPLIT, REVERSE, KFIX, DLOC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              L::SMEM);
-        attr = true;
     }
     const int grid = (int)std::min<int64_t>(a.num_tiles, num_sms());
     prof_begin(REVERSE ? (DLOC ? "tc_reverse_dloc" : "tc_reverse") : "tc_forward", st);
@@ -1362,24 +1361,27 @@ int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int c
     using L = DtLayout;
     const int64_t num_tiles = ceil_div(total, kTcM);
     const int grid = (int)std::min<int64_t>(num_tiles, num_sms());
+    Scratch centre_buf;
     float *centre = nullptr;
     int rc = FC_OK;
     if ((d_theta || d_theta_b || d_locations) && k == kSlots && fast_enabled()) {
         if (d_locations) {
-            centre = (float *)scratch_alloc(sizeof(float) * total * 3, st);
-            if (!centre) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc backward)");
+            centre_buf.alloc(sizeof(float) * total * 3, st);
+            if (!centre_buf.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc backward)");
+            centre = centre_buf.as<float>();
         }
         rc = tc_fast_dtheta(total, n, feat, loc, nbr, g, theta, theta_b, d_theta, d_theta_b, centre, st);
-        if (rc) {
-            scratch_free(centre, st);
-            return rc;
-        }
+        if (rc) return rc;
     } else if (d_theta || d_theta_b || d_locations) {
         const size_t img_bytes = (size_t)cout * 4 * cin * 2 * 2;
-        uint8_t *img = (uint8_t *)scratch_alloc(img_bytes + 256, st);
-        float *partial = (float *)scratch_alloc(sizeof(float) * 2 * grid * cout * cin * 4, st);
-        centre = (float *)scratch_alloc(sizeof(float) * total * 3, st);
-        if (!img || !partial || !centre) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc backward)");
+        Scratch img_buf(img_bytes + 256, st);
+        Scratch partial_buf(sizeof(float) * 2 * grid * cout * cin * 4, st);
+        centre_buf.alloc(sizeof(float) * total * 3, st);
+        if (!img_buf.ok() || !partial_buf.ok() || !centre_buf.ok())
+            return set_error(FC_ERR_CUDA, "scratch allocation failed (tc backward)");
+        uint8_t *img = img_buf.as<uint8_t>();
+        float *partial = partial_buf.as<float>();
+        centre = centre_buf.as<float>();
         float *binv = reinterpret_cast<float *>(img + img_bytes);
         tc_pack_b_kernel<true><<<(unsigned)ceil_div((int64_t)cout * 4 * cin, 1024), 1024, 0, st>>>(cin, cout, theta, theta_b, 0, cout, cin, img, binv);
         count_launch();
@@ -1396,18 +1398,16 @@ int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int c
         a.partial = partial;
         a.centre = centre;
         a.num_tiles = num_tiles;
-        static bool attr8 = false, attr0 = false;
+        static uint64_t attr8 = 0, attr0 = 0;
         prof_begin("tc_dtheta", st);
         if (k == kSlots) {
-            if (!attr8) {
+            if (first_use_on_device(attr8)) {
                 cudaFuncSetAttribute(tc_dtheta_kernel<kSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
-                attr8 = true;
             }
             tc_dtheta_kernel<kSlots><<<grid, kTcThreads, L::SMEM, st>>>(a);
         } else {
-            if (!attr0) {
+            if (first_use_on_device(attr0)) {
                 cudaFuncSetAttribute(tc_dtheta_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
-                attr0 = true;
             }
             tc_dtheta_kernel<0><<<grid, kTcThreads, L::SMEM, st>>>(a);
         }
@@ -1416,14 +1416,16 @@ int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int c
         rc = check_launch("tc_dtheta_kernel");
         if (!rc && (d_theta || d_theta_b))
             rc = launch_dtheta_reduce<float>(2 * grid, cin, 3, cout, partial, d_theta, d_theta_b, st);
-        scratch_free(img, st);
-        scratch_free(partial, st);
         if (rc) return rc;
     }
     if (d_features || d_locations) {
         float *df = d_features;
-        float *df_scratch = nullptr;
-        if (!df) df = df_scratch = (float *)scratch_alloc(sizeof(float) * total * cin, st);
+        Scratch df_buf;
+        if (!df) {
+            df_buf.alloc(sizeof(float) * total * cin, st);
+            if (!df_buf.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc backward)");
+            df = df_buf.as<float>();
+        }
         TcArgs a{};
         a.total = total;
         a.n = n;
@@ -1437,9 +1439,7 @@ int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int c
         a.dloc = d_locations;
         if (mode == FC_MODE_TC_BF16) rc = dispatch_tc<false, true>(cout, cin, a, cin, cout, theta, theta_b, st);
         else rc = dispatch_tc<true, true>(cout, cin, a, cin, cout, theta, theta_b, st);
-        scratch_free(df_scratch, st);
     }
-    scratch_free(centre, st);
     return rc;
 }
 

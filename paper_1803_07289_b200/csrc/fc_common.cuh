@@ -48,14 +48,32 @@ struct Ar<double> {
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+inline int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+
+// Per-device one-time set-up (kernel attributes, pool configuration): `mask` holds one bit
+// per device ordinal; returns true the first time it is called on the current device.
+// (Launches go to the caller's current device, so per-process flags would leave a second
+// GPU driven from the same process without its >48 KB shared-memory attributes.)
+inline bool first_use_on_device(uint64_t &mask) {
+    const int dev = current_device() & 63;
+    const uint64_t bit = 1ull << dev;
+    if (__atomic_fetch_or(&mask, bit, __ATOMIC_ACQ_REL) & bit) return false;
+    return true;
+}
+
 inline int num_sms() {
-    static int sms = -1;
-    if (sms < 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+    static int sms[64] = {0};
+    const int dev = current_device() & 63;
+    if (sms[dev] <= 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        sms[dev] = v;
     }
-    return sms;
+    return sms[dev];
 }
 
 // Reverse (transposed) neighbourhood in CSR form: for global point j,
@@ -86,6 +104,26 @@ int build_csr(const int32_t *keys, int64_t count, BucketFn bf, int64_t buckets, 
               int32_t *ent, int32_t *bad_dev, cudaStream_t st);
 void *scratch_alloc(size_t bytes, cudaStream_t st);
 void scratch_free(void *p, cudaStream_t st);
+
+// RAII stream-ordered scratch: released (stream-ordered) on every return path, so an early
+// error return can neither leak nor hand a kernel a null pointer unnoticed (check `ok()`).
+struct Scratch {
+    void *p = nullptr;
+    cudaStream_t st = nullptr;
+    Scratch() = default;
+    Scratch(size_t bytes, cudaStream_t s) : p(scratch_alloc(bytes, s)), st(s) {}
+    ~Scratch() { scratch_free(p, st); }
+    Scratch(const Scratch &) = delete;
+    Scratch &operator=(const Scratch &) = delete;
+    void alloc(size_t bytes, cudaStream_t s) {
+        scratch_free(p, st);
+        st = s;
+        p = scratch_alloc(bytes, s);
+    }
+    template <typename T>
+    T *as() const { return static_cast<T *>(p); }
+    bool ok() const { return p != nullptr; }
+};
 void count_launch();
 // per-kernel event timing (fc_profile_*); no-ops unless enabled
 void prof_begin(const char *name, cudaStream_t st);

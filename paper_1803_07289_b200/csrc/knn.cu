@@ -215,9 +215,52 @@ __global__ void bbox_final_kernel(int parts, const double *__restrict__ partial,
     if (lane == 0) box[t] = v;
 }
 
+// Grid parameters from the bounding box, on the device (no host read-back: the kNN and the
+// spatial order are stream-ordered and CUDA-graph capturable).  Cell edge h targets `ppc`
+// points per cell; per-axis resolution is clamped to 1024 cells; the Morton bucket space
+// 2^(sum of per-axis bits) must fit the caller's capacity `cap` (sized on the host from n
+// alone), else h grows until it does.  Any h > 0 gives the same (exact) neighbour rows.
+__global__ void grid_params_kernel(const double *__restrict__ box, int64_t n, int d, double ppc, int64_t cap,
+                                   GridParams *__restrict__ gp_out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    GridParams gp{};
+    gp.d = d;
+    double ext[3];
+    int deff = 0;
+    double vol = 1.0;
+    for (int t = 0; t < 3; ++t) {
+        ext[t] = t < d ? box[3 + t] - box[t] : 0.0;
+        gp.lo[t] = t < d ? box[t] : 0.0;
+        if (ext[t] > 0) {
+            ++deff;
+            vol *= ext[t];
+        }
+    }
+    const double target_cells = fmax(1.0, (double)n / ppc);
+    double h = deff > 0 ? pow(vol / target_cells, 1.0 / deff) : 1.0;
+    if (!(h > 0) || !isfinite(h)) h = 1.0;
+    for (int t = 0; t < 3; ++t)
+        if (ext[t] > 0 && ext[t] / h > 1024.0) h = ext[t] / 1024.0;
+    for (;;) {
+        int total_bits = 0;
+        for (int t = 0; t < 3; ++t) {
+            gp.G[t] = ext[t] > 0 ? (int)fmin(1024.0, floor(ext[t] / h) + 1.0) : 1;
+            int b = 0;
+            while ((1 << b) < gp.G[t]) ++b;
+            gp.bits[t] = b;
+            total_bits += b;
+        }
+        if (((int64_t)1 << total_bits) <= cap) break;
+        h *= 1.25;
+    }
+    gp.h = h;
+    *gp_out = gp;
+}
+
 template <typename PT>
-__global__ void cell_bucket_kernel(int64_t n, int d, const PT *__restrict__ pts, GridParams gp,
+__global__ void cell_bucket_kernel(int64_t n, int d, const PT *__restrict__ pts, const GridParams *__restrict__ gpp,
                                    int32_t *__restrict__ bucket) {
+    const GridParams gp = *gpp;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         int c[3] = {0, 0, 0};
@@ -256,9 +299,10 @@ template <int KK>
 __global__ void __launch_bounds__(128)
     knn_grid_query_kernel(int64_t n, int k, const double4 *__restrict__ sp,
                           const int32_t *__restrict__ ent, const int32_t *__restrict__ off,
-                          GridParams gp, int32_t *__restrict__ out) {
+                          const GridParams *__restrict__ gpp, int32_t *__restrict__ out) {
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n) return;
+    const GridParams gp = *gpp;
     const int32_t i = ent[q];
     const double4 pi = sp[q];
     const double px[3] = {pi.x, pi.y, pi.z};
@@ -367,77 +411,59 @@ static int knn_brute(int64_t batch, int64_t n, int d, int k, const PT *pts, int3
     return check_launch("knn_brute");
 }
 
-// Build the cell CSR of one cloud; returns grid params.  off [buckets+1], ent [n].
+// Bucket capacity of the cell CSR of an n-point cloud: the Morton space 2^(bits) of a grid
+// with ~n/ppc cells, each axis rounded up to a power of two (grid_params_kernel keeps the
+// actual space within it).
+static int64_t cell_capacity(int64_t n, double ppc) {
+    const double target = std::max(1.0, (double)n / ppc);
+    int64_t cap = 64;
+    while ((double)cap < 4.0 * target) cap <<= 1;
+    return std::min<int64_t>(cap, (int64_t)1 << 30);
+}
+
+// Build the cell CSR of one cloud, entirely stream-ordered: bounding box -> grid parameters
+// (device) -> cell keys -> stable counting sort.  gp_d (device), off [cap+1], ent [n].
 template <typename PT>
-static int cell_csr(int64_t n, int d, const PT *pts, GridParams *gp_out, int32_t **off_out,
-                    int32_t **ent_out, int64_t *buckets_out, cudaStream_t st, double ppc_default = 2.0) {
-    double *box_d = (double *)scratch_alloc(6 * sizeof(double), st);
-    {
-        const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)num_sms() * 4));
-        double *partial = (double *)scratch_alloc(sizeof(double) * 6 * parts, st);
-        if (!partial) return set_error(FC_ERR_CUDA, "scratch allocation failed (bbox)");
-        bbox_partial_kernel<PT><<<parts, 256, 0, st>>>(n, d, pts, partial);
-        bbox_final_kernel<<<1, 192, 0, st>>>(parts, partial, box_d);
-        count_launch();
-        count_launch();
-        scratch_free(partial, st);
-    }
-    double box[6];
-    cudaMemcpyAsync(box, box_d, sizeof(box), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    scratch_free(box_d, st);
-    if (int rc = check_launch("bbox")) return rc;
-    GridParams gp{};
-    gp.d = d;
-    double ext[3];
-    int deff = 0;
-    double vol = 1.0;
-    for (int t = 0; t < 3; ++t) {
-        ext[t] = t < d ? box[3 + t] - box[t] : 0.0;
-        gp.lo[t] = t < d ? box[t] : 0.0;
-        if (ext[t] > 0) {
-            ++deff;
-            vol *= ext[t];
-        }
-    }
+static int cell_csr(int64_t n, int d, const PT *pts, GridParams *gp_d, int32_t **off_out, int32_t **ent_out,
+                    int64_t *buckets_out, cudaStream_t st, double ppc_default = 2.0) {
     static const double ppc_env = [] {  // points per cell override (FC_KNN_PPC, for tuning)
         const char *e = getenv("FC_KNN_PPC");
         return e ? atof(e) : 0.0;
     }();
     const double ppc = ppc_env > 0.0 ? ppc_env : ppc_default;
-    const double target_cells = std::max(1.0, (double)n / ppc);
-    double h = deff > 0 ? std::pow(vol / target_cells, 1.0 / deff) : 1.0;
-    if (!(h > 0) || !std::isfinite(h)) h = 1.0;
-    // clamp per-axis resolution to 1024 cells
-    for (int t = 0; t < 3; ++t)
-        if (ext[t] > 0 && ext[t] / h > 1024.0) h = ext[t] / 1024.0;
-    gp.h = h;
-    int total_bits = 0;
-    for (int t = 0; t < 3; ++t) {
-        gp.G[t] = ext[t] > 0 ? (int)std::min(1024.0, std::floor(ext[t] / h) + 1.0) : 1;
-        int b = 0;
-        while ((1 << b) < gp.G[t]) ++b;
-        gp.bits[t] = b;
-        total_bits += b;
+    const int64_t cap = cell_capacity(n, ppc);
+    {
+        const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)num_sms() * 4));
+        Scratch partial(sizeof(double) * 6 * parts, st), box(6 * sizeof(double), st);
+        if (!partial.ok() || !box.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (bbox)");
+        bbox_partial_kernel<PT><<<parts, 256, 0, st>>>(n, d, pts, partial.as<double>());
+        bbox_final_kernel<<<1, 192, 0, st>>>(parts, partial.as<double>(), box.as<double>());
+        grid_params_kernel<<<1, 32, 0, st>>>(box.as<double>(), n, d, ppc, cap, gp_d);
+        count_launch();
+        count_launch();
+        count_launch();
     }
-    if (total_bits > 30) return set_error(FC_ERR_UNSUPPORTED, "kNN grid too fine (%d bits)", total_bits);
-    const int64_t buckets = (int64_t)1 << total_bits;
-    int32_t *bucket = (int32_t *)scratch_alloc(sizeof(int32_t) * n, st);
-    int32_t *off = (int32_t *)scratch_alloc(sizeof(int32_t) * (buckets + 1), st);
+    if (int rc = check_launch("bbox")) return rc;
+    Scratch bucket(sizeof(int32_t) * n, st), bad(sizeof(int32_t), st);
+    int32_t *off = (int32_t *)scratch_alloc(sizeof(int32_t) * (cap + 1), st);
     int32_t *ent = (int32_t *)scratch_alloc(sizeof(int32_t) * n, st);
-    int32_t *bad = (int32_t *)scratch_alloc(sizeof(int32_t), st);
-    if (!bucket || !off || !ent || !bad) return set_error(FC_ERR_CUDA, "scratch allocation failed (grid)");
-    cudaMemsetAsync(bad, 0, sizeof(int32_t), st);
-    cell_bucket_kernel<PT><<<grid_1d(n), 256, 0, st>>>(n, d, pts, gp, bucket);
+    if (!bucket.ok() || !off || !ent || !bad.ok()) {
+        scratch_free(off, st);
+        scratch_free(ent, st);
+        return set_error(FC_ERR_CUDA, "scratch allocation failed (grid)");
+    }
+    cudaMemsetAsync(bad.p, 0, sizeof(int32_t), st);
+    cell_bucket_kernel<PT><<<grid_1d(n), 256, 0, st>>>(n, d, pts, gp_d, bucket.as<int32_t>());
     count_launch();
-    int rc = build_csr(bucket, n, BucketFn{2, buckets, 1}, buckets, off, ent, bad, st);
-    scratch_free(bucket, st);
-    scratch_free(bad, st);
-    if (rc) return rc;
-    *gp_out = gp;
+    int rc = build_csr(bucket.as<int32_t>(), n, BucketFn{2, cap, 1}, cap, off, ent, bad.as<int32_t>(), st);
+    if (rc) {
+        scratch_free(off, st);
+        scratch_free(ent, st);
+        return rc;
+    }
     *off_out = off;
     *ent_out = ent;
-    *buckets_out = buckets;
+    *buckets_out = cap;
     return FC_OK;
 }
 
@@ -446,25 +472,35 @@ static int knn_grid(int64_t batch, int64_t n, int d, int k, const PT *pts, int32
     if (d > 3) return set_error(FC_ERR_UNSUPPORTED, "grid kNN supports d <= 3");
     const int kk = k - 1;
     if (kk > 32) return set_error(FC_ERR_UNSUPPORTED, "grid kNN supports k <= 33");
+    Scratch gp(sizeof(GridParams), st);
+    if (!gp.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (grid params)");
     for (int64_t b = 0; b < batch; ++b) {
         const PT *p = pts + b * n * d;
         int32_t *o = out + b * n * k;
-        GridParams gp;
         int32_t *off = nullptr, *ent = nullptr;
         int64_t buckets = 0;
         // kNN grid: ~3 points per cell at K <= 9 (measured 1M points: 1 -> 2.23, 2 -> 1.94,
         // 3 -> 1.82, 4 -> 1.83, 6 -> 1.93 ms), about K / 3 beyond
-        if (int rc = cell_csr<PT>(n, d, p, &gp, &off, &ent, &buckets, st, std::max(3.0, k / 3.0))) return rc;
-        double4 *sp = (double4 *)scratch_alloc(sizeof(double4) * n, st);
-        sorted_points_kernel<PT><<<grid_1d(n), 256, 0, st>>>(n, d, p, ent, sp);
+        if (int rc = cell_csr<PT>(n, d, p, gp.as<GridParams>(), &off, &ent, &buckets, st, std::max(3.0, k / 3.0)))
+            return rc;
+        Scratch sp(sizeof(double4) * n, st);
+        if (!sp.ok()) {
+            scratch_free(off, st);
+            scratch_free(ent, st);
+            return set_error(FC_ERR_CUDA, "scratch allocation failed (knn)");
+        }
+        sorted_points_kernel<PT><<<grid_1d(n), 256, 0, st>>>(n, d, p, ent, sp.as<double4>());
         count_launch();
         const unsigned g = (unsigned)ceil_div(n, 128);
-        if (kk <= 4) knn_grid_query_kernel<4><<<g, 128, 0, st>>>(n, k, sp, ent, off, gp, o);
-        else if (kk <= 8) knn_grid_query_kernel<8><<<g, 128, 0, st>>>(n, k, sp, ent, off, gp, o);
-        else if (kk <= 16) knn_grid_query_kernel<16><<<g, 128, 0, st>>>(n, k, sp, ent, off, gp, o);
-        else knn_grid_query_kernel<32><<<g, 128, 0, st>>>(n, k, sp, ent, off, gp, o);
+        const GridParams *gpd = gp.as<GridParams>();
+        const double4 *spd = sp.as<double4>();
+        prof_begin("knn_grid_query", st);
+        if (kk <= 4) knn_grid_query_kernel<4><<<g, 128, 0, st>>>(n, k, spd, ent, off, gpd, o);
+        else if (kk <= 8) knn_grid_query_kernel<8><<<g, 128, 0, st>>>(n, k, spd, ent, off, gpd, o);
+        else if (kk <= 16) knn_grid_query_kernel<16><<<g, 128, 0, st>>>(n, k, spd, ent, off, gpd, o);
+        else knn_grid_query_kernel<32><<<g, 128, 0, st>>>(n, k, spd, ent, off, gpd, o);
+        prof_end(st);
         count_launch();
-        scratch_free(sp, st);
         scratch_free(off, st);
         scratch_free(ent, st);
         if (int rc = check_launch("knn_grid")) return rc;
@@ -482,10 +518,11 @@ int launch_knn(int64_t batch, int64_t n, int d, int k, const PT *pts, int32_t *o
 template <typename PT>
 int launch_spatial_order(int64_t n, int d, const PT *pts, int32_t *order, cudaStream_t st) {
     if (d > 3) return set_error(FC_ERR_UNSUPPORTED, "spatial order supports d <= 3");
-    GridParams gp;
+    Scratch gp(sizeof(GridParams), st);
+    if (!gp.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (grid params)");
     int32_t *off = nullptr, *ent = nullptr;
     int64_t buckets = 0;
-    if (int rc = cell_csr<PT>(n, d, pts, &gp, &off, &ent, &buckets, st)) return rc;
+    if (int rc = cell_csr<PT>(n, d, pts, gp.as<GridParams>(), &off, &ent, &buckets, st)) return rc;
     cudaMemcpyAsync(order, ent, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st);
     scratch_free(off, st);
     scratch_free(ent, st);

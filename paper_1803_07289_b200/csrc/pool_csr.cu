@@ -483,10 +483,15 @@ __global__ void csr_fill_kernel(const int32_t *__restrict__ keys, int64_t count,
     }
 }
 
-// The fill order inside a bucket is arbitrary; sorting each (short) segment makes the
-// result a deterministic, stable counting sort.
+// The fill order inside a bucket is arbitrary; sorting each segment makes the result a
+// deterministic, stable counting sort.  Segments of up to 16 entries (the usual case: the
+// mean reverse-list length is k) are sorted here in registers; longer ones (hubs: duplicate
+// points, clustered scans) are queued in long_list for csr_sort_long_kernel.
+constexpr int kShortSeg = 16;
+
 __global__ void csr_sort_segments_kernel(int64_t buckets, const int32_t *__restrict__ off,
-                                         int32_t *__restrict__ ent) {
+                                         int32_t *__restrict__ ent, int32_t *__restrict__ long_list,
+                                         int32_t *__restrict__ long_count) {
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < buckets;
          b += (int64_t)gridDim.x * blockDim.x) {
         const int32_t lo = off[b], hi = off[b + 1];
@@ -499,13 +504,13 @@ __global__ void csr_sort_segments_kernel(int64_t buckets, const int32_t *__restr
             }
             continue;
         }
-        if (hi - lo <= 16) {  // the usual case: sort in registers (bounded insertion sort)
+        if (hi - lo <= kShortSeg) {  // sort in registers (bounded insertion network)
             constexpr int32_t kBig = 0x7fffffff;
-            int32_t v[16];
+            int32_t v[kShortSeg];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) v[q] = lo + q < hi ? ent[lo + q] : kBig;
+            for (int q = 0; q < kShortSeg; ++q) v[q] = lo + q < hi ? ent[lo + q] : kBig;
 #pragma unroll
-            for (int a = 1; a < 16; ++a) {
+            for (int a = 1; a < kShortSeg; ++a) {
 #pragma unroll
                 for (int q = a; q > 0; --q) {
                     const int32_t x = v[q - 1], y = v[q];
@@ -514,19 +519,60 @@ __global__ void csr_sort_segments_kernel(int64_t buckets, const int32_t *__restr
                 }
             }
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
+            for (int q = 0; q < kShortSeg; ++q)
                 if (lo + q < hi) ent[lo + q] = v[q];
             continue;
         }
-        for (int32_t a = lo + 1; a < hi; ++a) {
-            const int32_t v = ent[a];
-            int32_t q = a;
-            while (q > lo && ent[q - 1] > v) {
-                ent[q] = ent[q - 1];
-                --q;
+        long_list[atomicAdd(long_count, 1)] = (int32_t)b;
+    }
+}
+
+// One CTA per long segment (grid-strided over the queue, so the launch needs no host read
+// of the queue length): an ascending bitonic network over the next power of two, with the
+// virtual padding slots >= m treated as +inf.  In this network form (the first stage of each
+// merge compares i with i ^ (size - 1), later stages i with i ^ stride) every
+// compare-exchange puts the minimum at the lower index, so padding never moves into range
+// and comparisons with a partner >= m are skipped.  O(m log^2 m / threads) per segment;
+// segments of up to kLongSmem entries are sorted in shared memory.
+constexpr int kLongSmem = 8192;
+
+__device__ __forceinline__ void bitonic_ascending(int32_t *v, int32_t m) {
+    int32_t p2 = 1;
+    while (p2 < m) p2 <<= 1;
+    for (int32_t size = 2; size <= p2; size <<= 1) {
+        for (int32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int32_t i = threadIdx.x; i < p2; i += blockDim.x) {
+                const int32_t j = stride == (size >> 1) ? (i ^ (size - 1)) : (i ^ stride);
+                if (j > i && j < m) {
+                    const int32_t x = v[i], y = v[j];
+                    if (x > y) {
+                        v[i] = y;
+                        v[j] = x;
+                    }
+                }
             }
-            ent[q] = v;
+            __syncthreads();
         }
+    }
+}
+
+__global__ void __launch_bounds__(256) csr_sort_long_kernel(const int32_t *__restrict__ off, int32_t *ent,
+                                                            const int32_t *__restrict__ long_list,
+                                                            const int32_t *__restrict__ long_count) {
+    __shared__ int32_t sv[kLongSmem];
+    const int32_t nl = *long_count;
+    for (int32_t q = blockIdx.x; q < nl; q += gridDim.x) {
+        const int32_t b = long_list[q];
+        const int32_t lo = off[b], m = off[b + 1] - lo;
+        if (m <= kLongSmem) {
+            for (int32_t i = threadIdx.x; i < m; i += blockDim.x) sv[i] = ent[lo + i];
+            __syncthreads();
+            bitonic_ascending(sv, m);
+            for (int32_t i = threadIdx.x; i < m; i += blockDim.x) ent[lo + i] = sv[i];
+        } else {
+            bitonic_ascending(ent + lo, m);  // in place in global memory (__syncthreads between stages)
+        }
+        __syncthreads();
     }
 }
 
@@ -610,8 +656,20 @@ int build_csr(const int32_t *keys, int64_t count, BucketFn bf, int64_t buckets, 
     cudaMemcpyAsync(cursor, off, sizeof(int32_t) * (buckets + 1), cudaMemcpyDeviceToDevice, st);
     csr_fill_kernel<<<grid_1d(count), 256, 0, st>>>(keys, count, bf, cursor, ent);
     count_launch();
-    csr_sort_segments_kernel<<<grid_1d(buckets), 256, 0, st>>>(buckets, off, ent);
+    // long-segment queue: [0] = queue length, [1..] = bucket ids (at most
+    // count / (kShortSeg + 1) segments can be longer than kShortSeg)
+    int32_t *long_count = (int32_t *)scratch_alloc(sizeof(int32_t) * (count / (kShortSeg + 1) + 2), st);
+    if (!long_count) {
+        scratch_free(counts, st);
+        return set_error(FC_ERR_CUDA, "scratch allocation failed (csr)");
+    }
+    int32_t *long_list = long_count + 1;
+    cudaMemsetAsync(long_count, 0, sizeof(int32_t), st);
+    csr_sort_segments_kernel<<<grid_1d(buckets), 256, 0, st>>>(buckets, off, ent, long_list, long_count);
     count_launch();
+    csr_sort_long_kernel<<<(unsigned)num_sms() * 2, 256, 0, st>>>(off, ent, long_list, long_count);
+    count_launch();
+    scratch_free(long_count, st);
     scratch_free(counts, st);
     return check_launch("build_csr");
 }

@@ -71,8 +71,11 @@ class Neighborhood:
         return self.table.view(self.batch * self.n, self.k)
 
     def csr(self):
+        """Reverse neighbourhood, built on first use on the current stream without a host
+        sync (the table was range-checked when this Neighborhood was created, or came from
+        knn), so a backward that first needs it stays CUDA-graph capturable."""
         if self._csr is None:
-            self._csr = _ops.csr_build(self.flat, self.batch, self.n)
+            self._csr = _ops.csr_build(self.flat, self.batch, self.n, validate=False)
         return self._csr
 
 

@@ -67,6 +67,11 @@ def main():
             "l2_hit_rate": round(val(r, "lts__t_sector_hit_rate.pct") / 100, 4),
             "dram_bytes_per_point": round((val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum")) * 1e9 / args.n, 1),
             "registers_per_thread": val(r, "launch__registers_per_thread"),
+            "tensor_pipe_frac": (round(val(r, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active") / 100, 4)
+                                 if val(r, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active") is not None
+                                 else None),
+            "bank_conflict_wavefronts_per_point": (round(val(r, "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum") / args.n, 2)
+                                                   if val(r, "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum") else None),
         }
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as fh:

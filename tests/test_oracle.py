@@ -93,3 +93,46 @@ def test_oracle_matches_compiled_reference(oracle_mod):
     df, dth, dtb, dl = oracle_mod.conv_backward(g, f, loc, nb, th, tb)
     for a, b in zip((df, dl, dth, dtb), bufs):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("case", CONV_CASES[1:])
+def test_oracle_row_checkers_bitwise_vs_golden(oracle_mod, case):
+    """The large-n checkers (row subsets, parallel parameter gradients) against the
+    reference's own golden outputs: rows bitwise, d_theta/d_theta_b to fp64 regrouping."""
+    g = load_golden(f"conv_{case}.npz")
+    n = g["features"].shape[0]
+    rows = np.unique(np.r_[0, n - 1, np.random.default_rng(3).integers(0, n, 40)])
+    args = (g["features"], g["locations"], g["neighbors"], g["theta"], g["theta_b"])
+    np.testing.assert_array_equal(oracle_mod.conv_forward_rows(*args, rows), g["out"][rows])
+    df, dl = oracle_mod.conv_backward_rows(g["upstream"], *args, rows)
+    np.testing.assert_array_equal(df, g["d_features"][rows])
+    np.testing.assert_array_equal(dl, g["d_locations"][rows])
+    dth, dtb = oracle_mod.conv_param_grads(g["upstream"], g["features"], g["locations"], g["neighbors"])
+    np.testing.assert_allclose(dth, g["d_theta"], rtol=1e-12, atol=1e-12 * np.abs(g["d_theta"]).max())
+    np.testing.assert_allclose(dtb, g["d_theta_b"], rtol=1e-12, atol=1e-12 * np.abs(g["d_theta_b"]).max())
+
+
+def test_oracle_backward_rows_repeated_slots(oracle_mod):
+    """A neighbour listed twice in one row and duplicated query rows: still the serial
+    reference's values, bitwise."""
+    from paper_1803_07289_b200.core import synthetic_layer
+
+    loc, feat, th, tb, up = synthetic_layer(3, 0, 600, 3, 8, 5)
+    nbr = oracle_mod.knn_brute(loc, 6)
+    nbr[10, 3] = nbr[10, 2]
+    rows = np.array([0, 10, nbr[10, 2], 599, 5, 5])
+    df, _, _, dl = oracle_mod.conv_backward(up, feat, loc, nbr, th, tb)
+    rdf, rdl = oracle_mod.conv_backward_rows(up, feat, loc, nbr, th, tb, rows)
+    np.testing.assert_array_equal(rdf, df[rows])
+    np.testing.assert_array_equal(rdl, dl[rows])
+
+
+def test_oracle_synthetic_layer_matches_package(oracle_mod):
+    """bench.py's CPU legs draw inputs through oracle.synthetic_layer (numpy only); it must
+    be the package's generator, value for value."""
+    from paper_1803_07289_b200.core import synthetic_layer
+
+    for a, b in zip(oracle_mod.synthetic_layer(4, 0, 500, 3, 8, 6), synthetic_layer(4, 0, 500, 3, 8, 6)):
+        np.testing.assert_array_equal(a, b)
+    for a, b in zip(oracle_mod.synthetic_layer(9, 3, 50, 2, 4, 5), synthetic_layer(9, 3, 50, 2, 4, 5)):
+        np.testing.assert_array_equal(a, b)
