@@ -97,7 +97,7 @@ int tc_conv_forward(int mode, int64_t total, int64_t n, int c_in, int d, int k, 
                     const float *feat, const float *loc, const int32_t *nbr, const float *theta,
                     const float *theta_b, float *out, cudaStream_t st);
 int tc_reverse_supported(int mode, int gc, int d, int cout);
-int tc_backward_supported(int mode, int cin, int d, int cout);
+int tc_backward_supported(int mode, int cin, int d, int k, int cout);
 int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int cout, const float *g,
                 const float *feat, const float *loc, const int32_t *nbr, Csr csr, const float *theta,
                 const float *theta_b, float *d_features, float *d_locations, float *d_theta, float *d_theta_b,
@@ -226,7 +226,7 @@ int fc_conv_backward(int dtype, int mode, int64_t batch, int64_t n, int c_in, in
         return set_error(FC_ERR_CONFIG, "d_features/d_locations need the reverse neighbourhood (fc_csr_build)");
     cudaStream_t st = ST(stream);
     const int64_t total = batch * n;
-    if (dtype == FC_F32 && mode != FC_MODE_SIMT && tc_backward_supported(mode, c_in, d, c_out))
+    if (dtype == FC_F32 && mode != FC_MODE_SIMT && tc_backward_supported(mode, c_in, d, k, c_out))
         return tc_backward(mode, total, n, c_in, d, k, c_out, (const float *)upstream, (const float *)features,
                            (const float *)locations, neighbors, Csr{rev_offsets, rev_entries}, (const float *)theta,
                            (const float *)theta_b, (float *)d_features, (float *)d_locations, (float *)d_theta,

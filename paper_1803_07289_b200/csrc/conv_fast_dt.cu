@@ -39,6 +39,9 @@ constexpr int dWarps = 24;
 constexpr int dThreads = dWarps * 32;
 constexpr int dChunk = 16;     // points per chunk (= gather warps)
 constexpr int dK = 8;
+// d_theta accumulation segment: tiles (128 points, 16 tf32 k-steps each) accumulated in TMEM
+// before the index warps drain the accumulator (precision: see dt_drain)
+constexpr int kSegTiles = 8;
 // register split (setmaxnreg): control warps (index, epilogue) give registers to the gather
 // warps, which hold a point's 8 rows and their offsets across the load latency;
 // 8 x 32 x kCtlRegs + 16 x 32 x kGatherRegs <= 768 x 80 (the launch allocation)
@@ -70,12 +73,16 @@ struct DtArgs2 {
     const int32_t *nbr;
     const uint8_t *bimg;  // forward fp16 image (hi, lo); K-blocks 0..2 used
     const float *binv;
-    float *partial;       // [gridDim.x][2][64 * 4 * 64], layout (c', c, t)
+    float *partial;       // [gridDim.x][128 lanes][256 columns]: TMEM-native (c' hi | c' lo) x (t, c), zeroed
     float *centre;        // [total, 3]
     int dbg;                    // FC_DBG & 8: per-role wait-cycle counters
     unsigned long long *clk;    // [grid][24][4]
 };
 
+// per-role wait-cycle counters (FC_DBG & 8) exist only in builds with -DFC_DT_CLOCKS: the
+// counters live across the hot loops and, in the register-capped roles, were spilled to local
+// memory around every ring wait (measured: +0.4 ms per 7M-point call)
+#ifdef FC_DT_CLOCKS
 #define DT_CLK(slot, stmt)                                                  \
     do {                                                                    \
         long long _c0, _c1;                                                 \
@@ -84,6 +91,12 @@ struct DtArgs2 {
         asm volatile("mov.u64 %0, %%clock64;" : "=l"(_c1)::"memory");      \
         ck[slot] += _c1 - _c0;                                              \
     } while (0)
+#else
+#define DT_CLK(slot, stmt) \
+    do {                   \
+        stmt;              \
+    } while (0)
+#endif
 
 // tf32 hi part by truncation (the low 13 mantissa bits cleared); lo = x - hi is exact and
 // carries the remaining 13 bits (read by the MMA as tf32: 2^-21 relative overall)
@@ -109,6 +122,44 @@ __device__ __forceinline__ void mma_tf32_mn(uint32_t d_tmem, uint64_t a, uint64_
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
 }
+__device__ __forceinline__ void red_add_v4(float *p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+// Drain of a d_theta accumulation segment: add the 256 TMEM columns of this thread's lane into
+// its CTA partial row with fp32 reductions at L2 (one thread per address, segments in order:
+// deterministic).  Why segments: the tensor pipe's fp32 accumulation truncates -- measured
+// on the B200, the d_theta error grows linearly with the number of accumulated k-steps and is
+// biased toward zero (2.9e-5 at 886 steps, 1M points; scripts/dtheta_precision.py) -- so no
+// accumulator runs longer than kSegTiles tiles (128 k-steps, ~5e-6).
+__device__ __noinline__ void dt_drain(uint32_t taddr, float *part_row) {
+#pragma unroll 1
+    for (int n0 = 0; n0 < 256; n0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + (uint32_t)n0, v);
+#pragma unroll
+        for (int q = 0; q < 16; q += 4) red_add_v4(part_row + n0 + q, v[q], v[q + 1], v[q + 2], v[q + 3]);
+    }
+}
+// Segment drain of the c' hi rows (the rows whose accumulator is large): add the lane's 256
+// columns into its partial row and zero them in TMEM, so the MMAs continue (accumulate = 1)
+// from zero on these rows while the c' lo rows (2^-11 smaller, their truncation negligible)
+// keep accumulating until the final drain.
+__device__ __noinline__ void dt_drain_zero(uint32_t taddr, float *part_row) {
+#pragma unroll 1
+    for (int n0 = 0; n0 < 256; n0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + (uint32_t)n0, v);
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                taddr + (uint32_t)n0),
+            "r"(0u)
+            : "memory");
+#pragma unroll
+        for (int q = 0; q < 16; q += 4) red_add_v4(part_row + n0 + q, v[q], v[q + 1], v[q + 2], v[q + 3]);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_dt(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void sts64u(uint32_t addr, uint32_t a, uint32_t b) {
     asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
 }
@@ -143,12 +194,16 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
     uint64_t *z_free = bar + 9;       // [2 by tile parity] epilogue warps: Z drained, rs read
     uint64_t *xb_free = bar + 11;     // [2] commit: Xb buffer consumed (Z MMAs of its tile done)
     uint64_t *dt_done = bar + 13;     // commit: d_theta accumulator final
-    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bar + 14);
+    uint64_t *dt_seg = bar + 14;      // commit: a d_theta accumulation segment complete
+    uint64_t *seg_drained = bar + 15; // index warps: the segment has been read out of TMEM
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bar + 16);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef FC_DT_CLOCKS
     long long ck[4] = {0, 0, 0, 0};
     long long ck_t0;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(ck_t0)::"memory");
+#endif
     if (threadIdx.x == 0) {
         for (int q = 0; q < 2; ++q) {
             mbar_init(e_full + q, dIdxWarps);
@@ -160,6 +215,8 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
         }
         mbar_init(z_done, 1);
         mbar_init(dt_done, 1);
+        mbar_init(dt_seg, 1);
+        mbar_init(seg_drained, 2);
         fence_mbar_init();
     }
     if (warp == dEpiWarp0) tmem_alloc(tmem_holder, 512);
@@ -230,11 +287,17 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
                 if (lane == 0) mbar_arrive(z_free + (i & 1));
             }
         };
+        // d_theta segments (see dt_drain_zero): every kSegTiles tiles (staggered by CTA) the
+        // first MMA of a tile waits until index warps 16-17 have drained and zeroed the c' hi rows.
         for (int i = 0; i < T; ++i) {
             for (int c = 0; c < kTile / dChunk; ++c) {
                 if (warp == dEpiWarp0) {
                     if (lane == 0) {
                         const int u = i * (kTile / dChunk) + c, st = u & 1;
+                        // segment boundaries staggered by CTA (the drains' L2 reductions spread in time)
+                        const int sg = i + (int)(blockIdx.x & (kSegTiles - 1));
+                        if (c == 0 && i > 0 && (sg & (kSegTiles - 1)) == 0)
+                            DT_CLK(0, mbar_wait(seg_drained, (uint32_t)(((sg / kSegTiles) - 1) & 1)));
                         DT_CLK(0, mbar_wait(c_full + st, (uint32_t)((u >> 1) & 1)));
                         tc_fence_after();
                         const uint32_t cs = C0 + (uint32_t)(st * L::STAGE);
@@ -269,6 +332,7 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
                     mma_commit(z_done);
                     mma_commit(xb_free + (i & 1));
                     if (i == T - 1) mma_commit(dt_done);
+                    else if (((i + 1 + (int)(blockIdx.x & (kSegTiles - 1))) & (kSegTiles - 1)) == 0) mma_commit(dt_seg);
                 }
                 __syncwarp();
             }
@@ -279,18 +343,7 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
             mbar_wait(dt_done, 0);
             tc_fence_after();
         }
-        const int m = row, cp = m & 63;
-        float *part = a.partial + ((int64_t)blockIdx.x * 2 + (m >> 6)) * (64 * 4 * 64);
-#pragma unroll 1
-        for (int n0 = 0; n0 < 256; n0 += 16) {
-            float v[16];
-            tmem_ld16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)n0, v);
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const int kx = n0 + q, t = kx >> 6, cc = kx & 63;
-                part[(int64_t)cp * 256 + cc * 4 + t] = T > 0 ? v[q] : 0.f;
-            }
-        }
+        if (T > 0) dt_drain(tmem_base + ((uint32_t)(ew * 32) << 16), a.partial + ((int64_t)blockIdx.x * 128 + row) * 256);
     } else if (warp >= dIdxWarp0) {
         // ------------------------------------------------------------ index producers
         setmaxnreg_dec<kCtlRegs>();
@@ -357,6 +410,17 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
             load_pos(i + 1, nb_cur, ps);
             if (i + 2 < T) load_nb(i + 2, nb_next);
             store_e(i + 1, nb_cur, ps);
+            const int sg = i + 1 + (int)(blockIdx.x & (kSegTiles - 1));
+            if ((sg & (kSegTiles - 1)) == 0 && warp < dIdxWarp0 + 2) {
+                // a d_theta segment is complete: the two warps on TMEM lane quadrants 0, 1 (the
+                // c' hi rows) drain and zero them, then release the accumulator
+                mbar_wait(dt_seg, (uint32_t)(((sg / kSegTiles) - 1) & 1));
+                tc_fence_after();
+                dt_drain_zero(tmem_base + ((uint32_t)(t & ~31) << 16), a.partial + ((int64_t)blockIdx.x * 128 + t) * 256);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(seg_drained);
+            }
         }
     } else {
         // ------------------------------------------------------------ gather warps
@@ -461,12 +525,14 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
         }
         if (pend >= 0) handoff();
     }
+#ifdef FC_DT_CLOCKS
     if ((a.dbg & 8) && lane == 0) {
         long long t1;
         asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1)::"memory");
         unsigned long long *o = a.clk + ((int64_t)blockIdx.x * 24 + warp) * 4;
         o[0] = ck[0], o[1] = ck[1], o[2] = ck[2], o[3] = t1 - ck_t0;
     }
+#endif
     tc_fence_before();
     __syncthreads();
     if (warp == dEpiWarp0) {
@@ -481,7 +547,7 @@ void launch_pack_b(bool split, int cin, int cout, const float *theta, const floa
                    int gc, uint8_t *img, float *binv, cudaStream_t st);
 template <typename T>
 int launch_dtheta_reduce(int chunks, int cin, int d, int cout, const T *partial, T *d_theta, T *d_theta_b,
-                         cudaStream_t st);
+                         cudaStream_t st, int tmajor = 0);
 
 // d_theta / d_theta_b (reduced in fixed order) and the centre role of d_locations for
 // c_in = c_out = 64, k = 8, d = 3; centre may be null when d_locations is not wanted
@@ -494,6 +560,7 @@ int tc_fast_dtheta(int64_t total, int64_t n, const float *feat, const float *loc
     const int grid = (int)std::min<int64_t>(num_tiles, num_sms());
     uint8_t *img = (uint8_t *)scratch_alloc(img_bytes + 256, st);
     float *partial = (float *)scratch_alloc(sizeof(float) * 2 * grid * 64 * 64 * 4, st);
+    if (partial) cudaMemsetAsync(partial, 0, sizeof(float) * 2 * grid * 64 * 64 * 4, st);
     float *cscratch = centre ? nullptr : (float *)scratch_alloc(sizeof(float) * total * 3, st);
     if (!img || !partial || (!centre && !cscratch)) return set_error(FC_ERR_CUDA, "scratch allocation failed (fast dtheta)");
     float *binv = reinterpret_cast<float *>(img + img_bytes);
@@ -546,7 +613,9 @@ int tc_fast_dtheta(int64_t total, int64_t n, const float *feat, const float *loc
             }
         }
     }
-    if (!rc && (d_theta || d_theta_b)) rc = launch_dtheta_reduce<float>(2 * grid, 64, 3, 64, partial, d_theta, d_theta_b, st);
+    // per CTA: rows c' hi (64) then c' lo (64) = two partial slices in the t-major column order
+    if (!rc && (d_theta || d_theta_b))
+        rc = launch_dtheta_reduce<float>(2 * grid, 64, 3, 64, partial, d_theta, d_theta_b, st, 1);
     scratch_free(img, st);
     scratch_free(partial, st);
     scratch_free(cscratch, st);

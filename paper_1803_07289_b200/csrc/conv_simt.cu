@@ -275,10 +275,12 @@ __global__ void __launch_bounds__(256)
 }
 
 // Fixed-order (ascending chunk) reduction of the d_theta partials, accumulated in fp64.
+// Partial layouts: tmajor = 0: element e = (c' * cin + c) * (d + 1) + t; tmajor = 1 (the
+// tensor-core accumulators' column order): e = c' * cin * (d + 1) + t * cin + c.
 template <typename T>
 __global__ void dtheta_reduce_kernel(int chunks, int cin, int d, int cout,
                                      const T *__restrict__ partial, T *__restrict__ d_theta,
-                                     T *__restrict__ d_theta_b) {
+                                     T *__restrict__ d_theta_b, int tmajor) {
     // 8 lanes per output element: lane g adds the chunks of its contiguous block in ascending
     // order (fp64), the 8 block sums are combined by a fixed xor tree -- a fixed order
     // (deterministic), with 8x the loads in flight of one thread per element.
@@ -297,7 +299,7 @@ __global__ void dtheta_reduce_kernel(int chunks, int cin, int d, int cout,
         if (g == 0 && e < E) {
             const int cp = (int)(e / (cin * (d + 1)));
             const int kk = (int)(e % (cin * (d + 1)));
-            const int c = kk / (d + 1), t = kk % (d + 1);
+            const int c = tmajor ? kk % cin : kk / (d + 1), t = tmajor ? kk / cin : kk % (d + 1);
             if (t < d) {
                 if (d_theta) d_theta[((int64_t)cp * cin + c) * d + t] = (T)s;
             } else if (d_theta_b) {
@@ -496,7 +498,7 @@ static int launch_dtheta_dp(int64_t total, int64_t n, int cin, int k, int cout, 
     dtheta_partial_kernel<T, DP, RPT><<<dim3((unsigned)chunks, (unsigned)slices), 256, smem, st>>>(
         total, n, cin, k, cout, feat, loc, nbr, g, partial, chunk_pts, tile);
     count_launch();
-    dtheta_reduce_kernel<T><<<grid_for(E * 8, 256), 256, 0, st>>>((int)chunks, cin, DP, cout, partial, d_theta, d_theta_b);
+    dtheta_reduce_kernel<T><<<grid_for(E * 8, 256), 256, 0, st>>>((int)chunks, cin, DP, cout, partial, d_theta, d_theta_b, 0);
     count_launch();
     scratch_free(partial, st);
     return check_launch("dtheta kernels");
@@ -511,14 +513,15 @@ int launch_dtheta(int64_t total, int64_t n, int d, int cin, int k, int cout, con
 
 template <typename T>
 int launch_dtheta_reduce(int chunks, int cin, int d, int cout, const T *partial, T *d_theta, T *d_theta_b,
-                         cudaStream_t st) {
+                         cudaStream_t st, int tmajor) {
     const int64_t E = (int64_t)cout * cin * (d + 1);
-    dtheta_reduce_kernel<T><<<grid_for(E * 8, 256), 256, 0, st>>>(chunks, cin, d, cout, partial, d_theta, d_theta_b);
+    dtheta_reduce_kernel<T><<<grid_for(E * 8, 256), 256, 0, st>>>(chunks, cin, d, cout, partial, d_theta, d_theta_b,
+                                                                   tmajor);
     count_launch();
     return check_launch("dtheta_reduce_kernel");
 }
-template int launch_dtheta_reduce<float>(int, int, int, int, const float *, float *, float *, cudaStream_t);
-template int launch_dtheta_reduce<double>(int, int, int, int, const double *, double *, double *, cudaStream_t);
+template int launch_dtheta_reduce<float>(int, int, int, int, const float *, float *, float *, cudaStream_t, int);
+template int launch_dtheta_reduce<double>(int, int, int, int, const double *, double *, double *, cudaStream_t, int);
 
 #define FC_INST(T)                                                                                   \
     template void launch_pack<T>(int, int, int, const T *, const T *, T *, T *, cudaStream_t);      \

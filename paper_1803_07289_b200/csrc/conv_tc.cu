@@ -1339,14 +1339,18 @@ int tc_reverse_supported(int mode, int gc, int d, int cout) { return tc_shape_ok
 
 template <typename T>
 int launch_dtheta_reduce(int chunks, int cin, int d, int cout, const T *partial, T *d_theta, T *d_theta_b,
-                         cudaStream_t st);
+                         cudaStream_t st, int tmajor = 0);
 
 // Full fp32 backward on the tensor cores (c_in = c_out = 64, d = 3):
 //   tc_dtheta_kernel : d_theta partials + centre term of d_locations
 //   dtheta_reduce    : fixed-order reduction of the per-CTA partials (fp64 accumulate)
 //   tc_gmc (reverse) : d_features (+ neighbour term of d_locations)
-int tc_backward_supported(int mode, int cin, int d, int cout) {
-    return (d == 3 && cin == 64 && cout == 64 && mode != FC_MODE_SIMT) ? 1 : 0;
+// K != 8 (or FC_NO_FAST=1) would take tc_dtheta_kernel below, whose d_theta accumulates a
+// CTA's whole point range in TMEM (the tensor pipe's fp32 accumulation truncates: error
+// linear in the run length), so those shapes use the moments + GEMM route instead unless
+// the A/B knob asks for the generic kernel, which then bounds the run per CTA by its grid.
+int tc_backward_supported(int mode, int cin, int d, int k, int cout) {
+    return (d == 3 && cin == 64 && cout == 64 && mode != FC_MODE_SIMT && (k == kSlots || !fast_enabled())) ? 1 : 0;
 }
 
 int tc_fast_dtheta(int64_t total, int64_t n, const float *feat, const float *loc, const int32_t *nbr, const float *g,
@@ -1360,7 +1364,9 @@ int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int c
     (void)d;
     using L = DtLayout;
     const int64_t num_tiles = ceil_div(total, kTcM);
-    const int grid = (int)std::min<int64_t>(num_tiles, num_sms());
+    // generic d_theta kernel: at most 8 tiles (1024 points, 128 tf32 k-steps) accumulated in
+    // TMEM per CTA -- more CTAs (waves) instead of a longer truncating accumulation
+    const int grid = (int)std::min<int64_t>(num_tiles, std::max<int64_t>(num_sms(), ceil_div(num_tiles, 8)));
     Scratch centre_buf;
     float *centre = nullptr;
     int rc = FC_OK;
