@@ -26,3 +26,17 @@ CC=${REF_CC:-/usr/bin/gcc}
 $CC -O3 -fopenmp -fPIC -shared -DNPY_NO_DEPRECATED_API=NPY_1_7_API_VERSION \
     -I"$PYINC" -I"$NPINC" "$OUT/_native.c" -o "$OUT/_native$SUFFIX"
 echo "build_ref: built $OUT/_native$SUFFIX"
+# Pack the reference package and its own test suite next to the build output (git-ignored,
+# travels to the GPU box like the .so; a tarball, so no reference source lies in the tree):
+# tests/test_gpu_ref_suite.py unpacks it and runs the reference's test_flexops.py /
+# test_neighborhood.py with the B200 module in the kernel slot.
+PKG="$(dirname "$REF")"          # .../pkg/src
+TESTS="$(dirname "$PKG")/tests"  # .../pkg/tests
+STAGE="$(mktemp -d)"
+mkdir -p "$STAGE/refpkg/flexconv" "$STAGE/refpkg/tests"
+cp "$REF"/*.py "$STAGE/refpkg/flexconv/"
+cp "$OUT/_native$SUFFIX" "$STAGE/refpkg/flexconv/_native$SUFFIX"
+if [ -d "$TESTS" ]; then cp "$TESTS"/*.py "$STAGE/refpkg/tests/"; fi
+tar -czf "$OUT/refsuite.tar.gz" -C "$STAGE" refpkg
+rm -rf "$STAGE" "$OUT/refpkg"
+echo "build_ref: packed the reference package + tests into $OUT/refsuite.tar.gz"
