@@ -84,8 +84,8 @@ class NeighborIndex:
         hi = self.n if n_points is None else int(n_points)
         table = self.device_table(device, hi)
         entry = self._dev[(str(device), hi)]
-        if "csr" not in entry:
-            entry["csr"] = _ops.csr_build(table, 1, hi)
+        if "csr" not in entry:  # the table was range-checked by device_table: no host sync here
+            entry["csr"] = _ops.csr_build(table, 1, hi, validate=False)
         return entry["csr"]
 
 
