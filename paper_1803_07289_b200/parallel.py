@@ -9,25 +9,30 @@ loop over clouds with gradient accumulation, harness.py:589-599).  Two partition
   in rank order in fp64 -- bitwise reproducible for a given world size (no float
   reduction-order nondeterminism).
 
-* Point-chunk sharding of ONE large cloud with neighbour halos (config C4, 7M points):
-  after a spatial ordering the cloud is cut into contiguous row ranges; `HaloPlan` computes,
-  once per neighbourhood, the halo (neighbours owned elsewhere), the grouped point-to-point
-  exchange lists and the local neighbour table.  Forward = halo gather + local flex_conv.
-  Backward = local backward with zero upstream on halo rows, then the halo rows' partial
-  d_features / d_locations are sent back to their owners and added in fixed rank order, and
-  d_theta / d_theta_b are summed with `fixed_order_allreduce`.  Results equal the
-  unsharded operator (tests/test_parallel.py checks this against the oracle with gloo).
+* Point-chunk sharding of ONE large cloud with neighbour halos (configs C3 / C4, the
+  north_star's 7M-point cloud over 8 GPUs): `ShardedCloud`.  Each rank holds a contiguous
+  block of the spatially ordered cloud and never the global neighbour table:
+    1. exact kNN of its own points with a POSITION GHOST SHELL -- a local kNN among the
+       owned points bounds every point's k-th-neighbour distance by R (the rank's largest),
+       so all true neighbours lie in the owned bounding box grown by R; each rank sends
+       the others its points inside their grown boxes, and the kNN over [owned | ghosts]
+       (ordered by global index, so index tie-breaking is the global one) gives the exact
+       rows of the owned points (tests/test_parallel.py: equal to the unsharded table);
+    2. the halo (neighbours owned elsewhere, a subset of the ghosts), the local neighbour
+       table over [owned | halo], the reverse CSR and the exchange index lists, all device
+       tensors built once per neighbourhood;
+  then per layer: forward = halo gather of feature rows (one grouped point-to-point
+  exchange) + the flex-conv kernels on the local buffers; backward = the local backward
+  with zero upstream on the halo rows, the halo rows' d_features / d_locations partials
+  sent back and added at the owners in fixed source-rank order, d_theta / d_theta_b summed
+  by `fixed_order_allreduce` -- the only collective, and only for training.
 
-Transport: `DistTransport` (torch.distributed grouped isend/irecv -- NCCL over NVLink on
-the GPU box, gloo for the CPU tests; gloo has no all-to-all) or `LocalTransport` (all ranks
-in one process, used to emulate a sharded run on one GPU).
+Transport: torch.distributed grouped isend/irecv (NCCL over NVLink on the GPU box; gloo in
+the CPU tests and for several ranks sharing one GPU, through host staging).
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
-
-import numpy as np
 import torch
 
 from .errors import ConfigInvalidError, ShapeMismatchError
@@ -90,221 +95,229 @@ def ordered_allgather_sum(local: torch.Tensor, units: int, group=None) -> torch.
     return acc
 
 
-# ---------------------------------------------------------------------------- transports
-class DistTransport:
-    """Grouped point-to-point exchange over torch.distributed (one call per direction)."""
+# ---------------------------------------------------------------------------- transport
+class Comm:
+    """Grouped point-to-point exchange and all-gather over torch.distributed.  NCCL moves
+    device tensors directly (NVLink); gloo (the CPU tests, or several ranks sharing one GPU)
+    stages device tensors through host memory.  Zero-sized messages are skipped on both
+    sides (their sizes are always agreed first)."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, device=None):
         import torch.distributed as dist
 
         self.dist = dist
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.host = dist.get_backend(group) == "gloo"
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else \
+                torch.device("cpu")
+        self.wire = torch.device("cpu") if self.host else torch.device(device)
+
+    def all_gather(self, t: torch.Tensor) -> list[torch.Tensor]:
+        """Same-shape tensors from every rank, in rank order."""
+        w = t.contiguous().to(self.wire)
+        parts = [torch.empty_like(w) for _ in range(self.world)]
+        self.dist.all_gather(parts, w, group=self.group)
+        return [p.to(t.device) for p in parts]
+
+    def ordered_sum(self, t: torch.Tensor) -> torch.Tensor:
+        """Sum over ranks accumulated in rank order in fp64 (deterministic), in t's dtype."""
+        if self.world == 1:
+            return t
+        acc = torch.zeros(t.shape, dtype=torch.float64, device=t.device)
+        for p in self.all_gather(t):
+            acc += p.to(torch.float64)
+        return acc.to(t.dtype)
 
     def exchange(self, sends: dict, recv_shapes: dict, dtype, device) -> dict:
-        """sends[r] -> tensor to rank r; returns {r: tensor received from r}."""
-        ops, recvs = [], {}
+        """sends[r]: tensor for rank r; recv_shapes[r]: shape expected from rank r.
+        Returns {r: received tensor on `device`} (empty tensors for zero-sized shapes)."""
+        ops, bufs, keep = [], {}, []
         for r, shape in recv_shapes.items():
-            buf = torch.empty(shape, dtype=dtype, device=device)
-            recvs[r] = buf
-            ops.append(self.dist.P2POp(self.dist.irecv, buf, r, self.group))
+            bufs[r] = torch.empty(shape, dtype=dtype, device=self.wire)
+            if bufs[r].numel():
+                ops.append(self.dist.P2POp(self.dist.irecv, bufs[r], r, self.group))
         for r, t in sends.items():
-            ops.append(self.dist.P2POp(self.dist.isend, t.contiguous(), r, self.group))
+            if t.numel():
+                w = t.contiguous().to(self.wire)
+                keep.append(w)
+                ops.append(self.dist.P2POp(self.dist.isend, w, r, self.group))
         if ops:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
-        return recvs
+        return {r: b.to(device) for r, b in bufs.items()}
+
+    def exchange_sizes(self, counts: dict) -> dict:
+        """counts[r] = number of items this rank will send to r; returns {r: number of items
+        r will send here} for every other rank."""
+        mine = torch.tensor([int(counts.get(r, 0)) for r in range(self.world)], dtype=torch.int64)
+        table = self.all_gather(mine.to(self.wire))  # [world] rows of counts: table[src][dst]
+        return {r: int(table[r][self.rank].item()) for r in range(self.world) if r != self.rank}
 
 
-class LocalTransport:
-    """All ranks live in this process (sequential emulation of a sharded run)."""
-
-    def __init__(self, world: int):
-        self.world = world
-        self.mailbox: dict = {}
-
-    def post(self, src: int, sends: dict):
-        for dst, t in sends.items():
-            self.mailbox[(src, dst)] = t
-
-    def collect(self, dst: int, srcs) -> dict:
-        return {s: self.mailbox.pop((s, dst)) for s in srcs}
-
-
-# ---------------------------------------------------------------------------- halo plan
-@dataclass
-class HaloPlan:
-    """Rank `rank`'s view of a point-chunk sharded cloud.
-
-    owned rows [lo, hi) of the global (spatially ordered) point set; `halo` = sorted global
-    ids of neighbours owned elsewhere; local point ids: owned j -> j - lo, halo[q] ->
-    n_own + q.  `local_nbr` is [n_own + n_halo, K] (halo rows are self-loops: they carry
-    zero upstream gradient and their forward outputs are discarded).
-    """
-
-    rank: int
-    world: int
-    lo: int
-    hi: int
-    halo: np.ndarray                # [n_halo] global ids
-    recv_lists: dict                # src rank -> positions in `halo` (ascending)
-    send_lists: dict                # dst rank -> owned local ids requested by dst
-    local_nbr: np.ndarray           # [n_own + n_halo, K] int64
-
-    @property
-    def n_own(self) -> int:
-        return self.hi - self.lo
-
-    @property
-    def n_local(self) -> int:
-        return self.n_own + len(self.halo)
-
-    @staticmethod
-    def bounds(n: int, world: int) -> list[int]:
-        return [shard_range(n, world, r)[0] for r in range(world)] + [n]
-
-    @staticmethod
-    def requests(nbr: np.ndarray, bounds: list[int], rank: int):
-        """Halo ids of `rank` and, per owner, the positions in the halo they fill."""
-        lo, hi = bounds[rank], bounds[rank + 1]
-        rows = np.asarray(nbr[lo:hi], dtype=np.int64)
-        if rows.size and (rows.min() < 0 or rows.max() >= bounds[-1]):
-            raise ShapeMismatchError("neighbour index out of the sharded point range")
-        ext = rows[(rows < lo) | (rows >= hi)]
-        halo = np.unique(ext)
-        owner = np.searchsorted(np.asarray(bounds), halo, side="right") - 1
-        recv = {int(r): np.nonzero(owner == r)[0] for r in np.unique(owner)}
-        return halo, recv
-
-    @classmethod
-    def build_all(cls, nbr, world: int, bounds: list[int] | None = None) -> list["HaloPlan"]:
-        """Plans of every rank from the full neighbour table (host-side, once per
-        neighbourhood; each rank can also build only its own with `build_local`)."""
-        nbr = np.asarray(nbr, dtype=np.int64)
-        n = nbr.shape[0]
-        bounds = bounds or cls.bounds(n, world)
-        reqs = [cls.requests(nbr, bounds, r) for r in range(world)]
-        plans = []
-        for r in range(world):
-            halo, recv = reqs[r]
-            send = {}
-            for d in range(world):
-                if d == r:
-                    continue
-                h_d, rv_d = reqs[d]
-                if r in rv_d:
-                    send[d] = h_d[rv_d[r]] - bounds[r]
-            plans.append(cls._finish(r, world, bounds, nbr, halo, recv, send))
-        return plans
-
-    @classmethod
-    def build_local(cls, nbr, world: int, rank: int, transport: DistTransport,
-                    bounds: list[int] | None = None) -> "HaloPlan":
-        """This rank's plan; request lists are exchanged with the owners (p2p)."""
-        nbr = np.asarray(nbr, dtype=np.int64)
-        n = nbr.shape[0]
-        bounds = bounds or cls.bounds(n, world)
-        halo, recv = cls.requests(nbr, bounds, rank)
-        # 1) counts to every other rank, 2) the id lists
-        counts = {d: torch.tensor([len(recv.get(d, []))], dtype=torch.int64) for d in range(world) if d != rank}
-        got = transport.exchange(counts, {d: (1,) for d in counts}, torch.int64, torch.device("cpu"))
-        sends = {d: torch.from_numpy(halo[recv[d]]) for d in recv}
-        shapes = {d: (int(c.item()),) for d, c in got.items() if int(c.item()) > 0}
-        ids = transport.exchange(sends, shapes, torch.int64, torch.device("cpu"))
-        send = {d: t.numpy() - bounds[rank] for d, t in ids.items()}
-        return cls._finish(rank, world, bounds, nbr, halo, recv, send)
-
-    @classmethod
-    def _finish(cls, rank, world, bounds, nbr, halo, recv, send) -> "HaloPlan":
-        lo, hi = bounds[rank], bounds[rank + 1]
-        rows = np.asarray(nbr[lo:hi], dtype=np.int64)
-        n_own = hi - lo
-        remap = np.empty(rows.shape, dtype=np.int64)
-        inside = (rows >= lo) & (rows < hi)
-        remap[inside] = rows[inside] - lo
-        remap[~inside] = n_own + np.searchsorted(halo, rows[~inside])
-        k = rows.shape[1] if rows.ndim == 2 else nbr.shape[1]
-        halo_rows = np.repeat((n_own + np.arange(len(halo), dtype=np.int64))[:, None], k, axis=1)
-        local = np.concatenate([remap, halo_rows], axis=0) if len(halo) else remap
-        return cls(rank, world, lo, hi, halo, {int(r): v for r, v in recv.items()},
-                   {int(d): np.asarray(v, dtype=np.int64) for d, v in send.items()}, local)
-
-    # ------------------------------------------------------------------ exchanges
-    def _send_rows(self, owned: torch.Tensor) -> dict:
-        return {d: owned[torch.as_tensor(ids, device=owned.device)] for d, ids in self.send_lists.items()}
-
-    def gather_halo(self, owned: torch.Tensor, transport) -> torch.Tensor:
-        """[n_own, C] owned rows -> [n_own + n_halo, C] with the halo rows filled in."""
-        c = owned.shape[1:]
-        out = torch.empty((self.n_local,) + tuple(c), dtype=owned.dtype, device=owned.device)
-        out[: self.n_own] = owned
-        if isinstance(transport, DistTransport):
-            got = transport.exchange(self._send_rows(owned),
-                                     {s: (len(p),) + tuple(c) for s, p in self.recv_lists.items()},
-                                     owned.dtype, owned.device)
-        else:
-            got = transport.collect(self.rank, self.recv_lists.keys())
-        for s, pos in self.recv_lists.items():
-            out[self.n_own + torch.as_tensor(pos, device=owned.device)] = got[s].to(owned.device)
-        return out
-
-    def post_halo(self, owned: torch.Tensor, transport: LocalTransport):
-        """LocalTransport only: publish this rank's rows for the others' gather_halo."""
-        transport.post(self.rank, self._send_rows(owned))
-
-    def _halo_partials(self, local: torch.Tensor) -> dict:
-        return {s: local[self.n_own + torch.as_tensor(pos, device=local.device)] for s, pos in self.recv_lists.items()}
-
-    def scatter_halo_add(self, local: torch.Tensor, transport) -> torch.Tensor:
-        """Return the owned rows of `local` plus every other rank's partial contribution
-        to them, added in ascending source-rank order (deterministic)."""
-        c = local.shape[1:]
-        owned = local[: self.n_own].clone()
-        if isinstance(transport, DistTransport):
-            got = transport.exchange(self._halo_partials(local),
-                                     {d: (len(ids),) + tuple(c) for d, ids in self.send_lists.items()},
-                                     local.dtype, local.device)
-        else:
-            got = transport.collect(self.rank, self.send_lists.keys())
-        for d in sorted(got):
-            idx = torch.as_tensor(self.send_lists[d], device=local.device)
-            owned.index_add_(0, idx, got[d].to(local.device))  # ids unique per source
-        return owned
-
-    def post_partials(self, local: torch.Tensor, transport: LocalTransport):
-        transport.post(self.rank, self._halo_partials(local))
-
-
-# ---------------------------------------------------------------------------- sharded layer
-def cuda_compute():
-    """The product compute: flex-conv forward / backward through libflexconv_b200.so."""
+# ---------------------------------------------------------------------------- sharded cloud
+def default_kernels():
+    """The product kernels (libflexconv_b200.so): kNN, conv forward / backward, CSR."""
     from . import _ops
 
-    def fwd(feat, loc, nbr, theta, theta_b):
-        nbr32 = torch.as_tensor(nbr).to(feat.device, torch.int32)
-        return _ops.conv_forward(feat, loc, nbr32, theta, theta_b, 1, feat.shape[0])
+    def knn(points, k):
+        return _ops.knn(points.contiguous(), 1, points.shape[0], k)
 
-    def bwd(g, feat, loc, nbr, theta, theta_b):
-        nbr32 = torch.as_tensor(nbr).to(feat.device, torch.int32)
-        csr = _ops.csr_build(nbr32, 1, feat.shape[0])
-        df, dth, dtb, dl = _ops.conv_backward(g, feat, loc, nbr32, csr, theta, theta_b, 1, feat.shape[0])
-        return df, dth, dtb, dl
+    def conv_fwd(feat, loc, nbr, theta, theta_b):
+        return _ops.conv_forward(feat, loc, nbr, theta, theta_b, 1, feat.shape[0])
 
-    return fwd, bwd
+    def conv_bwd(g, feat, loc, nbr, csr, theta, theta_b, need):
+        return _ops.conv_backward(g, feat, loc, nbr, csr, theta, theta_b, 1, feat.shape[0], need=need)
 
+    def csr(nbr):
+        return _ops.csr_build(nbr, 1, nbr.shape[0], validate=False)
 
-def sharded_forward(plan: HaloPlan, feat_local, loc_local, theta, theta_b, compute=None):
-    """Owned rows of flex_conv on the local [owned | halo] buffers."""
-    fwd, _ = compute or cuda_compute()
-    return fwd(feat_local, loc_local, plan.local_nbr, theta, theta_b)[: plan.n_own]
+    return {"knn": knn, "conv_fwd": conv_fwd, "conv_bwd": conv_bwd, "csr": csr}
 
 
-def sharded_backward_local(plan: HaloPlan, g_owned, feat_local, loc_local, theta, theta_b, compute=None):
-    """Local backward with zero upstream on the halo rows: returns the LOCAL partials
-    (d_features [n_local, C], d_theta, d_theta_b, d_locations [n_local, d]); finish with
-    scatter_halo_add on d_features / d_locations and fixed_order_allreduce on theta."""
-    _, bwd = compute or cuda_compute()
-    pad = torch.zeros((len(plan.halo),) + tuple(g_owned.shape[1:]), dtype=g_owned.dtype, device=g_owned.device)
-    g_local = torch.cat([g_owned, pad], 0)
-    return bwd(g_local, feat_local, loc_local, plan.local_nbr, theta, theta_b)
+class ShardedCloud:
+    """This rank's part of a point-chunk sharded cloud: owned rows [lo, hi) of the globally
+    (spatially) ordered cloud plus the halo, with everything the layers need on the device.
+
+    Local point ids: owned global g -> g - lo; halo[q] -> n_own + q.  `table` is the int32
+    [n_own + n_halo, k] neighbour table over local ids (halo rows are self-loops: they carry
+    zero upstream gradient and their forward outputs are discarded); `csr` its reverse.
+    """
+
+    def __init__(self):
+        raise TypeError("use ShardedCloud.build(...)")
+
+    @classmethod
+    def build(cls, positions: torch.Tensor, k: int, comm: Comm, kernels=None) -> "ShardedCloud":
+        """positions: this rank's owned points [n_own, d] (a contiguous block, in rank order,
+        of the spatially ordered cloud).  Collective over `comm`."""
+        self = object.__new__(cls)
+        kern = kernels or default_kernels()
+        self.comm, self.k, self.kernels = comm, int(k), kern
+        rank, world = comm.rank, comm.world
+        dev = positions.device
+        pos = positions.contiguous()
+        n_own, d = pos.shape
+        sizes = [int(t.item()) for t in comm.all_gather(torch.tensor([n_own], dtype=torch.int64, device=dev))]
+        self.bounds = [0]
+        for s in sizes:
+            self.bounds.append(self.bounds[-1] + s)
+        self.lo, self.hi = self.bounds[rank], self.bounds[rank + 1]
+        self.n_own, self.n_global = n_own, self.bounds[-1]
+        if min(sizes) < self.k:
+            raise ConfigInvalidError(f"every rank needs at least k={self.k} points (sizes {sizes})")
+
+        # 1) ghost shell: R = the largest k-th-neighbour distance among owned points when only
+        #    owned points are candidates (an upper bound on every owned point's true one)
+        own_tab = kern["knn"](pos, self.k).long()
+        p64 = pos.double()
+        r2 = ((p64 - p64[own_tab[:, -1]]) ** 2).sum(dim=1).max()
+        radius = torch.sqrt(r2) * (1.0 + 1e-9) + 1e-300
+        meta = torch.cat([p64.min(dim=0).values, p64.max(dim=0).values, radius.reshape(1)])
+        metas = comm.all_gather(meta)
+        sends_pos, sends_gid = {}, {}
+        for q in range(world):
+            if q == rank:
+                continue
+            lo_box = metas[q][:d] - metas[q][2 * d]
+            hi_box = metas[q][d:2 * d] + metas[q][2 * d]
+            mask = ((p64 >= lo_box) & (p64 <= hi_box)).all(dim=1)
+            ids = torch.nonzero(mask).flatten()
+            sends_pos[q] = pos[ids]
+            sends_gid[q] = ids + self.lo
+        counts = comm.exchange_sizes({q: t.shape[0] for q, t in sends_pos.items()})
+        got_pos = comm.exchange(sends_pos, {q: (c, d) for q, c in counts.items()}, pos.dtype, dev)
+        got_gid = comm.exchange(sends_gid, {q: (c,) for q, c in counts.items()}, torch.int64, dev)
+        # candidates ordered by global id: ghosts of lower ranks, owned block, higher ranks
+        before = [q for q in range(rank) if q in got_pos]
+        after = [q for q in range(rank + 1, world) if q in got_pos]
+        cand_pos = torch.cat([got_pos[q] for q in before] + [pos] + [got_pos[q] for q in after])
+        own_gid = torch.arange(self.lo, self.hi, device=dev, dtype=torch.int64)
+        cand_gid = torch.cat([got_gid[q] for q in before] + [own_gid] + [got_gid[q] for q in after])
+        off = sum(got_pos[q].shape[0] for q in before)
+        self.n_ghost = int(cand_pos.shape[0] - n_own)
+
+        # 2) exact rows of the owned points, in global ids
+        cand_tab = kern["knn"](cand_pos, self.k).long()
+        rows = cand_gid[cand_tab[off:off + n_own]]
+        self.global_rows = rows  # [n_own, k] global ids (inspection / tests)
+        outside = (rows < self.lo) | (rows >= self.hi)
+        self.halo = torch.unique(rows[outside])  # sorted global ids
+        n_halo = int(self.halo.numel())
+        self.n_local = n_own + n_halo
+        local = torch.where(outside, n_own + torch.searchsorted(self.halo, rows), rows - self.lo)
+        self_rows = (n_own + torch.arange(n_halo, device=dev, dtype=torch.int64))[:, None].expand(n_halo, self.k)
+        self.table = torch.cat([local, self_rows]).to(torch.int32).contiguous()
+        # halo positions come with the ghosts (no further exchange)
+        self.positions = torch.cat([pos, cand_pos[torch.searchsorted(cand_gid, self.halo)]]).contiguous()
+
+        # 3) exchange lists: the halo ids owned by rank q form a contiguous slice of `halo`
+        bnd = torch.tensor(self.bounds, device=dev, dtype=torch.int64)
+        cuts = torch.searchsorted(self.halo, bnd).tolist()
+        self.recv_slices = {q: (cuts[q], cuts[q + 1]) for q in range(world) if q != rank and cuts[q + 1] > cuts[q]}
+        req = {q: self.halo[a:b] - self.bounds[q] for q, (a, b) in self.recv_slices.items()}
+        counts = comm.exchange_sizes({q: t.numel() for q, t in req.items()})
+        got = comm.exchange(req, {q: (c,) for q, c in counts.items() if c > 0}, torch.int64, dev)
+        self.send_idx = {q: t for q, t in got.items()}  # owned local ids rank q needs from here
+        self.csr = kern["csr"](self.table)
+        return self
+
+    # ------------------------------------------------------------------ row exchanges
+    def gather(self, owned: torch.Tensor) -> torch.Tensor:
+        """[n_own, C] owned rows -> [n_local, C] with the halo rows from their owners."""
+        c = tuple(owned.shape[1:])
+        out = torch.empty((self.n_local,) + c, dtype=owned.dtype, device=owned.device)
+        out[: self.n_own] = owned
+        got = self.comm.exchange({q: owned[i] for q, i in self.send_idx.items()},
+                                 {q: (b - a,) + c for q, (a, b) in self.recv_slices.items()}, owned.dtype,
+                                 owned.device)
+        for q, (a, b) in self.recv_slices.items():
+            out[self.n_own + a:self.n_own + b] = got[q]
+        return out
+
+    def scatter_add(self, local: torch.Tensor) -> torch.Tensor:
+        """Owned rows of `local` plus the other ranks' halo-row partials for them, added in
+        ascending source-rank order (deterministic: indices are unique per source)."""
+        c = tuple(local.shape[1:])
+        owned = local[: self.n_own].clone()
+        got = self.comm.exchange({q: local[self.n_own + a:self.n_own + b] for q, (a, b) in self.recv_slices.items()},
+                                 {q: (i.numel(),) + c for q, i in self.send_idx.items()}, local.dtype, local.device)
+        for q in sorted(got):
+            owned.index_add_(0, self.send_idx[q], got[q])
+        return owned
+
+    @property
+    def halo_fraction(self) -> float:
+        return (self.n_local - self.n_own) / max(self.n_own, 1)
+
+
+class ShardedFlexConv:
+    """flex_conv on a ShardedCloud: owned rows of the forward, and the training backward
+    (d_features / d_locations of the owned rows, d_theta / d_theta_b summed over ranks)."""
+
+    def __init__(self, cloud: ShardedCloud):
+        self.cloud = cloud
+        self._saved = None
+
+    def forward(self, feat_owned, theta, theta_b):
+        cl = self.cloud
+        pos = cl.positions.to(feat_owned.dtype)
+        feat = cl.gather(feat_owned)
+        out = cl.kernels["conv_fwd"](feat, pos, cl.table, theta, theta_b)
+        self._saved = (feat, pos, theta, theta_b)
+        return out[: cl.n_own]
+
+    def backward(self, g_owned, with_locations=True):
+        cl = self.cloud
+        feat, pos, theta, theta_b = self._saved
+        self._saved = None
+        g = torch.zeros((cl.n_local,) + tuple(g_owned.shape[1:]), dtype=g_owned.dtype, device=g_owned.device)
+        g[: cl.n_own] = g_owned
+        df, dth, dtb, dl = cl.kernels["conv_bwd"](g, feat, pos, cl.table, cl.csr, theta, theta_b,
+                                                  (True, True, True, bool(with_locations)))
+        df = cl.scatter_add(df)
+        dl = cl.scatter_add(dl) if with_locations else None
+        grads = cl.comm.ordered_sum(torch.cat([dth.reshape(-1), dtb.reshape(-1)]))
+        return df, grads[: dth.numel()].view_as(dth), grads[dth.numel():].view_as(dtb), dl

@@ -1,9 +1,11 @@
 """Worker for tests/test_parallel.py: launched with torch.distributed.run (gloo, CPU).
 
-Checks that point-chunk sharding with halos (paper_1803_07289_b200.parallel) reproduces
-the unsharded flex-conv forward / backward.  The compute callback here is the CPU ORACLE
-(test infrastructure): the sharding, halo exchange and reductions under test are product
-code; only the per-shard arithmetic is stood in for, because this host has no GPU.
+Point-chunk sharding of one cloud (parallel.ShardedCloud / ShardedFlexConv): every rank
+holds only its block of the spatially ordered cloud; the sharded kNN (ghost shell), the
+halo plan, the halo exchanges and the gradient reductions under test are product code.
+The per-rank arithmetic (kNN, flex-conv forward / backward) is the CPU ORACLE here (test
+infrastructure) because this host has no GPU; tests/test_gpu_parallel.py runs the same
+path with the CUDA kernels.  Also checks the batch-sharded gradient combination.
 """
 
 import json
@@ -22,15 +24,18 @@ from paper_1803_07289_b200 import parallel  # noqa: E402
 from paper_1803_07289_b200.core import synthetic_layer  # noqa: E402
 
 
-def oracle_compute():
-    def fwd(feat, loc, nbr, th, tb):
-        return torch.from_numpy(oracle.conv_forward(feat.numpy(), loc.numpy(), nbr, th.numpy(), tb.numpy(), 1))
+def oracle_kernels():
+    def knn(points, k):
+        return torch.from_numpy(oracle.knn_brute(points.numpy().astype(np.float64), k))
 
-    def bwd(g, feat, loc, nbr, th, tb):
-        df, dth, dtb, dl = oracle.conv_backward(g.numpy(), feat.numpy(), loc.numpy(), nbr, th.numpy(), tb.numpy())
-        return tuple(torch.from_numpy(x) for x in (df, dth, dtb, dl))
+    def conv_fwd(feat, loc, nbr, th, tb):
+        return torch.from_numpy(oracle.conv_forward(feat.numpy(), loc.numpy(), nbr.numpy(), th.numpy(), tb.numpy(), 1))
 
-    return fwd, bwd
+    def conv_bwd(g, feat, loc, nbr, csr, th, tb, need):
+        out = oracle.conv_backward(g.numpy(), feat.numpy(), loc.numpy(), nbr.numpy(), th.numpy(), tb.numpy())
+        return tuple(torch.from_numpy(x) for x in out)
+
+    return {"knn": knn, "conv_fwd": conv_fwd, "conv_bwd": conv_bwd, "csr": lambda nbr: None}
 
 
 def main():
@@ -38,44 +43,38 @@ def main():
     rank, world = dist.get_rank(), dist.get_world_size()
     n, k, cin, cout = 3000, 8, 6, 5
     loc, feat, th, tb, up = synthetic_layer(41, 0, n, 3, cin, cout)
-    # spatial order (x-major sort is enough for a test) + exact kNN, identical on all ranks
+    # exact duplicates across the cloud (index tie-breaking must be the global one)
+    loc[2500:2520] = loc[10:30]
+    # spatial order (x-major sort is enough for a test), identical on all ranks
     order = np.lexsort((loc[:, 2], loc[:, 1], loc[:, 0]))
     loc, feat, up = loc[order], feat[order], up[order]
-    nbr = oracle.knn_brute(loc, k)
-    tr = parallel.DistTransport()
-    plan = parallel.HaloPlan.build_local(nbr, world, rank, tr)
-    ref_plan = parallel.HaloPlan.build_all(nbr, world)[rank]
-    same_plan = (np.array_equal(plan.halo, ref_plan.halo) and np.array_equal(plan.local_nbr, ref_plan.local_nbr)
-                 and sorted(plan.send_lists) == sorted(ref_plan.send_lists)
-                 and all(np.array_equal(plan.send_lists[d], ref_plan.send_lists[d]) for d in plan.send_lists))
-    lo, hi = plan.lo, plan.hi
+    lo, hi = parallel.shard_range(n, world, rank)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a))  # noqa: E731
-    feat_l = plan.gather_halo(t(feat[lo:hi]), tr)
-    loc_l = plan.gather_halo(t(loc[lo:hi]), tr)
-    comp = oracle_compute()
-    out = parallel.sharded_forward(plan, feat_l, loc_l, t(th), t(tb), comp)
-    df_l, dth, dtb, dl_l = parallel.sharded_backward_local(plan, t(up[lo:hi]), feat_l, loc_l, t(th), t(tb), comp)
-    df = plan.scatter_halo_add(df_l, tr)
-    dl = plan.scatter_halo_add(dl_l, tr)
-    dth = parallel.fixed_order_allreduce(dth)
-    dtb = parallel.fixed_order_allreduce(dtb)
-    # unsharded reference
-    ref_out = oracle.conv_forward(feat, loc, nbr, th, tb, 1)
-    rdf, rdth, rdtb, rdl = oracle.conv_backward(up, feat, loc, nbr, th, tb)
+    comm = parallel.Comm(device=torch.device("cpu"))
+    cloud = parallel.ShardedCloud.build(t(loc[lo:hi]), k, comm, kernels=oracle_kernels())
+    ref_nbr = oracle.knn_brute(loc, k)
+    layer = parallel.ShardedFlexConv(cloud)
+    out = layer.forward(t(feat[lo:hi]), t(th), t(tb))
+    df, dth, dtb, dl = layer.backward(t(up[lo:hi]))
+    ref_out = oracle.conv_forward(feat, loc, ref_nbr, th, tb, 1)
+    rdf, rdth, rdtb, rdl = oracle.conv_backward(up, feat, loc, ref_nbr, th, tb)
     res = {
         "rank": rank,
-        "halo": int(len(plan.halo)),
-        "same_plan": bool(same_plan),
+        "bounds": cloud.bounds,
+        "halo": int(cloud.halo.numel()),
+        "ghosts": cloud.n_ghost,
+        "knn_rows_exact": bool(np.array_equal(cloud.global_rows.numpy(), ref_nbr[lo:hi])),
+        "halo_outside": bool(((cloud.halo < lo) | (cloud.halo >= hi)).all()),
         "fwd_bitwise": bool(np.array_equal(out.numpy(), ref_out[lo:hi])),
         "df_err": float(np.abs(df.numpy() - rdf[lo:hi]).max() / np.abs(rdf).max()),
         "dl_err": float(np.abs(dl.numpy() - rdl[lo:hi]).max() / np.abs(rdl).max()),
         "dth_err": float(np.abs(dth.numpy() - rdth).max() / np.abs(rdth).max()),
         "dtb_err": float(np.abs(dtb.numpy() - rdtb).max() / np.abs(rdtb).max()),
     }
-    # determinism of the fixed-order reduction
-    again = parallel.fixed_order_allreduce(parallel.sharded_backward_local(
-        plan, t(up[lo:hi]), feat_l, loc_l, t(th), t(tb), comp)[1])
-    res["allreduce_bitwise"] = bool(torch.equal(again, dth))
+    # determinism of the whole sharded backward (fixed-order reductions)
+    layer.forward(t(feat[lo:hi]), t(th), t(tb))
+    again = layer.backward(t(up[lo:hi]))
+    res["backward_bitwise_repeat"] = bool(all(torch.equal(a, b) for a, b in zip(again, (df, dth, dtb, dl))))
     # batch-sharded gradient combination (network.train_step_batch): per-unit rows summed in
     # global unit order must equal the single-process sequential loop bitwise
     units = 5
@@ -87,7 +86,7 @@ def main():
         seq += r
     res["ordered_sum_bitwise"] = bool(torch.equal(got, seq))
     out_dir = os.environ.get("FC_RESULT_DIR")
-    if out_dir:  # one file per rank: the two ranks' stdout lines can interleave
+    if out_dir:  # one file per rank: the ranks' stdout lines can interleave
         with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fh:
             json.dump(res, fh)
     else:

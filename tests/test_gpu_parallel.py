@@ -1,58 +1,41 @@
-"""GPU: point-chunk sharding with halos, emulated in one process (LocalTransport) with the
-CUDA engines as the per-shard compute, against the unsharded CUDA operator; and batch
-sharding of the torch ops."""
+"""GPU: point-chunk sharding of one cloud (parallel.ShardedCloud / ShardedFlexConv) with
+the product kernels, 2 and 4 ranks sharing the test box's GPU (gloo transport), against
+the unsharded CUDA operator: ghost-shell kNN rows exact, forward rows bitwise, backward to
+fp32 rounding (the owners add the other ranks' halo partials after their own sums)."""
 
-import numpy as np
+import json
+import os
+import socket
+import subprocess
+import sys
+
 import pytest
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_emulated_point_chunk_sharding_matches_unsharded(fc):
-    import torch
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
-    from paper_1803_07289_b200 import _ops, parallel
-    from paper_1803_07289_b200.core import synthetic_layer
 
-    n, k, c, world = 200_000, 8, 64, 4
-    loc, feat, th, tb, up = synthetic_layer(51, 0, n, 3, c, c)
-    dev = torch.device("cuda")
-    pos = torch.from_numpy(loc).to(dev, torch.float32)
-    order = _ops.spatial_order(pos).long()
-    pos = pos[order].contiguous()
-    f = torch.from_numpy(feat).to(dev, torch.float32)[order].contiguous()
-    g = torch.from_numpy(up).to(dev, torch.float32)[order].contiguous()
-    theta = torch.from_numpy(th).to(dev, torch.float32)
-    theta_b = torch.from_numpy(tb).to(dev, torch.float32)
-    nbr = _ops.knn(pos, 1, n, k)
-    csr = _ops.csr_build(nbr, 1, n)
-    ref_out = _ops.conv_forward(f, pos, nbr, theta, theta_b, 1, n)
-    rdf, rdth, rdtb, rdl = _ops.conv_backward(g, f, pos, nbr, csr, theta, theta_b, 1, n)
-
-    plans = parallel.HaloPlan.build_all(nbr.cpu().numpy(), world)
-    tr = parallel.LocalTransport(world)
-    for p in plans:
-        p.post_halo(f[p.lo:p.hi], tr)
-    feat_l = [p.gather_halo(f[p.lo:p.hi], tr) for p in plans]
-    for p in plans:
-        p.post_halo(pos[p.lo:p.hi], tr)
-    loc_l = [p.gather_halo(pos[p.lo:p.hi], tr) for p in plans]
-    outs = [parallel.sharded_forward(p, feat_l[r], loc_l[r], theta, theta_b) for r, p in enumerate(plans)]
-    # forward rows are computed from identical inputs in identical order: bitwise equal
-    assert torch.equal(torch.cat(outs), ref_out)
-
-    parts = [parallel.sharded_backward_local(p, g[p.lo:p.hi], feat_l[r], loc_l[r], theta, theta_b)
-             for r, p in enumerate(plans)]
-    for r, p in enumerate(plans):
-        p.post_partials(parts[r][0], tr)
-    df = torch.cat([p.scatter_halo_add(parts[r][0], tr) for r, p in enumerate(plans)])
-    for r, p in enumerate(plans):
-        p.post_partials(parts[r][3], tr)
-    dl = torch.cat([p.scatter_halo_add(parts[r][3], tr) for r, p in enumerate(plans)])
-    dth = sum(x[1].double() for x in parts).float()
-    dtb = sum(x[2].double() for x in parts).float()
-    torch.testing.assert_close(df, rdf, rtol=1e-4, atol=1e-5)
-    for got, ref in ((dth, rdth), (dtb, rdtb), (dl, rdl)):
-        ref = ref.double()
-        err = (got.double() - ref).abs().max() / ref.abs().max()
-        assert err < 1e-5, float(err)
+@pytest.mark.parametrize("world", [2, 4])
+def test_point_chunk_sharding_on_gpu(fc, tmp_path, world):
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1", FC_RESULT_DIR=str(tmp_path))
+    for attempt in range(3):  # retries only guard against a rendezvous-port race
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+               os.path.join(ROOT, "tests", "_dist_worker_gpu.py")]
+        proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+        if proc.returncode == 0:
+            break
+    assert proc.returncode == 0, proc.stderr[-4000:]
+    for r in range(world):
+        res = json.loads((tmp_path / f"rank{r}.json").read_text())
+        assert res["halo"] > 0 and res["ghosts"] >= res["halo"], res
+        assert res["knn_rows_exact"], res
+        assert res["fwd_bitwise"], res
+        assert res["df_err"] < 1e-5 and res["dl_err"] < 1e-5, res
+        assert res["dth_err"] < 1e-5 and res["dtb_err"] < 1e-5, res
