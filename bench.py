@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=7_000_000)
+    ap.add_argument("--n", "--points", dest="n", type=int, default=7_000_000)
     ap.add_argument("--k", type=int, default=8)
     ap.add_argument("--c", type=int, default=64)
     ap.add_argument("--mode", default="auto")
@@ -51,6 +51,12 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp64", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: host-staged transport, only to exercise N ranks on one GPU")
+    ap.add_argument("--shard", default=None, choices=["points", "clouds"],
+                    help="N > 1: 'points' (default) = ONE n-point cloud point-chunk sharded with halos over "
+                         "the ranks (strong scaling, the north_star's 7M cloud on 8 GPUs); 'clouds' = an "
+                         "independent n-point cloud per rank (weak scaling)")
     return ap.parse_args()
 
 
@@ -271,17 +277,16 @@ def time_cpu_step(kind, nat, sample):
 
 
 # ------------------------------------------------------------------ workload
-def make_workload(n, k, c, rank, dev, d=3):
-    """The bench's synthetic layer on `dev` (tests/test_gpu_scale.py checks this exact
-    workload against the oracle): positions on the 2^-24 lattice (exact in fp32), spatially
-    ordered once, exact kNN table and reverse CSR; features / upstream N(0,1), theta /
-    theta_b 0.1 N(0,1).  Setup costs are timed with CUDA events and returned."""
+def make_cloud(n, c, seed, dev, d=3):
+    """The synthetic layer inputs: positions on the 2^-24 lattice (exact in fp32), spatially
+    ordered once; features / upstream N(0,1), theta / theta_b 0.1 N(0,1).  Returns the
+    tensors and the spatial-order time (ms)."""
     import torch
 
     from paper_1803_07289_b200 import _ops
 
     gen = torch.Generator(device=dev)
-    gen.manual_seed(1234 + rank)
+    gen.manual_seed(seed)
     pos = torch.floor(torch.rand(n, d, generator=gen, device=dev, dtype=torch.float64) * 2 ** 24) / 2 ** 24
     pos = pos.to(torch.float32)
     torch.cuda.synchronize()
@@ -296,6 +301,19 @@ def make_workload(n, k, c, rank, dev, d=3):
     g = torch.randn(n, c, generator=gen, device=dev)
     theta = 0.1 * torch.randn(c, c, d, generator=gen, device=dev)
     theta_b = 0.1 * torch.randn(c, c, generator=gen, device=dev)
+    return {"pos": pos, "feat": feat, "g": g, "theta": theta, "theta_b": theta_b, "sort_ms": sort_ms}
+
+
+def make_workload(n, k, c, rank, dev, d=3):
+    """The bench's synthetic layer on `dev` (tests/test_gpu_scale.py checks this exact
+    workload against the oracle): make_cloud + the exact kNN table and reverse CSR, their
+    setup costs timed with CUDA events."""
+    import torch
+
+    from paper_1803_07289_b200 import _ops
+
+    w = make_cloud(n, c, 1234 + rank, dev, d)
+    pos, feat, g, theta, theta_b, sort_ms = (w[x] for x in ("pos", "feat", "g", "theta", "theta_b", "sort_ms"))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -329,10 +347,17 @@ def main():
     import torch
     import torch.distributed as dist
 
+    local = local % torch.cuda.device_count()  # (ranks share a GPU only in --backend gloo tests)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    shard = args.shard or ("points" if world > 1 else "clouds")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    if shard == "points":
+        return run_sharded(args, world, rank, local, dev)
 
     from paper_1803_07289_b200 import _lib, _ops
 
@@ -466,6 +491,148 @@ def main():
             "fp64_engine": fp64,
             "e2e": e2e,
             "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline_line(args, k, c):
+    kind, nat = cpu_kernels()
+    sample = cpu_sample(args.cpu_sample, k, c)
+    tf, tb_ = time_cpu_step(kind, nat, sample)
+    return {"value": round(args.cpu_sample / (tf + tb_), 1), "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
+            "sample": f"{args.cpu_sample}-point cloud, K={k}, {c}->{c}, fwd {tf:.2f}s on {os.cpu_count()} threads + "
+                      f"bwd {tb_:.2f}s (single-threaded by reference design, _native.pyx:77-78), fp64"}
+
+
+def run_sharded(args, world, rank, local, dev):
+    """ONE n-point cloud, point-chunk sharded with halos over the ranks (parallel.ShardedCloud):
+    each rank keeps its block of the spatially ordered cloud, builds its exact kNN rows with
+    the ghost-shell exchange (no global table anywhere), and a step is the sharded layer's
+    forward (halo gather + kernels) and training backward (kernels, halo partials back to
+    their owners, ordered d_theta sum).  value = n / max-over-ranks step time (strong)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1803_07289_b200 import _lib, parallel
+
+    n, k, c, d = args.n, args.k, args.c, 3
+    w = make_cloud(n, c, 1234, dev)  # the same cloud on every rank; each keeps its block
+    lo, hi = parallel.shard_range(n, world, rank)
+    pos, feat, g = (w[x][lo:hi].contiguous() for x in ("pos", "feat", "g"))
+    theta, theta_b = w["theta"], w["theta_b"]
+    del w
+    torch.cuda.empty_cache()
+    comm = parallel.Comm(device=dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    cloud = parallel.ShardedCloud.build(pos, k, comm)
+    torch.cuda.synchronize()
+    build_ms = (time.perf_counter() - t0) * 1e3
+    layer = parallel.ShardedFlexConv(cloud)
+    # the layer's inputs live in [owned | halo] buffers (what a network's previous layer
+    # would write into); the halo rows are exchanged inside every step
+    feat_l, g_l = cloud.local_buffer(feat), cloud.local_buffer(g)
+
+    def step():
+        layer.forward(feat_l, theta, theta_b)
+        layer.backward(g_l)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            step()
+        b.record()
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    ms = a.elapsed_time(b)
+    stats = torch.tensor([ms, cloud.halo_fraction, build_ms, cloud.n_ghost / max(cloud.n_own, 1)], device=dev,
+                         dtype=torch.float64)
+    gathered = comm.all_gather(stats) if world > 1 else [stats]
+    ms = max(float(t[0]) for t in gathered)
+    ms_step = ms / args.steps
+    with _lib.KernelTimer() as kt:
+        for _ in range(max(1, min(args.steps, 5))):
+            step()
+    kern = {name: statistics.mean(v) for name, v in kt.times.items() if v and min(v) >= 0}
+    hbm, bf16, src = peaks()
+    n_loc = cloud.n_local
+    kernels = {}
+    for name, kms in kern.items():
+        bpp = kernel_bytes_per_point(name, c, c, d, k)
+        kernels[name] = {"ms": round(kms, 4), "bytes_per_point": bpp, "rows": n_loc,
+                         "GBps": round(bpp * n_loc / kms / 1e6, 1) if bpp else None,
+                         "frac": round(bpp * n_loc / kms / 1e6 / hbm, 4) if bpp else None}
+    dom = max((nm for nm in kern if kernel_bytes_per_point(nm, c, c, d, k)), key=kern.get, default=None)
+    roofline = None
+    if dom:
+        ach = kernel_bytes_per_point(dom, c, c, d, k) * n_loc / (kern[dom] / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(ach / hbm, 4), "traffic": None, "peak_source": src,
+                    "note": f"rank 0's shard ({n_loc} local rows incl. halo)", "kernels": kernels}
+    # e2e: every step each rank copies its owned inputs in from pinned host buffers and its
+    # results (forward output, d_features, d_locations, d_theta, d_theta_b) back out
+    e2e = None
+    if not args.no_e2e:
+        host_in = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t) for t in (feat, g)]
+        host_out = [torch.empty(s_, dtype=torch.float32, pin_memory=True)
+                    for s_ in ((hi - lo, c), (hi - lo, c), (hi - lo, d), tuple(theta.shape), tuple(theta_b.shape))]
+
+        def e2e_step():  # H2D straight into the owned rows of the layer's local buffers
+            feat_l[: cloud.n_own].copy_(host_in[0], non_blocking=True)
+            g_l[: cloud.n_own].copy_(host_in[1], non_blocking=True)
+            out = layer.forward(feat_l, theta, theta_b)
+            host_out[0].copy_(out, non_blocking=True)
+            df, dth, dtb, dl = layer.backward(g_l)
+            for h, t in zip(host_out[1:], (df, dl, dth, dtb)):
+                h.copy_(t, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e_steps = max(1, min(args.steps, 10))
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record()
+        for _ in range(e_steps):
+            e2e_step()
+        eb.record()
+        torch.cuda.synchronize()
+        ems = torch.tensor([ea.elapsed_time(eb) / e_steps], device=dev, dtype=torch.float64)
+        ems = max(float(t[0]) for t in comm.all_gather(ems)) if world > 1 else float(ems[0])
+        e2e = {"value": round(n / (ems / 1e3), 1), "unit": UNIT,
+               "h2d_bytes_per_step": sum(t.numel() * t.element_size() for t in host_in) * world,
+               "d2h_bytes_per_step": sum(t.numel() * t.element_size() for t in host_out) * world,
+               "ms_per_step": round(ems, 3), "steps": e_steps,
+               "path": "per rank: owned features / upstream H2D from pinned host buffers, sharded forward + "
+                       "backward (halo exchanges over NCCL), owned results + theta gradients D2H (bytes summed "
+                       "over ranks)"}
+    cpu = cpu_baseline_line(args, k, c) if (rank == 0 and not args.no_cpu) else None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(n / (ms_step / 1e3), 1), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"flex_conv fwd+bwd (with d_locations) on ONE {n}-point uniform cloud, K={k}, "
+                                   f"{c}->{c}, Dp=3, point-chunk sharded with halos over {world} GPU(s)",
+                       "points_total": n, "k": k, "c_in": c, "c_out": c, "dp": d, "parallelism": f"points{world}",
+                       "halo_fraction_max": round(max(float(t[1]) for t in gathered), 4),
+                       "ghost_fraction_max": round(max(float(t[3]) for t in gathered), 4),
+                       "setup_ms": {"sharded_knn_and_plan_max": round(max(float(t[2]) for t in gathered), 2)},
+                       "l2": "inputs exceed the 126 MB L2; no flush needed"},
+            "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": e2e, "clocks": clk.summary(),
         }
         print(json.dumps(line))
     if world > 1:

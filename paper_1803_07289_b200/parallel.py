@@ -107,9 +107,10 @@ class Comm:
 
         self.dist = dist
         self.group = group
-        self.rank = dist.get_rank(group)
-        self.world = dist.get_world_size(group)
-        self.host = dist.get_backend(group) == "gloo"
+        single = not (dist.is_available() and dist.is_initialized())
+        self.rank = 0 if single else dist.get_rank(group)
+        self.world = 1 if single else dist.get_world_size(group)
+        self.host = (not single) and dist.get_backend(group) == "gloo"
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else \
                 torch.device("cpu")
@@ -117,6 +118,8 @@ class Comm:
 
     def all_gather(self, t: torch.Tensor) -> list[torch.Tensor]:
         """Same-shape tensors from every rank, in rank order."""
+        if self.world == 1:
+            return [t]
         w = t.contiguous().to(self.wire)
         parts = [torch.empty_like(w) for _ in range(self.world)]
         self.dist.all_gather(parts, w, group=self.group)
@@ -210,21 +213,42 @@ class ShardedCloud:
             raise ConfigInvalidError(f"every rank needs at least k={self.k} points (sizes {sizes})")
 
         # 1) ghost shell: R = the largest k-th-neighbour distance among owned points when only
-        #    owned points are candidates (an upper bound on every owned point's true one)
+        #    owned points are candidates (an upper bound on every owned point's true one).
+        #    A rank's region is described by its occupied cells of a coarse global grid (a
+        #    block of a Morton-type order is not a box); a point is a ghost for rank q when its
+        #    cell lies within floor(R_q / cell) + 1 cells of one of q's occupied cells -- every
+        #    true neighbour of q's points does (per-axis gap <= R_q).
         own_tab = kern["knn"](pos, self.k).long()
         p64 = pos.double()
         r2 = ((p64 - p64[own_tab[:, -1]]) ** 2).sum(dim=1).max()
-        radius = torch.sqrt(r2) * (1.0 + 1e-9) + 1e-300
-        meta = torch.cat([p64.min(dim=0).values, p64.max(dim=0).values, radius.reshape(1)])
-        metas = comm.all_gather(meta)
+        radius = torch.sqrt(r2) * (1.0 + 1e-9)
+        metas = comm.all_gather(torch.cat([p64.min(dim=0).values, p64.max(dim=0).values, radius.reshape(1)]))
+        gmin = torch.stack([m[:d] for m in metas]).min(dim=0).values
+        gmax = torch.stack([m[d:2 * d] for m in metas]).max(dim=0).values
+        cells_per_axis = int(min(64, max(4, round((self.n_global / 8) ** (1.0 / d)))))
+        cs = torch.clamp((gmax - gmin) / cells_per_axis, min=1e-300)
+        shape = (cells_per_axis,) * d + (1,) * (3 - d)
+
+        def cell_ids(p):
+            c = torch.clamp(((p - gmin) / cs).floor().long(), 0, cells_per_axis - 1)
+            ids = c[:, 0]
+            for t in range(1, d):
+                ids = ids * cells_per_axis + c[:, t]
+            return ids
+
+        my_cells = cell_ids(p64)
+        occ = torch.zeros(cells_per_axis ** d, dtype=torch.uint8, device=dev)
+        occ[my_cells] = 1
+        occs = comm.all_gather(occ)
         sends_pos, sends_gid = {}, {}
         for q in range(world):
             if q == rank:
                 continue
-            lo_box = metas[q][:d] - metas[q][2 * d]
-            hi_box = metas[q][d:2 * d] + metas[q][2 * d]
-            mask = ((p64 >= lo_box) & (p64 <= hi_box)).all(dim=1)
-            ids = torch.nonzero(mask).flatten()
+            reach = int(torch.max(torch.floor(metas[q][2 * d] / cs)).item()) + 1
+            grown = torch.nn.functional.max_pool3d(occs[q].view(1, 1, *shape).float(), kernel_size=tuple(
+                2 * reach + 1 if s_ > 1 else 1 for s_ in shape), stride=1,
+                padding=tuple(reach if s_ > 1 else 0 for s_ in shape)).flatten() > 0
+            ids = torch.nonzero(grown[my_cells]).flatten()
             sends_pos[q] = pos[ids]
             sends_gid[q] = ids + self.lo
         counts = comm.exchange_sizes({q: t.shape[0] for q, t in sends_pos.items()})
@@ -265,28 +289,43 @@ class ShardedCloud:
         return self
 
     # ------------------------------------------------------------------ row exchanges
-    def gather(self, owned: torch.Tensor) -> torch.Tensor:
-        """[n_own, C] owned rows -> [n_local, C] with the halo rows from their owners."""
-        c = tuple(owned.shape[1:])
-        out = torch.empty((self.n_local,) + c, dtype=owned.dtype, device=owned.device)
-        out[: self.n_own] = owned
-        got = self.comm.exchange({q: owned[i] for q, i in self.send_idx.items()},
-                                 {q: (b - a,) + c for q, (a, b) in self.recv_slices.items()}, owned.dtype,
-                                 owned.device)
-        for q, (a, b) in self.recv_slices.items():
-            out[self.n_own + a:self.n_own + b] = got[q]
-        return out
+    def local_buffer(self, owned: torch.Tensor) -> torch.Tensor:
+        """A [n_local, C] buffer holding `owned` in its first n_own rows (halo rows zero).
+        Layers exchange halo rows in place in such buffers, so a producer that writes its
+        output straight into one (or a caller that keeps one) pays no per-call copy."""
+        buf = torch.zeros((self.n_local,) + tuple(owned.shape[1:]), dtype=owned.dtype, device=owned.device)
+        buf[: self.n_own] = owned
+        return buf
 
-    def scatter_add(self, local: torch.Tensor) -> torch.Tensor:
-        """Owned rows of `local` plus the other ranks' halo-row partials for them, added in
-        ascending source-rank order (deterministic: indices are unique per source)."""
+    def fill_halo(self, local: torch.Tensor) -> torch.Tensor:
+        """Fill the halo rows of a [n_local, C] buffer from their owners (in place)."""
         c = tuple(local.shape[1:])
-        owned = local[: self.n_own].clone()
+        got = self.comm.exchange({q: local[i] for q, i in self.send_idx.items()},
+                                 {q: (b - a,) + c for q, (a, b) in self.recv_slices.items()}, local.dtype,
+                                 local.device)
+        for q, (a, b) in self.recv_slices.items():
+            local[self.n_own + a:self.n_own + b] = got[q]
+        return local
+
+    def gather(self, owned: torch.Tensor) -> torch.Tensor:
+        """[n_own, C] owned rows -> a new [n_local, C] buffer with the halo rows filled."""
+        return self.fill_halo(self.local_buffer(owned))
+
+    def reduce_halo(self, local: torch.Tensor) -> torch.Tensor:
+        """Add the other ranks' halo-row partials for this rank's points into the owned rows
+        of `local` (in place; ascending source-rank order, indices unique per source:
+        deterministic).  Returns the owned rows (a view)."""
+        c = tuple(local.shape[1:])
         got = self.comm.exchange({q: local[self.n_own + a:self.n_own + b] for q, (a, b) in self.recv_slices.items()},
                                  {q: (i.numel(),) + c for q, i in self.send_idx.items()}, local.dtype, local.device)
+        owned = local[: self.n_own]
         for q in sorted(got):
             owned.index_add_(0, self.send_idx[q], got[q])
         return owned
+
+    def scatter_add(self, local: torch.Tensor) -> torch.Tensor:
+        """reduce_halo on a copy (leaves `local` untouched)."""
+        return self.reduce_halo(local.clone())
 
     @property
     def halo_fraction(self) -> float:
@@ -295,29 +334,35 @@ class ShardedCloud:
 
 class ShardedFlexConv:
     """flex_conv on a ShardedCloud: owned rows of the forward, and the training backward
-    (d_features / d_locations of the owned rows, d_theta / d_theta_b summed over ranks)."""
+    (d_features / d_locations of the owned rows, d_theta / d_theta_b summed over ranks).
+
+    Inputs may be owned rows ([n_own, C], copied into a local buffer per call) or local
+    buffers ([n_local, C] from cloud.local_buffer: the features' halo rows are refreshed in
+    place, the upstream gradient's halo rows must be zero) -- the latter is the copy-free
+    path a multi-layer network uses."""
 
     def __init__(self, cloud: ShardedCloud):
         self.cloud = cloud
         self._saved = None
 
-    def forward(self, feat_owned, theta, theta_b):
+    def _local(self, t):
+        return t if t.shape[0] == self.cloud.n_local else self.cloud.local_buffer(t)
+
+    def forward(self, feat, theta, theta_b):
         cl = self.cloud
-        pos = cl.positions.to(feat_owned.dtype)
-        feat = cl.gather(feat_owned)
+        pos = cl.positions if cl.positions.dtype == feat.dtype else cl.positions.to(feat.dtype)
+        feat = cl.fill_halo(self._local(feat))
         out = cl.kernels["conv_fwd"](feat, pos, cl.table, theta, theta_b)
         self._saved = (feat, pos, theta, theta_b)
         return out[: cl.n_own]
 
-    def backward(self, g_owned, with_locations=True):
+    def backward(self, g, with_locations=True):
         cl = self.cloud
         feat, pos, theta, theta_b = self._saved
         self._saved = None
-        g = torch.zeros((cl.n_local,) + tuple(g_owned.shape[1:]), dtype=g_owned.dtype, device=g_owned.device)
-        g[: cl.n_own] = g_owned
-        df, dth, dtb, dl = cl.kernels["conv_bwd"](g, feat, pos, cl.table, cl.csr, theta, theta_b,
+        df, dth, dtb, dl = cl.kernels["conv_bwd"](self._local(g), feat, pos, cl.table, cl.csr, theta, theta_b,
                                                   (True, True, True, bool(with_locations)))
-        df = cl.scatter_add(df)
-        dl = cl.scatter_add(dl) if with_locations else None
+        df = cl.reduce_halo(df)
+        dl = cl.reduce_halo(dl) if with_locations else None
         grads = cl.comm.ordered_sum(torch.cat([dth.reshape(-1), dtb.reshape(-1)]))
         return df, grads[: dth.numel()].view_as(dth), grads[dth.numel():].view_as(dtb), dl
