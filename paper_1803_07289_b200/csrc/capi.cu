@@ -3,6 +3,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 
 #include "fc_common.cuh"
 
@@ -105,6 +106,16 @@ int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int c
 int tc_reverse_gmc(int mode, int64_t total, int64_t n, int gc, int d, int k, int cout,
                    const float *rows, const float *loc, Csr csr, const float *theta,
                    const float *theta_b, float *out, cudaStream_t st);
+int tc_blocked_supported(int mode, int c_in, int d, int c_out);
+int tc_blocked_forward(int mode, int64_t total, int64_t n, int c_in, int k, int c_out, const float *feat,
+                       const float *loc, const int32_t *nbr, const float *theta, const float *theta_b, float *out,
+                       cudaStream_t st);
+int tc_blocked_deconv(int mode, int64_t total, int64_t n, int c_in, int k, int c_out, const float *x,
+                      const float *loc, Csr csr, const float *theta, const float *theta_b, float *y, cudaStream_t st);
+int tc_blocked_backward(int mode, int64_t total, int64_t n, int c_in, int k, int c_out, const float *g,
+                        const float *feat, const float *loc, const int32_t *nbr, Csr csr, const float *theta,
+                        const float *theta_b, float *d_features, float *d_locations, float *d_theta,
+                        float *d_theta_b, cudaStream_t st);
 // pool_csr.cu
 template <typename T>
 int launch_pool_fwd(int64_t total, int64_t n, int c, int k, const T *feat, const int32_t *nbr, T *out,
@@ -144,6 +155,17 @@ int launch_inverse_density(int64_t n, int d, int k, const double *pts, const int
 using namespace fc;
 
 #define ST(s) (reinterpret_cast<cudaStream_t>(s))
+
+// FC_GEMM_ROUTE=1: wide fp32 shapes on the moments + library GEMM route instead of the
+// channel-blocked tensor-core engines (A/B timing only)
+static bool blocked_route(int mode, int c_in, int d, int c_out) {
+    static int gemm = -1;
+    if (gemm < 0) {
+        const char *e = getenv("FC_GEMM_ROUTE");
+        gemm = (e && e[0] == '1') ? 1 : 0;
+    }
+    return !gemm && tc_blocked_supported(mode, c_in, d, c_out);
+}
 
 static int check_dtype(int dtype) {
     if (dtype != FC_F32 && dtype != FC_F64) return set_error(FC_ERR_CONFIG, "unknown dtype %d", dtype);
@@ -198,6 +220,10 @@ int fc_conv_forward(int dtype, int mode, int64_t batch, int64_t n, int c_in, int
             return tc_conv_forward(mode, total, n, c_in, d, k, c_out, (const float *)features,
                                    (const float *)locations, neighbors, (const float *)theta,
                                    (const float *)theta_b, (float *)out, st);
+        if (blocked_route(mode, c_in, d, c_out))
+            return tc_blocked_forward(mode, total, n, c_in, k, c_out, (const float *)features,
+                                      (const float *)locations, neighbors, (const float *)theta,
+                                      (const float *)theta_b, (float *)out, st);
         if (mode != FC_MODE_AUTO)
             return set_error(FC_ERR_UNSUPPORTED, "tensor-core engine %d does not cover c_in=%d d=%d c_out=%d", mode, c_in, d, c_out);
     }
@@ -231,6 +257,11 @@ int fc_conv_backward(int dtype, int mode, int64_t batch, int64_t n, int c_in, in
                            (const float *)locations, neighbors, Csr{rev_offsets, rev_entries}, (const float *)theta,
                            (const float *)theta_b, (float *)d_features, (float *)d_locations, (float *)d_theta,
                            (float *)d_theta_b, st);
+    if (dtype == FC_F32 && mode != FC_MODE_SIMT && blocked_route(mode, c_in, d, c_out))
+        return tc_blocked_backward(mode, total, n, c_in, k, c_out, (const float *)upstream, (const float *)features,
+                                   (const float *)locations, neighbors, Csr{rev_offsets, rev_entries},
+                                   (const float *)theta, (const float *)theta_b, (float *)d_features,
+                                   (float *)d_locations, (float *)d_theta, (float *)d_theta_b, st);
     auto run = [&](auto tag) -> int {
         using T = decltype(tag);
         const T *g = (const T *)upstream;
@@ -291,6 +322,10 @@ int fc_deconv_forward(int dtype, int mode, int64_t batch, int64_t n, int c_in, i
             return tc_reverse_gmc(mode, total, n, c_out, d, k, c_in, (const float *)x, (const float *)locations,
                                   Csr{rev_offsets, rev_entries}, (const float *)theta, (const float *)theta_b,
                                   (float *)y, st);
+        if (blocked_route(mode, c_in, d, c_out))
+            return tc_blocked_deconv(mode, total, n, c_in, k, c_out, (const float *)x, (const float *)locations,
+                                     Csr{rev_offsets, rev_entries}, (const float *)theta, (const float *)theta_b,
+                                     (float *)y, st);
         if (mode != FC_MODE_AUTO)
             return set_error(FC_ERR_UNSUPPORTED, "tensor-core engine %d does not cover this deconv shape", mode);
     }

@@ -55,6 +55,12 @@ struct TcArgs {
     const float *feat;    // [total, NOUT] conv input features
     const float *centre;  // [total, 3] centre-role term (tc_dtheta kernel)
     float *dloc;          // [total, 3]
+    // channel blocks (wide shapes, tc_blocked_*): row strides of the gathered rows, of the
+    // output and of feat (elements; the pointers address the block's first channel), and
+    // acc = 1 to add into out (and subtract from dloc) instead of overwriting
+    int64_t ld_rows, ld_out, ld_feat;
+    int acc;       // out += block result
+    int acc_dloc;  // dloc -= this block's neighbour term (else dloc = centre - term)
 };
 
 template <bool SPLIT>
@@ -103,13 +109,18 @@ struct TcLayout {
 //   reverse: n = c  (rows = c_in),  c' = gathered chan  (GC = c_out)
 template <bool SPLIT>
 __global__ void __launch_bounds__(1024)
-    tc_pack_b_kernel(int cin, int cout, const float *__restrict__ theta, const float *__restrict__ theta_b,
+    tc_pack_b_kernel(int cin, int cout, int ld_cin, const float *__restrict__ theta, const float *__restrict__ theta_b,
                      int reverse, int nout, int gc, uint8_t *__restrict__ img, float *__restrict__ binv) {
+    // (cin, cout): the block of theta packed; ld_cin: theta's full c_in (row stride); theta /
+    // theta_b point at the block's first (c', c)
     __shared__ float red[32];
     float m = 0.f;
-    const int nth = cout * cin * 3, ntb = cout * cin;
-    for (int i = threadIdx.x; i < nth; i += blockDim.x) m = fmaxf(m, fabsf(theta[i]));
-    for (int i = threadIdx.x; i < ntb; i += blockDim.x) m = fmaxf(m, fabsf(theta_b[i]));
+    const int ntb = cout * cin;
+    for (int i = threadIdx.x; i < ntb; i += blockDim.x) {
+        const int64_t e = (int64_t)(i / cin) * ld_cin + i % cin;
+        m = fmaxf(m, fmaxf(fabsf(theta_b[e]), fmaxf(fabsf(theta[e * 3]), fmaxf(fabsf(theta[e * 3 + 1]),
+                                                                                  fabsf(theta[e * 3 + 2])))));
+    }
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
     __syncthreads();
@@ -130,7 +141,7 @@ __global__ void __launch_bounds__(1024)
         const int t = k / gc, c = k % gc;
         const int cp = reverse ? c : nn;
         const int ci = reverse ? nn : c;
-        const float v = (t < 3) ? theta[((int64_t)cp * cin + ci) * 3 + t] : theta_b[(int64_t)cp * cin + ci];
+        const float v = (t < 3) ? theta[((int64_t)cp * ld_cin + ci) * 3 + t] : theta_b[(int64_t)cp * ld_cin + ci];
         uint16_t lo;
         const uint16_t hi = pack1<SPLIT>(v * s, lo);
         const uint32_t off = sw128_offset(nn, k, nout);
@@ -264,6 +275,7 @@ struct GatherSrc {
     const float *rows, *loc;
     const int32_t *nbr;
     int64_t total, n;
+    int64_t ld;  // row stride of `rows` (elements)
 };
 struct ItemMap {
     int ipt;         // items per tile for this warp
@@ -340,11 +352,11 @@ struct FwdPipe8 {
 #pragma unroll
         for (int q = 0; q < kSlots; ++q) {
             const int32_t jj = __shfl_sync(0xffffffffu, cur.j, pt * 8 + q);
-            v[q] = __ldg(reinterpret_cast<const float4 *>(s.rows + (int64_t)jj * GC) + cl);
+            v[q] = __ldg(reinterpret_cast<const float4 *>(s.rows + (int64_t)jj * s.ld) + cl);
         }
         issue_pos(r1);
         if (r1.v) {
-            const float *rp = s.rows + (int64_t)j1 * GC;
+            const float *rp = s.rows + (int64_t)j1 * s.ld;
             asm volatile("prefetch.global.L2 [%0];" ::"l"(rp));
             if (GC * 4 > 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + 32));
         }
@@ -376,6 +388,7 @@ struct FwdPipe8 {
 struct RevPipe16 {
     static constexpr int GC = 64;
     const float *rows, *loc;
+    int64_t ld;  // row stride of `rows` (elements)
     Csr csr;
     int64_t total;
     int k;
@@ -441,9 +454,10 @@ struct RevPipe16 {
         o1 = v ? nl1_1 - lp1_1 : 0.f;
         o2 = v ? nl2_1 - lp2_1 : 0.f;
     }
-    __device__ __forceinline__ void start(const float *rows_, const float *loc_, Csr csr_, int64_t total_, int k_,
-                                          ItemMap map, int64_t n_items, int lane) {
+    __device__ __forceinline__ void start(const float *rows_, int64_t ld_, const float *loc_, Csr csr_, int64_t total_,
+                                          int k_, ItemMap map, int64_t n_items, int lane) {
         rows = rows_;
+        ld = ld_;
         loc = loc_;
         csr = csr_;
         total = total_;
@@ -468,7 +482,7 @@ struct RevPipe16 {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const int32_t jj = __shfl_sync(0xffffffffu, j, pt * 16 + b0 + q);
-            v[q] = (b0 + q < mycnt) ? __ldg(reinterpret_cast<const float4 *>(rows + (int64_t)jj * GC) + cl)
+            v[q] = (b0 + q < mycnt) ? __ldg(reinterpret_cast<const float4 *>(rows + (int64_t)jj * ld) + cl)
                                     : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
@@ -490,7 +504,7 @@ struct RevPipe16 {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const int32_t jj = __shfl_sync(0xffffffffu, j, pt * 16 + q);
-            v[q] = (q < mycnt) ? __ldg(reinterpret_cast<const float4 *>(rows + (int64_t)jj * GC) + cl)
+            v[q] = (q < mycnt) ? __ldg(reinterpret_cast<const float4 *>(rows + (int64_t)jj * ld) + cl)
                                : make_float4(0.f, 0.f, 0.f, 0.f);
         }
         load_pos();                    // item w+1: source positions
@@ -525,7 +539,7 @@ struct RevPipe16 {
                     const float w1 = __shfl_sync(0xffffffffu, t1, pt * 16 + q);
                     const float w2 = __shfl_sync(0xffffffffu, t2, pt * 16 + q);
                     if (b0 + q < mycnt) {
-                        const float4 x = __ldg(reinterpret_cast<const float4 *>(rows + (int64_t)jj * GC) + cl);
+                        const float4 x = __ldg(reinterpret_cast<const float4 *>(rows + (int64_t)jj * ld) + cl);
                         mom_add(acc, x, w0, w1, w2);
                     }
                 }
@@ -549,7 +563,7 @@ __device__ __noinline__ void tc_gmc_epilogue(const TcArgs &a, int i, int warp, i
     const int64_t p = tile * kTcM + row;
     const bool pv = p < a.total;
     const float inv = rs[(i & 1) * kTcM + row];
-    float *orow = a.out + p * NOUT;
+    float *orow = a.out + p * a.ld_out;
     const uint32_t tbase = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)((i & 1) * CPB);
     float nb0 = 0.f, nb1 = 0.f, nb2 = 0.f;
 #pragma unroll 1
@@ -560,6 +574,10 @@ __device__ __noinline__ void tc_gmc_epilogue(const TcArgs &a, int i, int warp, i
 #pragma unroll
             for (int q = 0; q < 16; q += 4) {
                 float4 w = make_float4(v[q] * inv, v[q + 1] * inv, v[q + 2] * inv, v[q + 3] * inv);
+                if (a.acc) {
+                    const float4 o = *reinterpret_cast<const float4 *>(orow + c0 + q);
+                    w.x += o.x, w.y += o.y, w.z += o.z, w.w += o.w;
+                }
                 *reinterpret_cast<float4 *>(orow + c0 + q) = w;
             }
         }
@@ -569,7 +587,7 @@ __device__ __noinline__ void tc_gmc_epilogue(const TcArgs &a, int i, int warp, i
             if (pv) {
 #pragma unroll
                 for (int q = 0; q < 16; q += 4) {
-                    const float4 x = __ldg(reinterpret_cast<const float4 *>(a.feat + p * NOUT + c0 + q));
+                    const float4 x = __ldg(reinterpret_cast<const float4 *>(a.feat + p * a.ld_feat + c0 + q));
                     f[q] = x.x, f[q + 1] = x.y, f[q + 2] = x.z, f[q + 3] = x.w;
                 }
             } else {
@@ -590,9 +608,10 @@ __device__ __noinline__ void tc_gmc_epilogue(const TcArgs &a, int i, int warp, i
     }
     if constexpr (DLOC) {
         if (pv) {
-            a.dloc[p * 3 + 0] = a.centre[p * 3 + 0] - nb0 * inv;
-            a.dloc[p * 3 + 1] = a.centre[p * 3 + 1] - nb1 * inv;
-            a.dloc[p * 3 + 2] = a.centre[p * 3 + 2] - nb2 * inv;
+            const float *base = a.acc_dloc ? a.dloc : a.centre;  // blocks after the first subtract their part
+            a.dloc[p * 3 + 0] = base[p * 3 + 0] - nb0 * inv;
+            a.dloc[p * 3 + 1] = base[p * 3 + 1] - nb1 * inv;
+            a.dloc[p * 3 + 2] = base[p * 3 + 2] - nb2 * inv;
         }
     }
     tc_fence_before();
@@ -747,7 +766,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gmc_kernel(TcArgs a) {
             for (int s = 0; s < kSlots; ++s) {
                 const int32_t jj = __shfl_sync(0xffffffffu, x.j, pt * 8 + s);
                 v[s] = (KFIX || s < mycnt_b)
-                           ? __ldg(reinterpret_cast<const float4 *>(a.rows + (int64_t)jj * GC) + cl)
+                           ? __ldg(reinterpret_cast<const float4 *>(a.rows + (int64_t)jj * a.ld_rows) + cl)
                            : make_float4(0.f, 0.f, 0.f, 0.f);
             }
         };
@@ -801,7 +820,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gmc_kernel(TcArgs a) {
             //   rows of g loaded and accumulated during g.
             // (the loaded values are only consumed one iteration later)
             FwdPipe8<GC> pipe;
-            pipe.start(GatherSrc{a.rows, a.loc, a.nbr, a.total, a.n},
+            pipe.start(GatherSrc{a.rows, a.loc, a.nbr, a.total, a.n, a.ld_rows},
                        ItemMap{G::GPW, gw * G::PPI, kGatherWarps * G::PPI}, items, lane);
             for (int64_t w = 0; w < items; ++w) {
                 Mom acc;
@@ -811,7 +830,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gmc_kernel(TcArgs a) {
             }
         } else if (REVERSE && GC == 64) {
             RevPipe16 pipe;
-            pipe.start(a.rows, a.loc, a.csr, a.total, a.k, ItemMap{G::GPW, gw * G::PPI, kGatherWarps * G::PPI}, items,
+            pipe.start(a.rows, a.ld_rows, a.loc, a.csr, a.total, a.k, ItemMap{G::GPW, gw * G::PPI, kGatherWarps * G::PPI}, items,
                        lane);
             for (int64_t w = 0; w < items; ++w) {
                 Mom acc;
@@ -874,6 +893,8 @@ struct DtArgs {
     float *partial;       // [gridDim.x][2 (hi / lo lanes)][CO * 4 * GC], layout (c', c, t) like dtheta_partial_kernel
     float *centre;        // [total, 3]
     int64_t num_tiles;
+    int64_t ld_feat, ld_g;  // row strides of feat / g (channel blocks of wide shapes)
+    int acc;                // add into centre instead of overwriting (blocks after the first)
 };
 
 struct DtLayout {
@@ -1054,7 +1075,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
             if (p < a.total) {
 #pragma unroll
                 for (int q = 0; q < 16; q += 4) {
-                    const float4 x = __ldg(reinterpret_cast<const float4 *>(a.g + p * CO + q0 + q));
+                    const float4 x = __ldg(reinterpret_cast<const float4 *>(a.g + p * a.ld_g + q0 + q));
                     gv[q] = x.x, gv[q + 1] = x.y, gv[q + 2] = x.z, gv[q + 3] = x.w;
                 }
             } else {
@@ -1072,10 +1093,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
 #pragma unroll
             for (int q = 0; q < 16; ++q) c2 = fmaf(gv[q], z[q], c2);
         }
-        if (p < a.total) {
-            a.centre[p * 3 + 0] = c0 * inv;
-            a.centre[p * 3 + 1] = c1 * inv;
-            a.centre[p * 3 + 2] = c2 * inv;
+        if (p < a.total && a.centre) {
+            const float b0 = a.acc ? a.centre[p * 3 + 0] : 0.f;
+            const float b1 = a.acc ? a.centre[p * 3 + 1] : 0.f;
+            const float b2 = a.acc ? a.centre[p * 3 + 2] : 0.f;
+            a.centre[p * 3 + 0] = b0 + c0 * inv;
+            a.centre[p * 3 + 1] = b1 + c1 * inv;
+            a.centre[p * 3 + 2] = b2 + c2 * inv;
         }
         tc_fence_before();
         __syncwarp();
@@ -1092,7 +1116,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
         // items of this warp: (tile, chunk c = q + 2m), group r of the chunk
         const ItemMap im{4, q * kDtChunk + 2 * r, 2 * kDtChunk};
         FwdPipe8<GC> pipe;
-        if (KFIX == kSlots) pipe.start(GatherSrc{a.feat, a.loc, a.nbr, a.total, a.n}, im, tiles_mine * 4, lane);
+        if (KFIX == kSlots) pipe.start(GatherSrc{a.feat, a.loc, a.nbr, a.total, a.n, a.ld_feat}, im, tiles_mine * 4, lane);
         for (int64_t tl = 0; tl < tiles_mine; ++tl) {
             const int i = (int)tl;
             const int64_t tile = blockIdx.x + tl * gridDim.x;
@@ -1122,7 +1146,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
 #pragma unroll
                         for (int s = 0; s < kSlots; ++s) {
                             const int32_t jj = __shfl_sync(0xffffffffu, j, pt * 8 + s);
-                            v[s] = (b0 + s < cnt) ? __ldg(reinterpret_cast<const float4 *>(a.feat + (int64_t)jj * GC) + cl)
+                            v[s] = (b0 + s < cnt) ? __ldg(reinterpret_cast<const float4 *>(a.feat + (int64_t)jj * a.ld_feat) + cl)
                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
                         }
 #pragma unroll
@@ -1138,7 +1162,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
                 const bool valid = pme < a.total;
                 if (!valid) mom_zero(acc);
                 float4 gv = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (valid) gv = __ldg(reinterpret_cast<const float4 *>(a.g + pme * CO) + cl);
+                if (valid) gv = __ldg(reinterpret_cast<const float4 *>(a.g + pme * a.ld_g) + cl);
                 // ---- wait for the ring stage (and, at a tile's first chunk, the Xb/rs buffer)
                 if (u >= 1) mbar_wait(chunk_empty + q, (uint32_t)((u - 1) & 1));
                 if (c == q && i >= 2) mbar_wait(z_free + (i & 1), ((i >> 1) + 1) & 1);
@@ -1224,14 +1248,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
 // host side
 template <int GC, int NOUT, bool SPLIT, bool REVERSE, int KFIX, bool DLOC = false>
 static int launch_tc(const TcArgs &a0, int cin, int cout, const float *theta, const float *theta_b,
-                     cudaStream_t st) {
+                     cudaStream_t st, int ld_cin = -1) {
     using L = TcLayout<GC, NOUT, SPLIT, DLOC>;
     TcArgs a = a0;
     uint8_t *img = (uint8_t *)scratch_alloc((size_t)L::B_BYTES * L::NSPLIT + 256, st);
     if (!img) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc)");
     float *binv = reinterpret_cast<float *>(img + (size_t)L::B_BYTES * L::NSPLIT);
-    tc_pack_b_kernel<SPLIT><<<(unsigned)ceil_div(NOUT * 4 * GC, 1024), 1024, 0, st>>>(cin, cout, theta, theta_b,
-                                                                                    REVERSE ? 1 : 0, NOUT, GC, img, binv);
+    tc_pack_b_kernel<SPLIT><<<(unsigned)ceil_div(NOUT * 4 * GC, 1024), 1024, 0, st>>>(
+        cin, cout, ld_cin > 0 ? ld_cin : cin, theta, theta_b, REVERSE ? 1 : 0, NOUT, GC, img, binv);
     count_launch();
     a.bimg = img;
     a.binv = binv;
@@ -1257,29 +1281,37 @@ static bool fast_enabled();
 
 template <int GC, int NOUT, bool SPLIT, bool REVERSE>
 static int launch_tc_k(const TcArgs &a, int cin, int cout, const float *theta, const float *theta_b,
-                       cudaStream_t st) {
+                       cudaStream_t st, int ld_cin) {
+    const bool plain = a.ld_rows == GC && a.ld_out == NOUT && !a.acc && !a.acc_dloc && ld_cin == cin;
     if constexpr (REVERSE && GC == 64 && NOUT == 64) {
-        if (fast_enabled())
+        if (fast_enabled() && plain && a.ld_feat == NOUT)
             return tc_fast_reverse(SPLIT, a.total, a.k, a.rows, a.loc, a.csr, theta, theta_b, a.out, a.feat, a.centre,
                                    a.dloc, st);
     }
-    if (!REVERSE && a.k == kSlots) return launch_tc<GC, NOUT, SPLIT, REVERSE, kSlots>(a, cin, cout, theta, theta_b, st);
+    if (!REVERSE && a.k == kSlots)
+        return launch_tc<GC, NOUT, SPLIT, REVERSE, kSlots>(a, cin, cout, theta, theta_b, st, ld_cin);
     if constexpr (REVERSE && NOUT <= 64) {
-        if (a.dloc) return launch_tc<GC, NOUT, SPLIT, true, 0, true>(a, cin, cout, theta, theta_b, st);
+        if (a.dloc) return launch_tc<GC, NOUT, SPLIT, true, 0, true>(a, cin, cout, theta, theta_b, st, ld_cin);
     }
     if (REVERSE && a.dloc) return set_error(FC_ERR_UNSUPPORTED, "tensor-core location gradient needs c_in <= 64");
-    return launch_tc<GC, NOUT, SPLIT, REVERSE, 0>(a, cin, cout, theta, theta_b, st);
+    return launch_tc<GC, NOUT, SPLIT, REVERSE, 0>(a, cin, cout, theta, theta_b, st, ld_cin);
 }
 
 template <bool SPLIT, bool REVERSE>
-static int dispatch_tc(int gc, int nout, const TcArgs &a, int cin, int cout, const float *theta,
-                       const float *theta_b, cudaStream_t st) {
-    if (gc == 64 && nout == 64) return launch_tc_k<64, 64, SPLIT, REVERSE>(a, cin, cout, theta, theta_b, st);
-    if (gc == 64 && nout == 32) return launch_tc_k<64, 32, SPLIT, REVERSE>(a, cin, cout, theta, theta_b, st);
-    if (gc == 32 && nout == 32) return launch_tc_k<32, 32, SPLIT, REVERSE>(a, cin, cout, theta, theta_b, st);
-    if (gc == 32 && nout == 64) return launch_tc_k<32, 64, SPLIT, REVERSE>(a, cin, cout, theta, theta_b, st);
-    if (gc == 32 && nout == 128) return launch_tc_k<32, 128, SPLIT, REVERSE>(a, cin, cout, theta, theta_b, st);
-    if (!SPLIT && gc == 64 && nout == 128) return launch_tc_k<64, 128, false, REVERSE>(a, cin, cout, theta, theta_b, st);
+static int dispatch_tc(int gc, int nout, const TcArgs &a0, int cin, int cout, const float *theta,
+                       const float *theta_b, cudaStream_t st, int ld_cin = -1) {
+    TcArgs a = a0;  // unset strides = dense rows of the block's own width
+    if (a.ld_rows == 0) a.ld_rows = gc;
+    if (a.ld_out == 0) a.ld_out = nout;
+    if (a.ld_feat == 0) a.ld_feat = nout;
+    if (ld_cin <= 0) ld_cin = cin;
+    if (gc == 64 && nout == 64) return launch_tc_k<64, 64, SPLIT, REVERSE>(a, cin, cout, theta, theta_b, st, ld_cin);
+    if (gc == 64 && nout == 32) return launch_tc_k<64, 32, SPLIT, REVERSE>(a, cin, cout, theta, theta_b, st, ld_cin);
+    if (gc == 32 && nout == 32) return launch_tc_k<32, 32, SPLIT, REVERSE>(a, cin, cout, theta, theta_b, st, ld_cin);
+    if (gc == 32 && nout == 64) return launch_tc_k<32, 64, SPLIT, REVERSE>(a, cin, cout, theta, theta_b, st, ld_cin);
+    if (gc == 32 && nout == 128) return launch_tc_k<32, 128, SPLIT, REVERSE>(a, cin, cout, theta, theta_b, st, ld_cin);
+    if (!SPLIT && gc == 64 && nout == 128)
+        return launch_tc_k<64, 128, false, REVERSE>(a, cin, cout, theta, theta_b, st, ld_cin);
     return set_error(FC_ERR_UNSUPPORTED, "no tensor-core instance for gathered=%d out=%d", gc, nout);
 }
 
@@ -1300,8 +1332,8 @@ int tc_conv_forward_supported(int mode, int c_in, int d, int k, int c_out) {
 void launch_pack_b(bool split, int cin, int cout, const float *theta, const float *theta_b, int reverse, int nout,
                    int gc, uint8_t *img, float *binv, cudaStream_t st) {
     const unsigned g = (unsigned)ceil_div((int64_t)nout * 4 * gc, 1024);
-    if (split) tc_pack_b_kernel<true><<<g, 1024, 0, st>>>(cin, cout, theta, theta_b, reverse, nout, gc, img, binv);
-    else tc_pack_b_kernel<false><<<g, 1024, 0, st>>>(cin, cout, theta, theta_b, reverse, nout, gc, img, binv);
+    if (split) tc_pack_b_kernel<true><<<g, 1024, 0, st>>>(cin, cout, cin, theta, theta_b, reverse, nout, gc, img, binv);
+    else tc_pack_b_kernel<false><<<g, 1024, 0, st>>>(cin, cout, cin, theta, theta_b, reverse, nout, gc, img, binv);
     count_launch();
 }
 
@@ -1357,6 +1389,78 @@ int tc_fast_dtheta(int64_t total, int64_t n, const float *feat, const float *loc
                    const float *theta, const float *theta_b, float *d_theta, float *d_theta_b, float *centre,
                    cudaStream_t st);
 
+// d_theta / d_theta_b of one 64 x 64 channel block (c' block of g, c block of feat) and its
+// centre-role location term, on tc_dtheta_kernel: feat / g / theta / theta_b / d_theta /
+// d_theta_b point at the block's first channel; ld_* are the full row strides.  d_theta block
+// rows are written with row stride ld_dt (full c_in); centre is written (acc_centre = false)
+// or added to.
+static int generic_dtheta_block(int64_t total, int64_t n, int k, const float *feat, int64_t ld_feat,
+                                const float *loc, const int32_t *nbr, const float *g, int64_t ld_g,
+                                const float *theta, const float *theta_b, int ld_cin, float *d_theta,
+                                float *d_theta_b, int ld_dt, float *centre, bool acc_centre, cudaStream_t st) {
+    using L = DtLayout;
+    constexpr int cin = 64, cout = 64;
+    const int64_t num_tiles = ceil_div(total, kTcM);
+    // at most 8 tiles (1024 points, 128 tf32 k-steps) accumulated in TMEM per CTA -- more
+    // CTAs (waves) instead of a longer, truncating accumulation
+    const int grid = (int)std::min<int64_t>(num_tiles, std::max<int64_t>(num_sms(), ceil_div(num_tiles, 8)));
+    const size_t img_bytes = (size_t)cout * 4 * cin * 2 * 2;
+    Scratch img_buf(img_bytes + 256, st);
+    Scratch partial_buf(sizeof(float) * 2 * grid * cout * cin * 4, st);
+    const bool dense = ld_dt == cin;
+    Scratch blk_buf(dense ? 16 : sizeof(float) * cout * cin * 4, st);
+    if (!img_buf.ok() || !partial_buf.ok() || !blk_buf.ok())
+        return set_error(FC_ERR_CUDA, "scratch allocation failed (tc d_theta)");
+    uint8_t *img = img_buf.as<uint8_t>();
+    float *binv = reinterpret_cast<float *>(img + img_bytes);
+    tc_pack_b_kernel<true><<<(unsigned)ceil_div((int64_t)cout * 4 * cin, 1024), 1024, 0, st>>>(
+        cin, cout, ld_cin, theta, theta_b, 0, cout, cin, img, binv);
+    count_launch();
+    DtArgs a{};
+    a.total = total;
+    a.n = n;
+    a.k = k;
+    a.feat = feat;
+    a.loc = loc;
+    a.g = g;
+    a.nbr = nbr;
+    a.bimg = img;
+    a.binv = binv;
+    a.partial = partial_buf.as<float>();
+    a.centre = centre;
+    a.num_tiles = num_tiles;
+    a.ld_feat = ld_feat;
+    a.ld_g = ld_g;
+    a.acc = acc_centre ? 1 : 0;
+    static uint64_t attr8 = 0, attr0 = 0;
+    prof_begin("tc_dtheta", st);
+    if (k == kSlots) {
+        if (first_use_on_device(attr8))
+            cudaFuncSetAttribute(tc_dtheta_kernel<kSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+        tc_dtheta_kernel<kSlots><<<grid, kTcThreads, L::SMEM, st>>>(a);
+    } else {
+        if (first_use_on_device(attr0))
+            cudaFuncSetAttribute(tc_dtheta_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+        tc_dtheta_kernel<0><<<grid, kTcThreads, L::SMEM, st>>>(a);
+    }
+    prof_end(st);
+    count_launch();
+    int rc = check_launch("tc_dtheta_kernel");
+    if (rc || !(d_theta || d_theta_b)) return rc;
+    if (dense) return launch_dtheta_reduce<float>(2 * grid, cin, 3, cout, a.partial, d_theta, d_theta_b, st);
+    // a block of a wider theta: reduce densely, then place the rows (row stride ld_dt)
+    float *bt = blk_buf.as<float>(), *btb = bt + cout * cin * 3;
+    rc = launch_dtheta_reduce<float>(2 * grid, cin, 3, cout, a.partial, bt, btb, st);
+    if (rc) return rc;
+    if (d_theta)
+        cudaMemcpy2DAsync(d_theta, sizeof(float) * 3 * ld_dt, bt, sizeof(float) * 3 * cin, sizeof(float) * 3 * cin, cout,
+                          cudaMemcpyDeviceToDevice, st);
+    if (d_theta_b)
+        cudaMemcpy2DAsync(d_theta_b, sizeof(float) * ld_dt, btb, sizeof(float) * cin, sizeof(float) * cin, cout,
+                          cudaMemcpyDeviceToDevice, st);
+    return check_launch("d_theta block copy");
+}
+
 int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int cout, const float *g,
                 const float *feat, const float *loc, const int32_t *nbr, Csr csr, const float *theta,
                 const float *theta_b, float *d_features, float *d_locations, float *d_theta, float *d_theta_b,
@@ -1379,49 +1483,11 @@ int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int c
         rc = tc_fast_dtheta(total, n, feat, loc, nbr, g, theta, theta_b, d_theta, d_theta_b, centre, st);
         if (rc) return rc;
     } else if (d_theta || d_theta_b || d_locations) {
-        const size_t img_bytes = (size_t)cout * 4 * cin * 2 * 2;
-        Scratch img_buf(img_bytes + 256, st);
-        Scratch partial_buf(sizeof(float) * 2 * grid * cout * cin * 4, st);
         centre_buf.alloc(sizeof(float) * total * 3, st);
-        if (!img_buf.ok() || !partial_buf.ok() || !centre_buf.ok())
-            return set_error(FC_ERR_CUDA, "scratch allocation failed (tc backward)");
-        uint8_t *img = img_buf.as<uint8_t>();
-        float *partial = partial_buf.as<float>();
+        if (!centre_buf.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc backward)");
         centre = centre_buf.as<float>();
-        float *binv = reinterpret_cast<float *>(img + img_bytes);
-        tc_pack_b_kernel<true><<<(unsigned)ceil_div((int64_t)cout * 4 * cin, 1024), 1024, 0, st>>>(cin, cout, theta, theta_b, 0, cout, cin, img, binv);
-        count_launch();
-        DtArgs a{};
-        a.total = total;
-        a.n = n;
-        a.k = k;
-        a.feat = feat;
-        a.loc = loc;
-        a.g = g;
-        a.nbr = nbr;
-        a.bimg = img;
-        a.binv = binv;
-        a.partial = partial;
-        a.centre = centre;
-        a.num_tiles = num_tiles;
-        static uint64_t attr8 = 0, attr0 = 0;
-        prof_begin("tc_dtheta", st);
-        if (k == kSlots) {
-            if (first_use_on_device(attr8)) {
-                cudaFuncSetAttribute(tc_dtheta_kernel<kSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
-            }
-            tc_dtheta_kernel<kSlots><<<grid, kTcThreads, L::SMEM, st>>>(a);
-        } else {
-            if (first_use_on_device(attr0)) {
-                cudaFuncSetAttribute(tc_dtheta_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
-            }
-            tc_dtheta_kernel<0><<<grid, kTcThreads, L::SMEM, st>>>(a);
-        }
-        prof_end(st);
-        count_launch();
-        rc = check_launch("tc_dtheta_kernel");
-        if (!rc && (d_theta || d_theta_b))
-            rc = launch_dtheta_reduce<float>(2 * grid, cin, 3, cout, partial, d_theta, d_theta_b, st);
+        rc = generic_dtheta_block(total, n, k, feat, cin, loc, nbr, g, cout, theta, theta_b, cin, d_theta, d_theta_b,
+                                  cin, centre, false, st);
         if (rc) return rc;
     }
     if (d_features || d_locations) {
@@ -1464,6 +1530,123 @@ int tc_reverse_gmc(int mode, int64_t total, int64_t n, int gc, int d, int k, int
     // conv shapes: c_in = cout (output of this pass), c_out = gc (gathered rows)
     if (mode == FC_MODE_TC_BF16) return dispatch_tc<false, true>(gc, cout, a, cout, gc, theta, theta_b, st);
     return dispatch_tc<true, true>(gc, cout, a, cout, gc, theta, theta_b, st);
+}
+
+
+// ---------------------------------------------------------------------------------
+// Wide shapes on the tensor cores (C2's 64 -> 128, the U-Net's 128 / 256 channels): the
+// channels are cut into 64-wide blocks and every (gathered block, output block) pair runs
+// the 64 x 64 engines above (the A tile of one block fits shared memory, the whole
+// operand does not); the K-blocks of one output block accumulate in its epilogue (out +=,
+// in ascending block order: deterministic), d_theta is assembled block by block, and the
+// location gradient's two roles accumulate over all block pairs.  The gathers are repeated
+// once per output block -- the price of keeping the moments on chip instead of writing
+// [points, 4 C] moment rows to HBM for a library GEMM.
+int tc_blocked_supported(int mode, int c_in, int d, int c_out) {
+    return (d == 3 && mode != FC_MODE_SIMT && c_in % 64 == 0 && c_out % 64 == 0 && (c_in > 64 || c_out > 64)) ? 1 : 0;
+}
+
+int tc_blocked_forward(int mode, int64_t total, int64_t n, int c_in, int k, int c_out, const float *feat,
+                       const float *loc, const int32_t *nbr, const float *theta, const float *theta_b, float *out,
+                       cudaStream_t st) {
+    for (int o0 = 0; o0 < c_out; o0 += 64) {
+        for (int i0 = 0; i0 < c_in; i0 += 64) {
+            TcArgs a{};
+            a.total = total;
+            a.n = n;
+            a.k = k;
+            a.rows = feat + i0;
+            a.ld_rows = c_in;
+            a.loc = loc;
+            a.nbr = nbr;
+            a.out = out + o0;
+            a.ld_out = c_out;
+            a.acc = i0 > 0;
+            const float *th = theta + ((int64_t)o0 * c_in + i0) * 3, *tb = theta_b + (int64_t)o0 * c_in + i0;
+            const int rc = mode == FC_MODE_TC_BF16 ? dispatch_tc<false, false>(64, 64, a, 64, 64, th, tb, st, c_in)
+                                                   : dispatch_tc<true, false>(64, 64, a, 64, 64, th, tb, st, c_in);
+            if (rc) return rc;
+        }
+    }
+    return FC_OK;
+}
+
+// Reverse pass over blocks: out [total, c_in] = sum over gathered c' blocks of the block
+// products (d_features of the backward, or flex_deconv); with dloc, the neighbour role of
+// the location gradient (dloc = centre - sum of the blocks' terms).
+static int tc_blocked_reverse(int mode, int64_t total, int64_t n, int c_in, int k, int c_out, const float *rows,
+                              const float *loc, Csr csr, const float *theta, const float *theta_b, float *out,
+                              const float *feat, const float *centre, float *dloc, cudaStream_t st) {
+    for (int i0 = 0; i0 < c_in; i0 += 64) {
+        for (int j0 = 0; j0 < c_out; j0 += 64) {
+            TcArgs a{};
+            a.total = total;
+            a.n = n;
+            a.k = k;
+            a.rows = rows + j0;
+            a.ld_rows = c_out;
+            a.loc = loc;
+            a.csr = csr;
+            a.out = out + i0;
+            a.ld_out = c_in;
+            a.acc = j0 > 0;
+            if (dloc) {
+                a.feat = feat + i0;
+                a.ld_feat = c_in;
+                a.centre = centre;
+                a.dloc = dloc;
+                a.acc_dloc = (i0 > 0 || j0 > 0);
+            }
+            const float *th = theta + ((int64_t)j0 * c_in + i0) * 3, *tb = theta_b + (int64_t)j0 * c_in + i0;
+            const int rc = mode == FC_MODE_TC_BF16 ? dispatch_tc<false, true>(64, 64, a, 64, 64, th, tb, st, c_in)
+                                                   : dispatch_tc<true, true>(64, 64, a, 64, 64, th, tb, st, c_in);
+            if (rc) return rc;
+        }
+    }
+    return FC_OK;
+}
+
+int tc_blocked_deconv(int mode, int64_t total, int64_t n, int c_in, int k, int c_out, const float *x,
+                      const float *loc, Csr csr, const float *theta, const float *theta_b, float *y, cudaStream_t st) {
+    return tc_blocked_reverse(mode, total, n, c_in, k, c_out, x, loc, csr, theta, theta_b, y, nullptr, nullptr,
+                              nullptr, st);
+}
+
+int tc_blocked_backward(int mode, int64_t total, int64_t n, int c_in, int k, int c_out, const float *g,
+                        const float *feat, const float *loc, const int32_t *nbr, Csr csr, const float *theta,
+                        const float *theta_b, float *d_features, float *d_locations, float *d_theta,
+                        float *d_theta_b, cudaStream_t st) {
+    Scratch centre_buf;
+    if (d_theta || d_theta_b || d_locations) {
+        if (d_locations) {
+            centre_buf.alloc(sizeof(float) * total * 3, st);
+            if (!centre_buf.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (blocked backward)");
+        }
+        for (int j0 = 0; j0 < c_out; j0 += 64) {
+            for (int i0 = 0; i0 < c_in; i0 += 64) {
+                // the centre term needs every block pair; d_theta blocks are independent
+                const int64_t e0 = (int64_t)j0 * c_in + i0;
+                const int rc = generic_dtheta_block(total, n, k, feat + i0, c_in, loc, nbr, g + j0, c_out, theta + e0 * 3,
+                                                    theta_b + e0, c_in, d_theta ? d_theta + e0 * 3 : nullptr,
+                                                    d_theta_b ? d_theta_b + e0 : nullptr, c_in,
+                                                    d_locations ? centre_buf.as<float>() : nullptr,
+                                                    j0 > 0 || i0 > 0, st);
+                if (rc) return rc;
+            }
+        }
+    }
+    if (d_features || d_locations) {
+        Scratch df_buf;
+        float *df = d_features;
+        if (!df) {
+            df_buf.alloc(sizeof(float) * total * c_in, st);
+            if (!df_buf.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (blocked backward)");
+            df = df_buf.as<float>();
+        }
+        return tc_blocked_reverse(mode, total, n, c_in, k, c_out, g, loc, csr, theta, theta_b, df, feat,
+                                  centre_buf.as<float>(), d_locations, st);
+    }
+    return FC_OK;
 }
 
 }  // namespace fc

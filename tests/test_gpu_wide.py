@@ -120,3 +120,30 @@ def test_wide_batched_and_deterministic(fc, oracle_mod):
         nbr = nbh.bkn[bi].t().cpu().numpy().astype(np.int64)
         ref = oracle_mod.conv_forward(feat[bi], loc[bi], nbr, th, tb)
         np.testing.assert_allclose(_np(outs[0][0][bi].t()), ref, rtol=1e-4, atol=1e-5)
+
+
+@pytest.mark.parametrize("shape", [(1024, 16, 64, 128, 3), (700, 8, 128, 128, 3), (300, 8, 256, 256, 3)])
+def test_wide_fp32_default_route_is_hand_written_tcgen05(fc, shape):
+    """C2's 64 -> 128 (K = 16) and the U-Net's 128 / 256-channel layers: the default fp32
+    route (forward, backward with d_locations, flex_deconv) launches only this library's
+    kernels -- the channel-blocked tcgen05 engines -- and no library GEMM (cuBLAS / CUTLASS)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    loc, feat, th, tb, up, nbr = _case(shape)
+    f32 = torch.float32
+    nb = fc.NeighborIndex(_t(nbr, torch.int64))
+    params = fc.FlexConvParams(_t(th, f32), _t(tb, f32))
+    args = (_t(feat, f32), _t(loc, f32))
+    fc.flex_conv_forward(*args, nb, params)  # warm-up (module load, CSR)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fc.flex_conv_forward(*args, nb, params)
+        fc.flex_conv_backward(_t(up, f32), *args, nb, params, with_locations=True)
+        fc.flex_deconv_forward(_t(up, f32), args[1], nb, params)
+        torch.cuda.synchronize()
+    names = [e.key for e in prof.key_averages() if e.device_type == torch.autograd.DeviceType.CUDA]
+    gemms = [k for k in names if any(s in k.lower() for s in ("gemm", "cublas", "cutlass", "sm90_", "sm100_xmma"))]
+    assert not gemms, gemms
+    assert any("tc_gmc_kernel" in k for k in names), names
+    assert any("tc_dtheta_kernel" in k for k in names), names
