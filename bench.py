@@ -145,6 +145,29 @@ def tensor_pipe(kern, c_in, c_out, d, n, bf16_peak):
     return out
 
 
+def knn_roofline(knn_ms, n, k, d, hbm):
+    """The exact grid kNN (setup, timed with CUDA events around the whole builder: bbox, grid,
+    bucket sort, query) against SURVEY.md §8(d)'s compulsory bytes (positions in, K int32
+    indices out: 4*Dp + 4*K per point), beside what ncu says bounds its query kernel
+    (profiles/ncu_datapipe.json: issue / fp64-pipe utilisation -- the query loop evaluates
+    fp64 candidate distances, so it is latency/compute-bound, not HBM-bound)."""
+    b = 4 * d + 4 * k
+    gbs = b * n / (knn_ms / 1e3) / 1e9
+    out = {"bound": "hbm", "ms": round(knn_ms, 3), "bytes_per_point": b, "achieved": round(gbs, 1),
+           "unit": "GB/s", "peak": hbm, "frac": round(gbs / hbm, 4),
+           "points_per_s": round(n / (knn_ms / 1e3), 1)}
+    p = os.path.join(ROOT, "profiles", "ncu_datapipe.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            kq = json.load(fh).get("kernels", {}).get("knn_grid")
+        if kq:
+            out["query_kernel_limiter"] = {x: kq.get(x) for x in ("ncu_ms_cold", "issue_active_frac", "fp64_pipe_frac",
+                                                                    "l1_data_pipe_frac", "warps_active_per_smsp",
+                                                                    "dram_bytes_per_point")}
+            out["query_kernel_limiter"]["source"] = "profiles/ncu_datapipe.json"
+    return out
+
+
 def run_fp64(args, torch, _ops, feat, pos, nbr, csr, g, theta, theta_b, n, steps=2):
     f64 = [t.double() for t in (feat, pos, g, theta, theta_b)]
     torch.cuda.synchronize()
@@ -461,6 +484,7 @@ def main():
                                         "GBps": round(bwd_b * n / bwd_ms / 1e6, 1)}}}
 
     roofline["tensor"] = tensor_pipe(kern, c, c, d, n, bf16)
+    roofline["knn"] = knn_roofline(knn_ms, n, k, d, hbm)
 
     cpu = None
     if rank == 0 and not args.no_cpu:

@@ -70,6 +70,10 @@ def main():
             "tensor_pipe_frac": (round(val(r, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active") / 100, 4)
                                  if val(r, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active") is not None
                                  else None),
+            "fp64_pipe_frac": (round(val(r, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active") / 100, 4)
+                               if val(r, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active") is not None
+                               else None),
+            "warps_active_per_smsp": val(r, "smsp__warps_active.avg.per_cycle_active"),
             "bank_conflict_wavefronts_per_point": (round(val(r, "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum") / args.n, 2)
                                                    if val(r, "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum") else None),
         }

@@ -24,6 +24,8 @@ def bench_name(kernel: str):
         return "tc_forward"
     if "tc_dt64_kernel" in kernel:
         return "tc_dtheta"
+    if "knn_grid_query_kernel" in kernel:
+        return "knn_grid"
     m = re.search(r"tc_rev64w?_kernel<(?:\(bool\))?(\w+), (?:\(bool\))?(\w+)>", kernel)
     if m:
         return "tc_reverse_dloc" if m.group(2) in ("1", "true") else "tc_reverse"
