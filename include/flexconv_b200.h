@@ -217,6 +217,31 @@ int fc_count_nonfinite(int dtype, const void *x, int64_t count, int32_t *bad, vo
 int fc_check_indices(const int32_t *idx, int64_t count, int64_t hi, int32_t *bad,
                      void *stream);
 
+/* ---- pointwise (1x1) convolutions of the U-Net step: replace the
+ * reference's pointwise_conv (flexops.py:206-226) and the concatenations that feed it
+ * (network.py:94-122, 180-246).  fp32, tcgen05 kind::tf32 with hi/lo split operands.
+ *
+ * fc_gemm_pack_b: pack B [nrows x K] (K = the concatenation of nseg column segments
+ *   (seg_src[s] .. + seg_k[s]) of w, each padded to 32 columns; transpose = 1 reads w^T)
+ *   into the tensor-core image `img` of fc_gemm_image_bytes(nrows, kblocks) bytes,
+ *   kblocks = sum ceil(seg_k / 32).
+ * fc_gemm_rows: Y = bias + [A_0 | ... | A_{nops-1}] . B^T for n rows; A_q row-major
+ *   [n x ka[q]] (row stride lda[q]); operand 0 optionally masked by (mask > 0) (the
+ *   ReLU of a saved pre-activation); column range [c0[o], c1[o]) of Y written to out[o]
+ *   (row stride ld[o]); relu_out (nullable) receives max(Y, 0).
+ * fc_gemm_wgrad: dw [co x sum kx] = G^T [X_0 | ...], db [co] = column sums of G (G
+ *   optionally masked); deterministic (fixed-order partial sums).  dw / db nullable. */
+int64_t fc_gemm_image_bytes(int ncols, int kblocks);
+int fc_gemm_pack_b(int transpose, int nrows, int nseg, const int *seg_src, const int *seg_k,
+                   const float *w, int64_t ldw, uint8_t *img, void *stream);
+int fc_gemm_rows(int64_t n, int nops, const float *const *a, const int64_t *lda, const int *ka,
+                 const float *mask, int64_t mask_ld, const uint8_t *img, int ncols,
+                 const float *bias, int nouts, float *const *out, const int64_t *ld,
+                 const int *c0, const int *c1, float *relu_out, int64_t relu_ld, void *stream);
+int fc_gemm_wgrad(int64_t n, const float *g, int64_t ldg, const float *mask, int64_t mask_ld,
+                  int co, int nops, const float *const *x, const int64_t *ldx, const int *kx,
+                  float *dw, float *db, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

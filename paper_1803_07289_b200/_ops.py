@@ -305,3 +305,82 @@ def count_nonfinite(x, bad=None):
         bad = torch.zeros(1, dtype=torch.int32, device=x.device)
     _call(x.device, "fc_count_nonfinite", _dtype(x), _p(x), x.numel(), _p(bad), _stream(x))
     return bad
+
+
+# ------------------------------------------------------------------ pointwise (1x1) GEMMs
+def _carr(ctype, vals):
+    return (ctype * len(vals))(*vals)
+
+
+def gemm_pack(w: torch.Tensor, segments, transpose: bool = False) -> torch.Tensor:
+    """Tensor-core image of B for gemm_rows: B = w (rows = w.shape[0]) or w^T (transpose;
+    rows = w.shape[1]); its K axis is the concatenation of `segments` = [(first column (row
+    if transpose) of w, width)], each padded to 32 (fc_gemm_pack_b)."""
+    w = _need(w, "w", torch.float32)
+    if w.dim() != 2 or not segments:
+        raise ShapeMismatchError("gemm_pack: w must be 2-D with at least one K segment")
+    nrows = w.shape[1] if transpose else w.shape[0]
+    kmax = w.shape[0] if transpose else w.shape[1]
+    for a, k in segments:
+        if a < 0 or k < 1 or a + k > kmax:
+            raise ShapeMismatchError(f"gemm_pack: segment ({a}, {k}) outside w of shape {tuple(w.shape)}")
+    kb = sum((k + 31) // 32 for _, k in segments)
+    img = torch.empty(int(_lib.lib().fc_gemm_image_bytes(nrows, kb)), dtype=torch.uint8, device=w.device)
+    _call(w.device, "fc_gemm_pack_b", int(transpose), nrows, len(segments),
+          _carr(ctypes.c_int, [int(a) for a, _ in segments]), _carr(ctypes.c_int, [int(k) for _, k in segments]),
+          _p(w), w.stride(0), _p(img), _stream(w))
+    return img
+
+
+def _rows2d(t: torch.Tensor, name: str, n: int) -> torch.Tensor:
+    t = _need(t, name, torch.float32)
+    if t.dim() != 2 or t.shape[0] != n:
+        raise ShapeMismatchError(f"{name} must be [{n}, k], got {tuple(t.shape)}")
+    return t
+
+
+def gemm_rows(operands, img: torch.Tensor, ncols: int, bias=None, outs=None, relu=False, mask=None):
+    """Y = bias + [operands[0] | operands[1] | ...] . B^T (B packed by gemm_pack with the
+    operands' widths as its K segments).  Returns [Y[:, c0:c1] for (c0, c1) in outs]
+    (default: the whole Y) and, with relu=True, also max(Y, 0) as the last element.
+    mask: operand 0 is multiplied by (mask > 0) on the fly (same shape as operand 0)."""
+    n = operands[0].shape[0]
+    ops = [_rows2d(x, f"operand {q}", n) for q, x in enumerate(operands)]
+    dev = ops[0].device
+    outs = [(0, ncols)] if outs is None else list(outs)
+    res = [torch.empty((n, c1 - c0), dtype=torch.float32, device=dev) for c0, c1 in outs]
+    rl = torch.empty((n, ncols), dtype=torch.float32, device=dev) if relu else None
+    if mask is not None:
+        mask = _rows2d(mask, "mask", n)
+        _shape(mask, tuple(ops[0].shape), "mask")
+    if bias is not None:
+        bias = _need(bias, "bias", torch.float32)
+        _shape(bias, (ncols,), "bias")
+    _call(dev, "fc_gemm_rows", n, len(ops), _carr(ctypes.c_void_p, [x.data_ptr() for x in ops]),
+          _carr(ctypes.c_int64, [x.stride(0) for x in ops]), _carr(ctypes.c_int, [x.shape[1] for x in ops]),
+          _p(mask), mask.stride(0) if mask is not None else 0, _p(img), ncols, _p(bias), len(res),
+          _carr(ctypes.c_void_p, [r.data_ptr() for r in res]), _carr(ctypes.c_int64, [r.stride(0) for r in res]),
+          _carr(ctypes.c_int, [c0 for c0, _ in outs]), _carr(ctypes.c_int, [c1 for _, c1 in outs]),
+          _p(rl), rl.stride(0) if rl is not None else 0, _stream(ops[0]))
+    return res + ([rl] if relu else [])
+
+
+def gemm_wgrad(g: torch.Tensor, operands, dw=None, db=None, mask=None) -> None:
+    """dw [co, sum k_q] = G^T [operands...], db [co] = sum over rows of G (G masked by
+    (mask > 0) when given); written in place (contiguous), fixed-order reductions."""
+    g = _need(g, "g", torch.float32)
+    n, co = g.shape
+    ops = [_rows2d(x, f"operand {q}", n) for q, x in enumerate(operands)]
+    ci = sum(x.shape[1] for x in ops)
+    if dw is not None:
+        _shape(dw, (co, ci), "dw")
+        if not dw.is_contiguous():
+            raise ShapeMismatchError("dw must be contiguous")
+    if db is not None:
+        _shape(db, (co,), "db")
+    if mask is not None:
+        mask = _rows2d(mask, "mask", n)
+        _shape(mask, (n, co), "mask")
+    _call(g.device, "fc_gemm_wgrad", n, _p(g), g.stride(0), _p(mask), mask.stride(0) if mask is not None else 0, co,
+          len(ops), _carr(ctypes.c_void_p, [x.data_ptr() for x in ops]), _carr(ctypes.c_int64, [x.stride(0) for x in ops]),
+          _carr(ctypes.c_int, [x.shape[1] for x in ops]), _p(dw), _p(db), _stream(g))

@@ -1,0 +1,532 @@
+// gemm_tc.cu -- the pointwise (1x1) convolutions of the U-Net / classifier step (SURVEY.md
+// §8(f)-1; reference flexops.py:206-226 pointwise_conv, network.py:94-122 _Pointwise and the
+// concatenations feeding them, network.py:180-246) as fp32-accurate tcgen05 GEMMs.
+//
+//   rows:  Y[p, :] = bias + [A_0 | A_1 | ...][p, :] . B^T      (forward: B = W; d_input:
+//          A_0 = G (optionally masked by a saved pre-activation, G * (Z > 0)), B = W^T)
+//   wgrad: dW = G^T [X_0 | X_1 | ...], db = sum_p G[p, :]        (SIMT, fixed-order partials)
+//
+// The concatenation [A_0 | A_1 | ...] (features | skip | coordinates) is never built: each
+// operand contributes its own 32-column K-blocks.  Precision: kind::tf32 with a hi/lo split of
+// both operands (A_hi = the fp32 value, which the tensor core truncates to tf32; A_lo = the
+// exact remainder), D = A_hi.[B_hi; B_lo] + A_lo.[B_hi; B_lo] as two MMAs of N = 2 nc per
+// 8-wide k-step, the halves of D summed in the epilogue: ~2^-21 relative per product, no
+// per-row scaling (tf32 keeps the fp32 exponent range) -- so any row / operand mix works.
+// Epilogue: + bias, the result to up to four column ranges (per-operand d_input outputs) and
+// optionally ReLU(result) to a second buffer (the ResBlock's r and relu(r) in one pass).
+#include <cstdio>
+
+#include "fast_common.cuh"
+
+namespace fc {
+using namespace sm100;
+
+namespace gemm {
+using fast::ldg_nc4;
+using fast::sts128f;
+using fast::lds128f;
+
+constexpr int kMaxOps = 4;
+constexpr int kMaxOuts = 4;
+constexpr int kThreads = 256;
+constexpr int kStages = 3;
+constexpr int kTileM = 128;
+constexpr int kA = kTileM * 128;  // one fp32 K-block image: 128 rows x 32 columns (16 KB)
+
+struct Op {
+    const float *a;
+    int64_t lda;
+    int k;    // columns of this operand
+    int kb0;  // first K-block (rows) / first concatenated column (wgrad)
+};
+struct Out {
+    float *p;
+    int64_t ld;
+    int c0, c1;  // output columns [c0, c1) -> p[:, 0 .. c1 - c0)
+};
+struct Args {
+    int64_t n;
+    int nops;
+    Op ops[kMaxOps];
+    int kblocks;
+    const float *mask;  // operand 0 *= (mask > 0) (nullable)
+    int64_t mask_ld;
+    const uint8_t *bimg;
+    int nc, nchunks, ncols;
+    const float *bias;
+    int nouts;
+    Out outs[kMaxOuts];
+    float *relu;
+    int64_t relu_ld;
+};
+
+__host__ __device__ inline int chunk_cols(int ncols) { return std::min(128, (int)((ncols + 15) / 16 * 16)); }
+__host__ __device__ inline int64_t image_bytes(int ncols, int kblocks) {
+    const int nc = chunk_cols(ncols);
+    return (int64_t)ceil_div(ncols, nc) * kblocks * 2 * nc * 128;
+}
+
+// kind::tf32, fp32 accumulate, both operands K-major
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(
+            d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+// byte offset of 16-byte chunk c (0..7) of row r in a 128-byte-row SW128 K-major image
+__device__ __forceinline__ uint32_t sw_chunk(int r, int c) {
+    return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
+}
+
+// B image: chunk ch (nc output columns) x K-block kb -> [2 nc rows: hi then lo] x 128 B.
+// Element (row n, column k) of B: transpose ? w[k * ldw + n] : w[n * ldw + k], where the
+// K axis is the concatenation of segments (src column / row offset, width), each padded to
+// whole 32-column K-blocks.
+struct PackArgs {
+    const float *w;
+    int64_t ldw;
+    int transpose;
+    int nrows, nc, kblocks;
+    int nseg;
+    int seg_src[kMaxOps], seg_k[kMaxOps], seg_kb0[kMaxOps];
+    uint8_t *img;
+};
+__global__ void pack_b_kernel(PackArgs a) {
+    const int64_t total = (int64_t)ceil_div(a.nrows, a.nc) * a.kblocks * a.nc * 32;  // (row, k) pairs
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int kk = (int)(idx & 31);
+        const int64_t r1 = idx >> 5;
+        const int rr = (int)(r1 % a.nc);
+        const int64_t r2 = r1 / a.nc;
+        const int kb = (int)(r2 % a.kblocks);
+        const int ch = (int)(r2 / a.kblocks);
+        const int n = ch * a.nc + rr;
+        float v = 0.f;
+        if (n < a.nrows) {
+            for (int s = 0; s < a.nseg; ++s) {
+                const int kl = (kb - a.seg_kb0[s]) * 32 + kk;
+                if (kb >= a.seg_kb0[s] && kl < a.seg_k[s]) {
+                    const int kc = a.seg_src[s] + kl;
+                    v = a.transpose ? a.w[(int64_t)kc * a.ldw + n] : a.w[(int64_t)n * a.ldw + kc];
+                }
+            }
+        }
+        const float hi = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+        uint8_t *blk = a.img + ((int64_t)ch * a.kblocks + kb) * (2 * a.nc * 128);
+        const uint32_t o = sw_chunk(rr, kk >> 2) + (uint32_t)(kk & 3) * 4u;
+        *reinterpret_cast<float *>(blk + o) = v;  // hi: the tensor core reads the tf32 part
+        *reinterpret_cast<float *>(blk + sw_chunk(a.nc + rr, kk >> 2) + (uint32_t)(kk & 3) * 4u) = v - hi;
+    }
+}
+
+__device__ __forceinline__ void cpa16(uint32_t dst, const void *src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa4(uint32_t dst, const void *src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// Pipeline: iteration j = (tile, chunk, K-block) of this CTA; the raw fp32 A block (= the hi
+// operand: the tensor core reads its tf32 part) and the packed B block are copied with
+// cp.async kStages - 1 iterations ahead (zero-filled past the rows / columns); a short pass
+// over the landed block writes the lo operand (and applies the ReLU mask); one thread issues
+// the MMAs.  K-block partials accumulate in two alternating TMEM accumulators and are summed
+// in fp32 registers (round-to-nearest): the tensor pipe's fp32 accumulation truncates, so a
+// long K in one accumulator drifts (~2^-24 per MMA, biased; measured 3.5x the SGEMM error on
+// the U-Net's 387-wide merge GEMM before this change).
+__global__ void __launch_bounds__(kThreads, 1) gemm_rows_kernel(Args a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sb = smem_u32(smem);
+    const int bstage = 2 * a.nc * 128;
+    const int stage = 2 * kA + bstage;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + kStages * stage);
+    uint64_t *mma_done = bar;         // [kStages]
+    uint64_t *dfull = bar + kStages;  // [2] K-block accumulator ready
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bar + kStages + 2);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(mma_done + s, 1);
+        mbar_init(dfull, 1);
+        mbar_init(dfull + 1, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc(tmem_holder, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_holder;
+    const int64_t tiles = ceil_div(a.n, kTileM);
+    const int64_t my_tiles = tiles > blockIdx.x ? ceil_div(tiles - blockIdx.x, gridDim.x) : 0;
+    const int per_tile = a.nchunks * a.kblocks;
+    const int64_t total = my_tiles * per_tile;
+    const uint32_t idesc = idesc_tf32(kTileM, 2 * a.nc);
+    const int r = tid >> 1, hf = tid & 1;  // A rows: row r, columns 16 hf .. +15 of the K-block
+
+    auto issue = [&](int64_t j) {  // cp.async of iteration j into stage j % kStages
+        if (j < total) {
+            const int64_t tile = blockIdx.x + (j / per_tile) * gridDim.x;
+            const int rem = (int)(j % per_tile), ch = rem / a.kblocks, kb = rem % a.kblocks;
+            const uint32_t As = sb + (uint32_t)((j % kStages) * stage), Bs = As + 2 * kA;
+            int q = 0;
+            while (q + 1 < a.nops && kb >= a.ops[q + 1].kb0) ++q;
+            const Op op = a.ops[q];
+            const int col0 = (kb - op.kb0) * 32 + 16 * hf;
+            const int64_t p = tile * kTileM + r;
+            const bool pv = p < a.n;
+            const float *src = op.a + (pv ? p : 0) * op.lda + col0;
+            if (((op.lda & 3) == 0) && ((reinterpret_cast<uintptr_t>(op.a) & 15) == 0) && (op.k & 3) == 0) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) cpa16(As + sw_chunk(r, 4 * hf + c), src + 4 * c, pv && col0 + 4 * c < op.k);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    cpa4(As + sw_chunk(r, 4 * hf + (e >> 2)) + (uint32_t)(e & 3) * 4u, src + e, pv && col0 + e < op.k);
+            }
+            const uint8_t *bsrc = a.bimg + ((int64_t)ch * a.kblocks + kb) * bstage;
+            for (int v = tid; v < bstage / 16; v += kThreads) cpa16(Bs + (uint32_t)(v * 16), bsrc + v * 16, true);
+        }
+        cpa_commit();
+    };
+
+    float acc[4][16];
+    const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    auto drain = [&](int64_t jt) {  // add accumulator (jt & 1) of iteration jt into acc
+        mbar_wait(dfull + (jt & 1), (uint32_t)((jt >> 1) & 1));
+        tc_fence_after();
+        const uint32_t db = tb + (uint32_t)((jt & 1) * 2 * a.nc);
+#pragma unroll
+        for (int jb = 0; jb < 4; ++jb) {
+            const int c0 = 16 * (warp >> 2) + 32 * jb;
+            if (c0 < a.nc) {
+                float d0[16], d1[16];
+                tmem_ld16(db + (uint32_t)c0, d0);
+                tmem_ld16(db + (uint32_t)(a.nc + c0), d1);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) acc[jb][c] += d0[c] + d1[c];
+            }
+        }
+        tc_fence_before();
+    };
+
+    for (int j = 0; j < kStages - 1; ++j) issue(j);
+    for (int64_t it = 0; it < total; ++it) {
+        const int s = (int)(it % kStages);
+        const int64_t tile = blockIdx.x + (it / per_tile) * gridDim.x;
+        const int rem = (int)(it % per_tile), ch = rem / a.kblocks, kb = rem % a.kblocks;
+        if (kb == 0) {
+#pragma unroll
+            for (int jb = 0; jb < 4; ++jb)
+#pragma unroll
+                for (int c = 0; c < 16; ++c) acc[jb][c] = 0.f;
+        }
+        cpa_wait<kStages - 2>();  // this thread's copies of iteration it have landed
+        __syncthreads();
+        // ---- lo operand (+ the ReLU mask on operand 0) for this thread's 16 columns
+        const uint32_t As = sb + (uint32_t)(s * stage), Al = As + kA, Bs = As + 2 * kA;
+        {
+            const int64_t p = tile * kTileM + r;
+            const bool masked = a.mask != nullptr && kb < a.ops[a.nops > 1 ? 1 : 0].kb0 + (a.nops > 1 ? 0 : a.kblocks) &&
+                                p < a.n;
+            const int col0 = kb * 32 + 16 * hf;  // operand 0 starts at K-block 0
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint32_t o = sw_chunk(r, 4 * hf + c);
+                float4 v = lds128f(As + o);
+                if (masked) {
+                    const float *mk = a.mask + p * a.mask_ld + col0 + 4 * c;
+                    const int k0 = a.ops[0].k;
+                    if (col0 + 4 * c + 0 < k0 && !(__ldg(mk + 0) > 0.f)) v.x = 0.f;
+                    if (col0 + 4 * c + 1 < k0 && !(__ldg(mk + 1) > 0.f)) v.y = 0.f;
+                    if (col0 + 4 * c + 2 < k0 && !(__ldg(mk + 2) > 0.f)) v.z = 0.f;
+                    if (col0 + 4 * c + 3 < k0 && !(__ldg(mk + 3) > 0.f)) v.w = 0.f;
+                    sts128f(As + o, v.x, v.y, v.z, v.w);
+                }
+                sts128f(Al + o, tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+            }
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            const uint32_t d = tmem + (uint32_t)((it & 1) * 2 * a.nc);
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                const uint32_t ko = (uint32_t)(ks * 32);
+                const uint64_t bd = desc_sw128(Bs + ko);
+                mma_tf32(d, desc_sw128(As + ko), bd, idesc, ks > 0 ? 1u : 0u);
+                mma_tf32(d, desc_sw128(Al + ko), bd, idesc, 1u);
+            }
+            mma_commit(mma_done + s);
+            mma_commit(dfull + (it & 1));
+        }
+        if (kb > 0) drain(it - 1);  // overlaps this K-block's MMAs
+        // refill the stage of iteration it - 1 (its MMAs are done) with iteration it + kStages - 1
+        if (it >= 1 && it + kStages - 1 < total)
+            mbar_wait(mma_done + ((it - 1) % kStages), (uint32_t)((((it - 1) / kStages)) & 1));
+        issue(it + kStages - 1);
+        if (kb == a.kblocks - 1) {
+            drain(it);
+            // ---- epilogue of (tile, chunk): warp w holds TMEM lane quadrant w % 4, 16-column
+            // blocks starting at 16 (w / 4), stride 32
+            const int row = (warp & 3) * 32 + lane;
+            const int64_t pe = tile * kTileM + row;
+            if (pe < a.n) {
+#pragma unroll
+                for (int jb = 0; jb < 4; ++jb) {
+                    const int c0 = 16 * (warp >> 2) + 32 * jb;
+                    if (c0 >= a.nc) continue;
+                    const int g0 = ch * a.nc + c0;
+                    float y[16];
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) y[c] = acc[jb][c] + ((a.bias && g0 + c < a.ncols) ? __ldg(a.bias + g0 + c) : 0.f);
+                    for (int o = 0; o < a.nouts; ++o) {
+                        const Out ou = a.outs[o];
+                        float *dst = ou.p + pe * ou.ld + (g0 - ou.c0);
+                        if (g0 >= ou.c0 && g0 + 16 <= ou.c1 && ((ou.ld & 3) == 0) && (((g0 - ou.c0) & 3) == 0) &&
+                            ((reinterpret_cast<uintptr_t>(ou.p) & 15) == 0)) {
+#pragma unroll
+                            for (int c = 0; c < 16; c += 4)
+                                *reinterpret_cast<float4 *>(dst + c) = make_float4(y[c], y[c + 1], y[c + 2], y[c + 3]);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < 16; ++c)
+                                if (g0 + c >= ou.c0 && g0 + c < ou.c1) dst[c] = y[c];
+                        }
+                    }
+                    if (a.relu) {
+                        float *dst = a.relu + pe * a.relu_ld + g0;
+                        if (g0 + 16 <= a.ncols && ((a.relu_ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.relu) & 15) == 0)) {
+#pragma unroll
+                            for (int c = 0; c < 16; c += 4)
+                                *reinterpret_cast<float4 *>(dst + c) = make_float4(fmaxf(y[c], 0.f), fmaxf(y[c + 1], 0.f),
+                                                                                   fmaxf(y[c + 2], 0.f), fmaxf(y[c + 3], 0.f));
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < 16; ++c)
+                                if (g0 + c < a.ncols) dst[c] = fmaxf(y[c], 0.f);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    cpa_wait<0>();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// ---------------------------------------------------------------- weight gradient (SIMT)
+struct WArgs {
+    int64_t n, chunk;
+    const float *g;
+    int64_t ldg;
+    const float *mask;
+    int64_t mask_ld;
+    int co;
+    int nops;
+    Op ops[kMaxOps];  // kb0 = first concatenated column of the operand
+    int ci;           // concatenated columns; column ci = the bias (ones)
+    float *part;      // [nchunk][co][ci + 1]
+};
+// CTA (64 threads): 64 (co) x 64 (ci) outputs over one point chunk; thread: 8 x 8 outputs
+// (4 shared loads per 64 FMAs); 32-point slabs of G and X staged in shared memory.  Partial
+// sums per chunk, reduced in fixed order (deterministic).
+__global__ void __launch_bounds__(64) wgrad_kernel(WArgs a) {
+    __shared__ __align__(16) float Gs[32][64];
+    __shared__ __align__(16) float Xs[32][64];
+    const int tid = threadIdx.x, ty = tid >> 3, tx = tid & 7;
+    const int co0 = blockIdx.x * 64, ci0 = blockIdx.y * 64;
+    const int64_t p0 = (int64_t)blockIdx.z * a.chunk, p1 = std::min<int64_t>(a.n, p0 + a.chunk);
+    const int gcol = co0 + tid, xcol = ci0 + tid;  // loader: column tid of both slabs
+    int xq = -1, xk = 0;
+    if (xcol < a.ci)
+        for (int q = 0; q < a.nops; ++q)
+            if (xcol >= a.ops[q].kb0 && xcol < a.ops[q].kb0 + a.ops[q].k) xq = q, xk = xcol - a.ops[q].kb0;
+    const float *xp = xq >= 0 ? a.ops[xq].a + xk : nullptr;
+    const int64_t xld = xq >= 0 ? a.ops[xq].lda : 0;
+    const bool gval = gcol < a.co;
+    float acc[8][8] = {};
+    for (int64_t pb = p0; pb < p1; pb += 32) {
+        float gv[32], xv[32];
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) {
+            const int64_t p = pb + rr;
+            const bool pv = p < p1;
+            gv[rr] = (pv && gval) ? __ldg(a.g + p * a.ldg + gcol) : 0.f;
+            if (a.mask && pv && gval && !(__ldg(a.mask + p * a.mask_ld + gcol) > 0.f)) gv[rr] = 0.f;
+            xv[rr] = pv ? (xp ? __ldg(xp + p * xld) : (xcol == a.ci ? 1.f : 0.f)) : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) {
+            Gs[rr][tid] = gv[rr];
+            Xs[rr][tid] = xv[rr];
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int rr = 0; rr < 32; ++rr) {
+            const float4 g0 = *reinterpret_cast<const float4 *>(&Gs[rr][8 * ty]);
+            const float4 g1 = *reinterpret_cast<const float4 *>(&Gs[rr][8 * ty + 4]);
+            const float4 x0 = *reinterpret_cast<const float4 *>(&Xs[rr][8 * tx]);
+            const float4 x1 = *reinterpret_cast<const float4 *>(&Xs[rr][8 * tx + 4]);
+            const float g8[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+            const float x8[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(g8[i], x8[j], acc[i][j]);
+        }
+    }
+    const int ldp = a.ci + 1;
+    float *out = a.part + (int64_t)blockIdx.z * a.co * ldp;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int o = co0 + 8 * ty + i, c = ci0 + 8 * tx + j;
+            if (o < a.co && c <= a.ci) out[(int64_t)o * ldp + c] = acc[i][j];
+        }
+}
+__global__ void wgrad_reduce_kernel(const float *__restrict__ part, int nchunk, int co, int ci, float *__restrict__ dw,
+                                    float *__restrict__ db) {
+    const int ldp = ci + 1;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < co * ldp; idx += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int z = 0; z < nchunk; ++z) s += (double)part[(int64_t)z * co * ldp + idx];
+        const int o = idx / ldp, c = idx % ldp;
+        if (c < ci) {
+            if (dw) dw[(int64_t)o * ci + c] = (float)s;
+        } else if (db) {
+            db[o] = (float)s;
+        }
+    }
+}
+
+}  // namespace gemm
+}  // namespace fc
+
+using namespace fc;
+
+extern "C" int64_t fc_gemm_image_bytes(int ncols, int kblocks) { return gemm::image_bytes(ncols, kblocks); }
+
+extern "C" int fc_gemm_pack_b(int transpose, int nrows, int nseg, const int *seg_src, const int *seg_k,
+                              const float *w, int64_t ldw, uint8_t *img, void *stream) {
+    if (nseg < 1 || nseg > gemm::kMaxOps || nrows < 1) return set_error(FC_ERR_CONFIG, "gemm_pack_b: bad segments");
+    gemm::PackArgs a{};
+    a.w = w;
+    a.ldw = ldw;
+    a.transpose = transpose;
+    a.nrows = nrows;
+    a.nc = gemm::chunk_cols(nrows);
+    a.nseg = nseg;
+    int kb = 0;
+    for (int s = 0; s < nseg; ++s) {
+        if (seg_k[s] < 1) return set_error(FC_ERR_CONFIG, "gemm_pack_b: empty segment");
+        a.seg_src[s] = seg_src[s];
+        a.seg_k[s] = seg_k[s];
+        a.seg_kb0[s] = kb;
+        kb += (int)ceil_div(seg_k[s], 32);
+    }
+    a.kblocks = kb;
+    a.img = img;
+    const int64_t total = ceil_div(nrows, a.nc) * kb * a.nc * 32;
+    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 4 * num_sms());
+    gemm::pack_b_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(a);
+    count_launch();
+    return check_launch("gemm_pack_b");
+}
+
+extern "C" int fc_gemm_rows(int64_t n, int nops, const float *const *a_ptr, const int64_t *lda, const int *ka,
+                            const float *mask, int64_t mask_ld, const uint8_t *img, int ncols, const float *bias,
+                            int nouts, float *const *out, const int64_t *ld, const int *c0, const int *c1,
+                            float *relu_out, int64_t relu_ld, void *stream) {
+    if (nops < 1 || nops > gemm::kMaxOps || nouts < 0 || nouts > gemm::kMaxOuts || ncols < 1)
+        return set_error(FC_ERR_CONFIG, "gemm_rows: bad operand / output count");
+    if (n <= 0) return FC_OK;
+    gemm::Args a{};
+    a.n = n;
+    a.nops = nops;
+    int kb = 0;
+    for (int q = 0; q < nops; ++q) {
+        if (ka[q] < 1 || lda[q] < ka[q]) return set_error(FC_ERR_SHAPE, "gemm_rows: operand %d shape", q);
+        a.ops[q] = gemm::Op{a_ptr[q], lda[q], ka[q], kb};
+        kb += (int)ceil_div(ka[q], 32);
+    }
+    a.kblocks = kb;
+    a.mask = mask;
+    a.mask_ld = mask_ld;
+    a.bimg = img;
+    a.nc = gemm::chunk_cols(ncols);
+    a.nchunks = (int)ceil_div(ncols, a.nc);
+    a.ncols = ncols;
+    a.bias = bias;
+    a.nouts = nouts;
+    for (int o = 0; o < nouts; ++o) {
+        if (c0[o] < 0 || c1[o] > ncols || c0[o] >= c1[o] || ld[o] < c1[o] - c0[o])
+            return set_error(FC_ERR_SHAPE, "gemm_rows: output %d columns", o);
+        a.outs[o] = gemm::Out{out[o], ld[o], c0[o], c1[o]};
+    }
+    a.relu = relu_out;
+    a.relu_ld = relu_ld;
+    const int smem = gemm::kStages * (2 * gemm::kA + 2 * a.nc * 128) + 1024 + 64;  // (1 CTA / SM: TMEM 512)
+    static uint64_t attr = 0;
+    if (first_use_on_device(attr))
+        cudaFuncSetAttribute(gemm::gemm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             gemm::kStages * (2 * gemm::kA + 2 * 128 * 128) + 1024 + 64);
+    const int grid = (int)std::min<int64_t>(ceil_div(n, gemm::kTileM), num_sms());
+    prof_begin("tc_pointwise", (cudaStream_t)stream);
+    gemm::gemm_rows_kernel<<<grid, gemm::kThreads, smem, (cudaStream_t)stream>>>(a);
+    prof_end((cudaStream_t)stream);
+    count_launch();
+    return check_launch("gemm_rows");
+}
+
+extern "C" int fc_gemm_wgrad(int64_t n, const float *g, int64_t ldg, const float *mask, int64_t mask_ld, int co,
+                             int nops, const float *const *x, const int64_t *ldx, const int *kx, float *dw, float *db,
+                             void *stream) {
+    if (nops < 0 || nops > gemm::kMaxOps || co < 1) return set_error(FC_ERR_CONFIG, "gemm_wgrad: bad operands");
+    cudaStream_t st = (cudaStream_t)stream;
+    gemm::WArgs a{};
+    a.n = n;
+    a.g = g;
+    a.ldg = ldg;
+    a.mask = mask;
+    a.mask_ld = mask_ld;
+    a.co = co;
+    a.nops = nops;
+    int ci = 0;
+    for (int q = 0; q < nops; ++q) {
+        a.ops[q] = gemm::Op{x[q], ldx[q], kx[q], ci};
+        ci += kx[q];
+    }
+    a.ci = ci;
+    const int gx = (int)ceil_div(co, 64), gy = (int)ceil_div(ci + 1, 64);
+    int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(n, 1), 512),
+                                                            ceil_div(8 * num_sms(), gx * gy)));
+    a.chunk = ceil_div(std::max<int64_t>(n, 1), nchunk);
+    nchunk = ceil_div(std::max<int64_t>(n, 1), a.chunk);
+    Scratch part((size_t)nchunk * co * (ci + 1) * sizeof(float), st);
+    if (!part.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (gemm_wgrad)");
+    a.part = part.as<float>();
+    prof_begin("pointwise_wgrad", st);
+    gemm::wgrad_kernel<<<dim3(gx, gy, (unsigned)nchunk), 64, 0, st>>>(a);
+    count_launch();
+    gemm::wgrad_reduce_kernel<<<(int)std::min<int64_t>(ceil_div((int64_t)co * (ci + 1), 256), 1024), 256, 0, st>>>(
+        a.part, (int)nchunk, co, ci, dw, db);
+    count_launch();
+    prof_end(st);
+    return check_launch("gemm_wgrad");
+}

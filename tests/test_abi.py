@@ -16,7 +16,7 @@ LIB = os.path.join(ROOT, "paper_1803_07289_b200", "libflexconv_b200.so")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|void|float|const char \*|uint64_t)\s*(fc_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void|float|const char \*|uint64_t|int64_t)\s*(fc_\w+)\s*\(", text, re.M)))
 
 
 @pytest.fixture(scope="module")
