@@ -1310,6 +1310,7 @@ static int dispatch_tc(int gc, int nout, const TcArgs &a0, int cin, int cout, co
     if (gc == 32 && nout == 32) return launch_tc_k<32, 32, SPLIT, REVERSE>(a, cin, cout, theta, theta_b, st, ld_cin);
     if (gc == 32 && nout == 64) return launch_tc_k<32, 64, SPLIT, REVERSE>(a, cin, cout, theta, theta_b, st, ld_cin);
     if (gc == 32 && nout == 128) return launch_tc_k<32, 128, SPLIT, REVERSE>(a, cin, cout, theta, theta_b, st, ld_cin);
+    if (gc == 32 && nout == 256) return launch_tc_k<32, 256, SPLIT, REVERSE>(a, cin, cout, theta, theta_b, st, ld_cin);
     if (!SPLIT && gc == 64 && nout == 128)
         return launch_tc_k<64, 128, false, REVERSE>(a, cin, cout, theta, theta_b, st, ld_cin);
     return set_error(FC_ERR_UNSUPPORTED, "no tensor-core instance for gathered=%d out=%d", gc, nout);
@@ -1542,6 +1543,12 @@ int tc_reverse_gmc(int mode, int64_t total, int64_t n, int gc, int d, int k, int
 // location gradient's two roles accumulate over all block pairs.  The gathers are repeated
 // once per output block -- the price of keeping the moments on chip instead of writing
 // [points, 4 C] moment rows to HBM for a library GEMM.
+// output channels per pass of the channel-blocked engines: all of them up to 256
+static int blocked_out_block(int c) {
+    if (c <= 256) return c % 64 == 0 && c != 192 ? c : 64;
+    return c % 256 == 0 ? 256 : (c % 128 == 0 ? 128 : 64);
+}
+
 int tc_blocked_supported(int mode, int c_in, int d, int c_out) {
     return (d == 3 && mode != FC_MODE_SIMT && c_in % 64 == 0 && c_out % 64 == 0 && (c_in > 64 || c_out > 64)) ? 1 : 0;
 }
@@ -1549,8 +1556,14 @@ int tc_blocked_supported(int mode, int c_in, int d, int c_out) {
 int tc_blocked_forward(int mode, int64_t total, int64_t n, int c_in, int k, int c_out, const float *feat,
                        const float *loc, const int32_t *nbr, const float *theta, const float *theta_b, float *out,
                        cudaStream_t st) {
-    for (int o0 = 0; o0 < c_out; o0 += 64) {
-        for (int i0 = 0; i0 < c_in; i0 += 64) {
+    // each 32-channel block of the input is gathered ONCE and contracted against all (up to
+    // 256) output channels in one pass (N = 128 / 256 accumulators), the blocks' products
+    // summed in the epilogue (acc): the gather -- the kernel's cost -- is not repeated per
+    // output block
+    const int ob = blocked_out_block(c_out);
+    const int gb = ob > 64 ? 32 : 64;  // 64-channel gathers where the output block is 64 wide
+    for (int o0 = 0; o0 < c_out; o0 += ob) {
+        for (int i0 = 0; i0 < c_in; i0 += gb) {
             TcArgs a{};
             a.total = total;
             a.n = n;
@@ -1563,8 +1576,8 @@ int tc_blocked_forward(int mode, int64_t total, int64_t n, int c_in, int k, int 
             a.ld_out = c_out;
             a.acc = i0 > 0;
             const float *th = theta + ((int64_t)o0 * c_in + i0) * 3, *tb = theta_b + (int64_t)o0 * c_in + i0;
-            const int rc = mode == FC_MODE_TC_BF16 ? dispatch_tc<false, false>(64, 64, a, 64, 64, th, tb, st, c_in)
-                                                   : dispatch_tc<true, false>(64, 64, a, 64, 64, th, tb, st, c_in);
+            const int rc = mode == FC_MODE_TC_BF16 ? dispatch_tc<false, false>(gb, ob, a, gb, ob, th, tb, st, c_in)
+                                                   : dispatch_tc<true, false>(gb, ob, a, gb, ob, th, tb, st, c_in);
             if (rc) return rc;
         }
     }
@@ -1577,8 +1590,13 @@ int tc_blocked_forward(int mode, int64_t total, int64_t n, int c_in, int k, int 
 static int tc_blocked_reverse(int mode, int64_t total, int64_t n, int c_in, int k, int c_out, const float *rows,
                               const float *loc, Csr csr, const float *theta, const float *theta_b, float *out,
                               const float *feat, const float *centre, float *dloc, cudaStream_t st) {
-    for (int i0 = 0; i0 < c_in; i0 += 64) {
-        for (int j0 = 0; j0 < c_out; j0 += 64) {
+    // gathered (c') blocks of 32 channels, each gathered once per output block of up to 256
+    // channels (64-channel gathers for a 64-wide output block, e.g. with the location-gradient
+    // epilogue, whose U accumulators need 4x the columns)
+    const int ob = dloc ? 64 : blocked_out_block(c_in);
+    const int gb = ob > 64 ? 32 : 64;
+    for (int i0 = 0; i0 < c_in; i0 += ob) {
+        for (int j0 = 0; j0 < c_out; j0 += gb) {
             TcArgs a{};
             a.total = total;
             a.n = n;
@@ -1598,8 +1616,8 @@ static int tc_blocked_reverse(int mode, int64_t total, int64_t n, int c_in, int 
                 a.acc_dloc = (i0 > 0 || j0 > 0);
             }
             const float *th = theta + ((int64_t)j0 * c_in + i0) * 3, *tb = theta_b + (int64_t)j0 * c_in + i0;
-            const int rc = mode == FC_MODE_TC_BF16 ? dispatch_tc<false, true>(64, 64, a, 64, 64, th, tb, st, c_in)
-                                                   : dispatch_tc<true, true>(64, 64, a, 64, 64, th, tb, st, c_in);
+            const int rc = mode == FC_MODE_TC_BF16 ? dispatch_tc<false, true>(gb, ob, a, ob, gb, th, tb, st, c_in)
+                                                   : dispatch_tc<true, true>(gb, ob, a, ob, gb, th, tb, st, c_in);
             if (rc) return rc;
         }
     }
