@@ -141,6 +141,7 @@ struct GridParams {
     int G[3];
     int bits[3];
     int d;
+    int rowmajor;  // cell keys: 0 = Morton interleave (spatial order), 1 = x-fastest rows (kNN)
 };
 
 __device__ __forceinline__ int64_t interleave_cell(const GridParams &gp, int cx, int cy, int cz) {
@@ -152,6 +153,14 @@ __device__ __forceinline__ int64_t interleave_cell(const GridParams &gp, int cx,
         for (int t = 0; t < 3; ++t)
             if (l < gp.bits[t]) code |= (int64_t)((c[t] >> l) & 1) << (pos++);
     return code;
+}
+
+// cell key of the cell CSR: Morton code (spatial_order: 3-D-local runs for the conv tiles) or
+// x-fastest row-major (kNN: a row of cells along x is one contiguous bucket range, scanned
+// as one run of points instead of cell by cell)
+__device__ __forceinline__ int64_t cell_key(const GridParams &gp, int cx, int cy, int cz) {
+    if (gp.rowmajor) return ((int64_t)cz * gp.G[1] + cy) * gp.G[0] + cx;
+    return interleave_cell(gp, cx, cy, cz);
 }
 
 __device__ __forceinline__ int cell_coord(const GridParams &gp, double x, int t) {
@@ -221,10 +230,11 @@ __global__ void bbox_final_kernel(int parts, const double *__restrict__ partial,
 // 2^(sum of per-axis bits) must fit the caller's capacity `cap` (sized on the host from n
 // alone), else h grows until it does.  Any h > 0 gives the same (exact) neighbour rows.
 __global__ void grid_params_kernel(const double *__restrict__ box, int64_t n, int d, double ppc, int64_t cap,
-                                   GridParams *__restrict__ gp_out) {
+                                   int rowmajor, GridParams *__restrict__ gp_out) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     GridParams gp{};
     gp.d = d;
+    gp.rowmajor = rowmajor;
     double ext[3];
     int deff = 0;
     double vol = 1.0;
@@ -250,7 +260,8 @@ __global__ void grid_params_kernel(const double *__restrict__ box, int64_t n, in
             gp.bits[t] = b;
             total_bits += b;
         }
-        if (((int64_t)1 << total_bits) <= cap) break;
+        const int64_t space = rowmajor ? (int64_t)gp.G[0] * gp.G[1] * gp.G[2] : ((int64_t)1 << total_bits);
+        if (space <= cap) break;
         h *= 1.25;
     }
     gp.h = h;
@@ -265,7 +276,7 @@ __global__ void cell_bucket_kernel(int64_t n, int d, const PT *__restrict__ pts,
          i += (int64_t)gridDim.x * blockDim.x) {
         int c[3] = {0, 0, 0};
         for (int t = 0; t < d && t < 3; ++t) c[t] = cell_coord(gp, coord(pts, i, d, t), t);
-        bucket[i] = (int32_t)interleave_cell(gp, c[0], c[1], c[2]);
+        bucket[i] = (int32_t)cell_key(gp, c[0], c[1], c[2]);
     }
 }
 
@@ -319,6 +330,25 @@ __global__ void __launch_bounds__(128)
     const int rmax = max(gp.G[0], max(gp.G[1], gp.G[2]));
     const double margin = gp.h * 1e-7;
     const double prune_margin = gp.h * gp.h * 1e-6;
+    auto scan = [&](int32_t s0, int32_t s1) {  // candidates of a contiguous bucket range
+        for (int32_t s = s0; s < s1; ++s) {
+            const double4 pj = sp[s];
+            const int32_t j = (int32_t)pj.w;
+            if (j == i) continue;
+            double dist = 0.0, dv;
+            dv = __dsub_rn(pi.x, pj.x);
+            dist = __dadd_rn(dist, __dmul_rn(dv, dv));
+            if (gp.d > 1) {
+                dv = __dsub_rn(pi.y, pj.y);
+                dist = __dadd_rn(dist, __dmul_rn(dv, dv));
+            }
+            if (gp.d > 2) {
+                dv = __dsub_rn(pi.z, pj.z);
+                dist = __dadd_rn(dist, __dmul_rn(dv, dv));
+            }
+            topk_insert<KK>(bd, bi, dist, j);
+        }
+    };
     for (int r = 0;; ++r) {
         for (int dz = -r; dz <= r; ++dz) {
             const int z = c[2] + dz;
@@ -327,8 +357,7 @@ __global__ void __launch_bounds__(128)
                 const int y = c[1] + dy;
                 if (y < 0 || y >= gp.G[1]) continue;
                 const bool full = (dz == -r || dz == r || dy == -r || dy == r);
-                const int step = full ? 1 : (r > 0 ? 2 * r : 1);
-                // lower bound of the squared distance to any point of the cell row (y, z):
+                // lower bound of the squared distance to any point of a cell of row (y, z):
                 // cells farther than the current k-1-th distance cannot contribute (exact:
                 // boundary cells are unbounded outward, and a small margin covers rounding)
                 double worst = DBL_MAX;
@@ -336,28 +365,22 @@ __global__ void __launch_bounds__(128)
                 for (int a = 0; a < KK; ++a)
                     if (a == kk - 1) worst = bd[a];
                 const double gyz = cell_gap2(gp, px[1], y, 1) + cell_gap2(gp, px[2], z, 2);
-                for (int dx = -r; dx <= r; dx += step) {
-                    const int x = c[0] + dx;
-                    if (x < 0 || x >= gp.G[0]) continue;
-                    if (worst < DBL_MAX && gyz + cell_gap2(gp, px[0], x, 0) - prune_margin > worst) continue;
-                    const int64_t b = interleave_cell(gp, x, y, z);
-                    const int32_t s1 = off[b + 1];
-                    for (int32_t s = off[b]; s < s1; ++s) {
-                        const double4 pj = sp[s];
-                        const int32_t j = (int32_t)pj.w;
-                        if (j == i) continue;
-                        double dist = 0.0, dv;
-                        dv = __dsub_rn(pi.x, pj.x);
-                        dist = __dadd_rn(dist, __dmul_rn(dv, dv));
-                        if (gp.d > 1) {
-                            dv = __dsub_rn(pi.y, pj.y);
-                            dist = __dadd_rn(dist, __dmul_rn(dv, dv));
-                        }
-                        if (gp.d > 2) {
-                            dv = __dsub_rn(pi.z, pj.z);
-                            dist = __dadd_rn(dist, __dmul_rn(dv, dv));
-                        }
-                        topk_insert<KK>(bd, bi, dist, j);
+                if (worst < DBL_MAX && gyz - prune_margin > worst) continue;  // the whole row
+                const int64_t rb = ((int64_t)z * gp.G[1] + y) * gp.G[0];
+                if (full) {
+                    // the row's cells x0 .. x1 are one contiguous bucket range; trim pruned ends
+                    int x0 = max(c[0] - r, 0), x1 = min(c[0] + r, gp.G[0] - 1);
+                    if (worst < DBL_MAX) {
+                        while (x0 <= x1 && gyz + cell_gap2(gp, px[0], x0, 0) - prune_margin > worst) ++x0;
+                        while (x1 >= x0 && gyz + cell_gap2(gp, px[0], x1, 0) - prune_margin > worst) --x1;
+                    }
+                    if (x0 <= x1) scan(off[rb + x0], off[rb + x1 + 1]);
+                } else {
+                    for (int dx = -r; dx <= r; dx += 2 * r) {
+                        const int x = c[0] + dx;
+                        if (x < 0 || x >= gp.G[0]) continue;
+                        if (worst < DBL_MAX && gyz + cell_gap2(gp, px[0], x, 0) - prune_margin > worst) continue;
+                        scan(off[rb + x], off[rb + x + 1]);
                     }
                 }
             }
@@ -425,7 +448,7 @@ static int64_t cell_capacity(int64_t n, double ppc) {
 // (device) -> cell keys -> stable counting sort.  gp_d (device), off [cap+1], ent [n].
 template <typename PT>
 static int cell_csr(int64_t n, int d, const PT *pts, GridParams *gp_d, int32_t **off_out, int32_t **ent_out,
-                    int64_t *buckets_out, cudaStream_t st, double ppc_default = 2.0) {
+                    int64_t *buckets_out, cudaStream_t st, double ppc_default = 2.0, int rowmajor = 0) {
     static const double ppc_env = [] {  // points per cell override (FC_KNN_PPC, for tuning)
         const char *e = getenv("FC_KNN_PPC");
         return e ? atof(e) : 0.0;
@@ -438,7 +461,7 @@ static int cell_csr(int64_t n, int d, const PT *pts, GridParams *gp_d, int32_t *
         if (!partial.ok() || !box.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (bbox)");
         bbox_partial_kernel<PT><<<parts, 256, 0, st>>>(n, d, pts, partial.as<double>());
         bbox_final_kernel<<<1, 192, 0, st>>>(parts, partial.as<double>(), box.as<double>());
-        grid_params_kernel<<<1, 32, 0, st>>>(box.as<double>(), n, d, ppc, cap, gp_d);
+        grid_params_kernel<<<1, 32, 0, st>>>(box.as<double>(), n, d, ppc, cap, rowmajor, gp_d);
         count_launch();
         count_launch();
         count_launch();
@@ -481,7 +504,7 @@ static int knn_grid(int64_t batch, int64_t n, int d, int k, const PT *pts, int32
         int64_t buckets = 0;
         // kNN grid: ~3 points per cell at K <= 9 (measured 1M points: 1 -> 2.23, 2 -> 1.94,
         // 3 -> 1.82, 4 -> 1.83, 6 -> 1.93 ms), about K / 3 beyond
-        if (int rc = cell_csr<PT>(n, d, p, gp.as<GridParams>(), &off, &ent, &buckets, st, std::max(3.0, k / 3.0)))
+        if (int rc = cell_csr<PT>(n, d, p, gp.as<GridParams>(), &off, &ent, &buckets, st, std::max(3.0, k / 3.0), 1))
             return rc;
         Scratch sp(sizeof(double4) * n, st);
         if (!sp.ok()) {
