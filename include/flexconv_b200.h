@@ -108,6 +108,15 @@ int fc_conv_backward(int dtype, int mode, int64_t batch, int64_t n, int c_in, in
  * y = A(theta)^T x of flex_conv with the SAME theta shapes.  Exact reference equivalent:
  * flex_conv_backward(upstream=x, ...).d_features (_native.pyx:106-120).
  * x [B*N, c_out] -> y [B*N, c_in].  Needs the reverse neighbourhood. */
+/* Forward of the rows rows[0 .. nrows) only (sorted int32 row ids of one cloud of n points;
+ * the other rows of `out` are untouched): a point-chunk shard computes its interior rows while
+ * the halo exchange is in flight, then its boundary rows.  fp32, c_in = c_out = 64, d = 3,
+ * k = 8 (the tensor-core split engine); else FC_ERR_UNSUPPORTED.  Replaces nothing in the
+ * reference (single-process); the rows it computes equal fc_conv_forward's. */
+int fc_conv_forward_rows(int64_t n, int c_in, int d, int k, int c_out, const void *features,
+                         const void *locations, const int32_t *neighbors, const void *theta,
+                         const void *theta_b, const int32_t *rows, int64_t nrows, void *out,
+                         void *stream);
 int fc_deconv_forward(int dtype, int mode, int64_t batch, int64_t n, int c_in, int d, int k,
                       int c_out, const void *x, const void *locations,
                       const int32_t *rev_offsets, const int32_t *rev_entries,

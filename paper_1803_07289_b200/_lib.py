@@ -42,6 +42,7 @@ SIGNATURES = {
     "fc_profile_ms": [_I],
     "fc_conv_forward": [_I, _I, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P],
     "fc_conv_backward": [_I, _I, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "fc_conv_forward_rows": [_I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I64, _P, _P],
     "fc_deconv_forward": [_I, _I, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "fc_csr_build": [_I64, _I64, _I, _P, _P, _P, _P],
     "fc_csr_build_async": [_I64, _I64, _I, _P, _P, _P, _P, _P],

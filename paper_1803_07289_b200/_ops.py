@@ -115,6 +115,31 @@ def conv_forward(feat, loc, nbr, theta, theta_b, batch, n, mode="auto"):
     return out
 
 
+def conv_forward_rows_supported(c_in, d, k, c_out, dtype) -> bool:
+    return dtype == torch.float32 and (c_in, d, k, c_out) == (64, 3, 8, 64)
+
+
+def conv_forward_rows(feat, loc, nbr, theta, theta_b, rows, out):
+    """Write rows `rows` (sorted int32 row ids) of the forward of one cloud into `out` [n, C_out]
+    (fc_conv_forward_rows; other rows untouched).  Used to overlap a shard's interior rows with
+    its halo exchange."""
+    feat = _need(feat, "features", torch.float32)
+    dev = feat.device
+    loc = _need(loc, "locations", torch.float32, dev)
+    nbr = _need(nbr, "neighbors", torch.int32, dev)
+    rows = _need(rows, "rows", torch.int32, dev)
+    c_out, c_in, d = _conv_shapes(theta, theta_b)
+    n, k = nbr.shape
+    _shape(feat, (n, c_in), "features")
+    _shape(loc, (n, d), "locations")
+    _shape(out, (n, c_out), "out")
+    if not out.is_contiguous():
+        raise ShapeMismatchError("out must be contiguous")
+    _call(dev, "fc_conv_forward_rows", n, c_in, d, k, c_out, _p(feat), _p(loc), _p(nbr), _p(_need(theta, "theta")),
+          _p(_need(theta_b, "theta_b")), _p(rows), rows.numel(), _p(out), _stream(feat))
+    return out
+
+
 def conv_backward(g, feat, loc, nbr, csr, theta, theta_b, batch, n, need=(True, True, True, True),
                   mode="auto"):
     """Returns (d_features, d_theta, d_theta_b, d_locations); entries not in `need` are None."""

@@ -152,6 +152,12 @@ int launch_inverse_density(int64_t n, int d, int k, const double *pts, const int
 
 }  // namespace fc
 
+namespace fc {
+int tc_fast_forward(bool split, int64_t total, int64_t n, const float *feat, const float *loc, const int32_t *nbr,
+                    const float *theta, const float *theta_b, float *out, cudaStream_t st, const int32_t *rows,
+                    int64_t nrows);
+}
+
 using namespace fc;
 
 #define ST(s) (reinterpret_cast<cudaStream_t>(s))
@@ -206,6 +212,19 @@ float fc_profile_ms(int i) {
         return -1.f;
     }
     return ms;
+}
+
+// Forward of a subset of the rows of one cloud (the interior rows of a point-chunk shard while
+// its halo rows are in flight, then the boundary rows): fp32 split engine, the headline shape.
+int fc_conv_forward_rows(int64_t n, int c_in, int d, int k, int c_out, const void *features, const void *locations,
+                         const int32_t *neighbors, const void *theta, const void *theta_b, const int32_t *rows,
+                         int64_t nrows, void *out, void *stream) {
+    if (int rc = check_conv_shape(1, n, c_in, d, k, c_out)) return rc;
+    if (!(c_in == 64 && c_out == 64 && d == 3 && k == 8))
+        return set_error(FC_ERR_UNSUPPORTED, "row-list forward covers c_in = c_out = 64, d = 3, k = 8");
+    if (nrows < 0 || nrows > n) return set_error(FC_ERR_SHAPE, "nrows %lld outside [0, %lld]", (long long)nrows, (long long)n);
+    return fc::tc_fast_forward(true, n, n, (const float *)features, (const float *)locations, neighbors, (const float *)theta,
+                           (const float *)theta_b, (float *)out, ST(stream), rows, nrows);
 }
 
 int fc_conv_forward(int dtype, int mode, int64_t batch, int64_t n, int c_in, int d, int k, int c_out,

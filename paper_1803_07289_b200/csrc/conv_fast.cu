@@ -70,6 +70,10 @@ struct FwdArgs {
     const uint8_t *bimg;
     const float *binv;
     float *out;
+    // row-list mode (wide kernel): compute only the rows rows[0 .. nrows) (sorted, < total),
+    // e.g. the interior rows of a shard while its halo is in flight; null = every row
+    const int32_t *rows;
+    int64_t nrows;
     int dbg;                    // timing-probe variants (FC_DBG): 2 no MMA, 8 gather+index only, 32 CTA-0 trace
     unsigned long long *trace;  // [24 warps][kTraceN]
 };
@@ -352,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_fwd64_kernel(FwdArgs a) {
         if (T > 0) issue_loads(0, 0, 0);
         for (int i = 0; i < T; ++i) {
             const bool tile_ok = true;
-            const int64_t lim = a.total - ((int64_t)blockIdx.x + (int64_t)i * gridDim.x) * kTile;
+            const int64_t lim = (a.rows ? a.nrows : a.total) - ((int64_t)blockIdx.x + (int64_t)i * gridDim.x) * kTile;
 #pragma unroll 1
             for (int hk = 0; hk < 4; ++hk) {
                 const int h = hk >> 1, k = hk & 1;
@@ -511,6 +515,12 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     const int T = a.num_tiles > blockIdx.x ? (int)ceil_div(a.num_tiles - blockIdx.x, gridDim.x) : 0;
+    // point of row t of tile `tile` (past the end: a.total, i.e. invalid)
+    auto row_of = [&](int64_t tile, int t) -> int64_t {
+        const int64_t q = tile * kTile + t;
+        if (!a.rows) return q;
+        return q < a.nrows ? (int64_t)__ldg(a.rows + q) : a.total;
+    };
 
     if (warp >= wCtlWarp0) {
         // ------------------------------------------------------------ control warpgroup
@@ -539,7 +549,7 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
             const int b = i & 1;
             mbar_wait_sleep(acc_full + b, (uint32_t)((i >> 1) & 1));
             tc_fence_after();
-            const int64_t p = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + t;
+            const int64_t p = row_of(blockIdx.x + (int64_t)i * gridDim.x, t);
             const float s0 = exp2i(rs[(b * 2 + 0) * kTile + t]) * binv;
             const float s1 = exp2i(rs[(b * 2 + 1) * kTile + t]) * binv;
             const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(b * 256);
@@ -570,7 +580,7 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
             if (lane == 0) mbar_arrive(acc_free + b);
         };
         auto produce = [&](int i) {  // entries of tile i (one thread per row)
-            const int64_t p = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + t;
+            const int64_t p = row_of(blockIdx.x + (int64_t)i * gridDim.x, t);
             const bool v = p < a.total;
             int4 n0 = make_int4(0, 0, 0, 0), n1 = n0;
             int32_t base = 0;
@@ -655,7 +665,7 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
             load4(0, 0, 0);
         }
         for (int i = 0; i < T; ++i) {
-            const int64_t lim = a.total - ((int64_t)blockIdx.x + (int64_t)i * gridDim.x) * kTile;
+            const int64_t lim = (a.rows ? a.nrows : a.total) - ((int64_t)blockIdx.x + (int64_t)i * gridDim.x) * kTile;
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
 #pragma unroll
@@ -727,7 +737,8 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
 
 // forward for c_in = c_out = 64, k = 8, d = 3 (the bench / C3 / C4 shape)
 int tc_fast_forward(bool split, int64_t total, int64_t n, const float *feat, const float *loc, const int32_t *nbr,
-                    const float *theta, const float *theta_b, float *out, cudaStream_t st) {
+                    const float *theta, const float *theta_b, float *out, cudaStream_t st, const int32_t *rows,
+                    int64_t nrows) {
     using namespace fast;
     const size_t bbytes = split ? FwdL<true>::B_BYTES : FwdL<false>::B_BYTES;
     uint8_t *img = (uint8_t *)scratch_alloc(bbytes + 256, st);
@@ -739,7 +750,9 @@ int tc_fast_forward(bool split, int64_t total, int64_t n, const float *feat, con
     FwdArgs a{};
     a.total = total;
     a.n = n;
-    a.num_tiles = ceil_div(total, kTile);
+    a.num_tiles = ceil_div(rows ? nrows : total, kTile);
+    a.rows = rows;
+    a.nrows = nrows;
     a.feat = feat;
     a.loc = loc;
     a.nbr = nbr;
@@ -762,6 +775,12 @@ int tc_fast_forward(bool split, int64_t total, int64_t n, const float *feat, con
     if (narrow < 0) {
         const char *e = getenv("FC_FWD_NARROW");
         narrow = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (rows && narrow) return set_error(FC_ERR_UNSUPPORTED, "row-list forward needs the wide kernel");
+    if (a.num_tiles == 0) {
+        prof_end(st);
+        scratch_free(img, st);
+        return FC_OK;
     }
     if (!narrow) {
         if (split) {

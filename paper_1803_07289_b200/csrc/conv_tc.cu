@@ -1339,7 +1339,8 @@ void launch_pack_b(bool split, int cin, int cout, const float *theta, const floa
 }
 
 int tc_fast_forward(bool split, int64_t total, int64_t n, const float *feat, const float *loc, const int32_t *nbr,
-                    const float *theta, const float *theta_b, float *out, cudaStream_t st);
+                    const float *theta, const float *theta_b, float *out, cudaStream_t st,
+                    const int32_t *rows = nullptr, int64_t nrows = 0);
 
 static bool fast_enabled() {
     static int on = -1;

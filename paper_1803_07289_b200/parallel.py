@@ -22,7 +22,9 @@ loop over clouds with gradient accumulation, harness.py:589-599).  Two partition
        table over [owned | halo], the reverse CSR and the exchange index lists, all device
        tensors built once per neighbourhood;
   then per layer: forward = halo gather of feature rows (one grouped point-to-point
-  exchange) + the flex-conv kernels on the local buffers; backward = the local backward
+  exchange, posted first; the interior rows -- all neighbours owned -- are computed while it
+  is in flight, fc_conv_forward_rows, then the boundary rows) + the flex-conv kernels on the
+  local buffers; backward = the local backward
   with zero upstream on the halo rows, the halo rows' d_features / d_locations partials
   sent back and added at the owners in fixed source-rank order, d_theta / d_theta_b summed
   by `fixed_order_allreduce` -- the only collective, and only for training.
@@ -137,6 +139,12 @@ class Comm:
     def exchange(self, sends: dict, recv_shapes: dict, dtype, device) -> dict:
         """sends[r]: tensor for rank r; recv_shapes[r]: shape expected from rank r.
         Returns {r: received tensor on `device`} (empty tensors for zero-sized shapes)."""
+        return self.exchange_finish(self.exchange_start(sends, recv_shapes, dtype, device))
+
+    def exchange_start(self, sends: dict, recv_shapes: dict, dtype, device):
+        """Post the grouped sends / receives and return at once (NCCL: the transfers run on
+        the process group's stream while the caller keeps launching kernels); gloo completes
+        here.  exchange_finish(handle) waits (stream-ordered for NCCL) and returns the rows."""
         ops, bufs, keep = [], {}, []
         for r, shape in recv_shapes.items():
             bufs[r] = torch.empty(shape, dtype=dtype, device=self.wire)
@@ -147,9 +155,17 @@ class Comm:
                 w = t.contiguous().to(self.wire)
                 keep.append(w)
                 ops.append(self.dist.P2POp(self.dist.isend, w, r, self.group))
-        if ops:
-            for req in self.dist.batch_isend_irecv(ops):
+        reqs = self.dist.batch_isend_irecv(ops) if ops else []
+        if self.host:  # gloo: blocking transport
+            for req in reqs:
                 req.wait()
+            reqs = []
+        return reqs, bufs, keep, device
+
+    def exchange_finish(self, handle) -> dict:
+        reqs, bufs, _keep, device = handle
+        for req in reqs:
+            req.wait()
         return {r: b.to(device) for r, b in bufs.items()}
 
     def exchange_sizes(self, counts: dict) -> dict:
@@ -177,7 +193,14 @@ def default_kernels():
     def csr(nbr):
         return _ops.csr_build(nbr, 1, nbr.shape[0], validate=False)
 
-    return {"knn": knn, "conv_fwd": conv_fwd, "conv_bwd": conv_bwd, "csr": csr}
+    def conv_fwd_rows(feat, loc, nbr, theta, theta_b, rows, out):
+        """None when the shape has no row-list kernel (the caller then runs the plain path)."""
+        c_out, c_in, d = theta.shape
+        if not _ops.conv_forward_rows_supported(c_in, d, nbr.shape[1], c_out, feat.dtype):
+            return None
+        return _ops.conv_forward_rows(feat, loc, nbr, theta, theta_b, rows, out)
+
+    return {"knn": knn, "conv_fwd": conv_fwd, "conv_bwd": conv_bwd, "csr": csr, "conv_fwd_rows": conv_fwd_rows}
 
 
 class ShardedCloud:
@@ -286,6 +309,10 @@ class ShardedCloud:
         got = comm.exchange(req, {q: (c,) for q, c in counts.items() if c > 0}, torch.int64, dev)
         self.send_idx = {q: t for q, t in got.items()}  # owned local ids rank q needs from here
         self.csr = kern["csr"](self.table)
+        # interior rows (every neighbour owned) can be computed before the halo arrives
+        bnd_mask = (self.table[:n_own] >= n_own).any(dim=1)
+        self.interior_rows = torch.nonzero(~bnd_mask).flatten().to(torch.int32)
+        self.boundary_rows = torch.nonzero(bnd_mask).flatten().to(torch.int32)
         return self
 
     # ------------------------------------------------------------------ row exchanges
@@ -299,10 +326,19 @@ class ShardedCloud:
 
     def fill_halo(self, local: torch.Tensor) -> torch.Tensor:
         """Fill the halo rows of a [n_local, C] buffer from their owners (in place)."""
+        return self.fill_halo_finish(self.fill_halo_start(local))
+
+    def fill_halo_start(self, local: torch.Tensor):
+        """Post the halo exchange of `local` (returns at once with NCCL)."""
         c = tuple(local.shape[1:])
-        got = self.comm.exchange({q: local[i] for q, i in self.send_idx.items()},
-                                 {q: (b - a,) + c for q, (a, b) in self.recv_slices.items()}, local.dtype,
-                                 local.device)
+        h = self.comm.exchange_start({q: local[i] for q, i in self.send_idx.items()},
+                                     {q: (b - a,) + c for q, (a, b) in self.recv_slices.items()}, local.dtype,
+                                     local.device)
+        return h, local
+
+    def fill_halo_finish(self, handle) -> torch.Tensor:
+        h, local = handle
+        got = self.comm.exchange_finish(h)
         for q, (a, b) in self.recv_slices.items():
             local[self.n_own + a:self.n_own + b] = got[q]
         return local
@@ -349,10 +385,27 @@ class ShardedFlexConv:
         return t if t.shape[0] == self.cloud.n_local else self.cloud.local_buffer(t)
 
     def forward(self, feat, theta, theta_b):
+        """Owned rows of the forward.  With a row-list kernel (kernels["conv_fwd_rows"]) the
+        interior rows -- whose neighbours are all owned -- are computed while the halo rows
+        are in flight (posted before, waited for after), then the boundary rows."""
         cl = self.cloud
         pos = cl.positions if cl.positions.dtype == feat.dtype else cl.positions.to(feat.dtype)
-        feat = cl.fill_halo(self._local(feat))
-        out = cl.kernels["conv_fwd"](feat, pos, cl.table, theta, theta_b)
+        feat = self._local(feat)
+        rows_k = cl.kernels.get("conv_fwd_rows")
+        out = None
+        if rows_k is not None:
+            handle = cl.fill_halo_start(feat)
+            buf = torch.empty((cl.n_local, theta.shape[0]), dtype=feat.dtype, device=feat.device)
+            if rows_k(feat, pos, cl.table, theta, theta_b, cl.interior_rows, buf) is not None:
+                cl.fill_halo_finish(handle)
+                rows_k(feat, pos, cl.table, theta, theta_b, cl.boundary_rows, buf)
+                out = buf
+            else:
+                cl.fill_halo_finish(handle)
+        else:
+            cl.fill_halo(feat)
+        if out is None:
+            out = cl.kernels["conv_fwd"](feat, pos, cl.table, theta, theta_b)
         self._saved = (feat, pos, theta, theta_b)
         return out[: cl.n_own]
 

@@ -35,7 +35,16 @@ def oracle_kernels():
         out = oracle.conv_backward(g.numpy(), feat.numpy(), loc.numpy(), nbr.numpy(), th.numpy(), tb.numpy())
         return tuple(torch.from_numpy(x) for x in out)
 
-    return {"knn": knn, "conv_fwd": conv_fwd, "conv_bwd": conv_bwd, "csr": lambda nbr: None}
+    def conv_fwd_rows(feat, loc, nbr, th, tb, rows, out):
+        # the rows from the CURRENT feature buffer: rows computed before the halo exchange
+        # completed (the interior rows) are wrong if they touch a halo row
+        full = oracle.conv_forward(feat.numpy(), loc.numpy(), nbr.numpy(), th.numpy(), tb.numpy(), 1)
+        r = rows.long()
+        out[r] = torch.from_numpy(full)[r]
+        return out
+
+    return {"knn": knn, "conv_fwd": conv_fwd, "conv_bwd": conv_bwd, "csr": lambda nbr: None,
+            "conv_fwd_rows": conv_fwd_rows}
 
 
 def main():
@@ -65,6 +74,8 @@ def main():
         "ghosts": cloud.n_ghost,
         "knn_rows_exact": bool(np.array_equal(cloud.global_rows.numpy(), ref_nbr[lo:hi])),
         "halo_outside": bool(((cloud.halo < lo) | (cloud.halo >= hi)).all()),
+        "interior_boundary_partition": bool(cloud.interior_rows.numel() + cloud.boundary_rows.numel() == hi - lo
+                                            and cloud.boundary_rows.numel() > 0 and cloud.interior_rows.numel() > 0),
         "fwd_bitwise": bool(np.array_equal(out.numpy(), ref_out[lo:hi])),
         "df_err": float(np.abs(df.numpy() - rdf[lo:hi]).max() / np.abs(rdf).max()),
         "dl_err": float(np.abs(dl.numpy() - rdl[lo:hi]).max() / np.abs(rdl).max()),

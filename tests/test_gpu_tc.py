@@ -222,3 +222,32 @@ def test_tc_backward_batched_partial_tiles(fc, oracle_mod):
         rdtb += r_tb
     _close_reduction(dth.cpu().numpy(), rdth, "d_theta")
     _close_reduction(dtb.cpu().numpy(), rdtb, "d_theta_b")
+
+
+def test_forward_rows_subset_equals_full_forward():
+    """fc_conv_forward_rows (a shard's interior rows while the halo is in flight, then its
+    boundary rows): every listed row bitwise equal to the full forward, other rows untouched."""
+    import torch
+
+    from paper_1803_07289_b200 import _ops
+
+    n, k = 50_000, 8
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    pos = (torch.floor(torch.rand(n, 3, device="cuda", dtype=torch.float64, generator=g) * 2 ** 24) / 2 ** 24).float()
+    pos = pos[_ops.spatial_order(pos).long()].contiguous()
+    nbr = _ops.knn(pos, 1, n, k)
+    feat = torch.randn(n, 64, device="cuda", generator=g)
+    th = 0.1 * torch.randn(64, 64, 3, device="cuda", generator=g)
+    tb = 0.1 * torch.randn(64, 64, device="cuda", generator=g)
+    full = _ops.conv_forward(feat, pos, nbr, th, tb, 1, n)
+    pick = torch.rand(n, device="cuda", generator=g) < 0.7
+    a = torch.nonzero(pick).flatten().int()
+    b = torch.nonzero(~pick).flatten().int()
+    out = torch.full((n, 64), float("nan"), device="cuda")
+    _ops.conv_forward_rows(feat, pos, nbr, th, tb, a, out)
+    assert torch.isnan(out[b.long()]).all()
+    assert torch.equal(out[a.long()], full[a.long()])
+    _ops.conv_forward_rows(feat, pos, nbr, th, tb, b, out)
+    assert torch.equal(out, full)
+    _ops.conv_forward_rows(feat, pos, nbr, th, tb, a[:0], out)  # empty list: no work

@@ -51,6 +51,7 @@ def test_point_chunk_sharding_gloo(oracle_mod, tmp_path, world):
         assert r["halo"] > 0 and r["ghosts"] >= r["halo"]
         assert r["knn_rows_exact"]
         assert r["halo_outside"]
+        assert r["interior_boundary_partition"]
         assert r["fwd_bitwise"]
         assert r["df_err"] < 1e-12 and r["dl_err"] < 1e-12
         assert r["dth_err"] < 1e-12 and r["dtb_err"] < 1e-12
