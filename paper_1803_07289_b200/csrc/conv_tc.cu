@@ -897,21 +897,28 @@ struct DtArgs {
     int acc;                // add into centre instead of overwriting (blocks after the first)
 };
 
-struct DtLayout {
-    static constexpr int GC = 64, CO = 64;
+// MT = 64-channel c' tiles per pass (M-tiles of the d_theta MMA, each [c' hi; c' lo] = 128
+// rows x N = 256 columns of TMEM): MT = 1 with the centre-role Z GEMM (TMEM 256 + 192), MT = 2
+// without it (TMEM 2 x 256) -- a wide layer's 64-channel feature block is then gathered once
+// per 128 upstream channels instead of once per 64.
+template <int MT = 1>
+struct DtLayoutT {
+    static constexpr int GC = 64, CO = 64 * MT;
+    static constexpr bool Z = MT == 1;
     static constexpr int XST = kDtChunk * 4 * GC * 4;   // one tf32 X chunk image (16 KB)
-    static constexpr int GST = kDtChunk * CO * 4;       // one tf32 G chunk image (4 KB)
+    static constexpr int GST = kDtChunk * 64 * 4;       // one tf32 G image of a c' tile (4 KB)
     static constexpr int XB = kTcM * GC * 2;            // fp16 bias-moment tile (16 KB)
-    static constexpr int BZ = CO * 128;                 // one K-block of the forward image (8 KB)
+    static constexpr int BZ = 64 * 128;                 // one K-block of the forward image (8 KB)
     static constexpr int X_OFF = 0;                     // [stage][hi, lo]
-    static constexpr int G_OFF = X_OFF + 2 * 2 * XST;   // [stage][hi, lo]
-    static constexpr int XB_OFF = G_OFF + 2 * 2 * GST;  // [buf][hi, lo]
-    static constexpr int B_OFF = XB_OFF + 2 * 2 * XB;   // [hi K-blocks 0..2][lo K-blocks 0..2]
-    static constexpr int RS_OFF = B_OFF + 2 * 3 * BZ;   // float rs[2][128]
+    static constexpr int G_OFF = X_OFF + 2 * 2 * XST;   // [stage][c' tile][hi, lo]
+    static constexpr int XB_OFF = G_OFF + 2 * MT * 2 * GST;        // [buf][hi, lo]   (Z only)
+    static constexpr int B_OFF = XB_OFF + (Z ? 2 * 2 * XB : 0);    // [hi K-blocks 0..2][lo] (Z only)
+    static constexpr int RS_OFF = B_OFF + (Z ? 2 * 3 * BZ : 0);    // float rs[2][128]
     static constexpr int BAR_OFF = RS_OFF + 2 * kTcM * 4;
     static constexpr int SMEM = BAR_OFF + 128 + 1024;
-    static constexpr int TMEM_COLS = 512;               // D: 256 (M = [c' hi; c' lo], N = k), Z: 192
+    static constexpr int TMEM_COLS = 512;  // D: MT x 256 (M = [c' hi; c' lo], N = k) [+ Z: 192]
 };
+using DtLayout = DtLayoutT<1>;
 
 __device__ __forceinline__ uint32_t f32_to_tf32(float x) {
     uint32_t r;
@@ -964,9 +971,9 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint6
         : "memory");
 }
 
-template <int KFIX>
+template <int KFIX, int MT = 1>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
-    using L = DtLayout;
+    using L = DtLayoutT<MT>;
     constexpr int GC = L::GC, CO = L::CO;
     using G = Geo<GC>;  // 16 lanes per point, 2 points per group
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -993,7 +1000,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
         fence_mbar_init();
     }
     if (warp == kMmaWarp) tmem_alloc(tmem_holder, L::TMEM_COLS);
-    {  // K-blocks 0..2 of the forward image (hi, then lo) -> resident B for Z
+    if (L::Z) {  // K-blocks 0..2 of the forward image (hi, then lo) -> resident B for Z
         const int img_b = CO * 4 * GC * 2;  // bytes of one full forward image
         for (int h = 0; h < 2; ++h) {
             const uint4 *src = reinterpret_cast<const uint4 *>(a.bimg + h * img_b);
@@ -1001,7 +1008,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
             for (int i = threadIdx.x; i < 3 * L::BZ / 16; i += blockDim.x) dst[i] = src[i];
         }
     }
-    const float binv = a.binv[0];
+    const float binv = L::Z ? a.binv[0] : 1.f;
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
@@ -1024,13 +1031,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
             tc_fence_after();
             constexpr uint32_t idesc = idesc_tf32_mn(kTcM, 4 * GC);
             const uint32_t xh = s_base + L::X_OFF + st * 2 * L::XST, xl = xh + L::XST;
-            const uint32_t gh = s_base + L::G_OFF + st * 2 * L::GST;  // [G_hi | G_lo]: 4 MN blocks of 32
 #pragma unroll
-            for (int ks = 0; ks < kDtChunk / 8; ++ks) {
-                const uint32_t ko = (uint32_t)(ks * 1024);
-                const uint32_t first = (u_global == 0 && ks == 0) ? 0u : 1u;
-                mma_tf32(tmem_base, desc_sw128b32_mn(gh + ko, 2048, 512), desc_sw128b32_mn(xh + ko, 2048, 512), idesc, first);
-                mma_tf32(tmem_base, desc_sw128b32_mn(gh + ko, 2048, 512), desc_sw128b32_mn(xl + ko, 2048, 512), idesc, 1u);
+            for (int mt = 0; mt < MT; ++mt) {
+                // c' tile mt: [G_hi | G_lo] = 4 MN blocks of 32
+                const uint32_t gh = s_base + L::G_OFF + (st * MT + mt) * 2 * L::GST;
+                const uint32_t dt = tmem_base + (uint32_t)(mt * 256);
+#pragma unroll
+                for (int ks = 0; ks < kDtChunk / 8; ++ks) {
+                    const uint32_t ko = (uint32_t)(ks * 1024);
+                    const uint32_t first = (u_global == 0 && ks == 0) ? 0u : 1u;
+                    mma_tf32(dt, desc_sw128b32_mn(gh + ko, 2048, 512), desc_sw128b32_mn(xh + ko, 2048, 512), idesc, first);
+                    mma_tf32(dt, desc_sw128b32_mn(gh + ko, 2048, 512), desc_sw128b32_mn(xl + ko, 2048, 512), idesc, 1u);
+                }
             }
             mma_commit(chunk_empty + st);
         }
@@ -1161,11 +1173,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
                 const int64_t pme = p0 + pt;
                 const bool valid = pme < a.total;
                 if (!valid) mom_zero(acc);
-                float4 gv = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (valid) gv = __ldg(reinterpret_cast<const float4 *>(a.g + pme * a.ld_g) + cl);
+                float4 gvs[MT];
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt)
+                    gvs[mt] = valid ? __ldg(reinterpret_cast<const float4 *>(a.g + pme * a.ld_g + 64 * mt) + cl)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
                 // ---- wait for the ring stage (and, at a tile's first chunk, the Xb/rs buffer)
                 if (u >= 1) mbar_wait(chunk_empty + q, (uint32_t)((u - 1) & 1));
-                if (c == q && i >= 2) mbar_wait(z_free + (i & 1), ((i >> 1) + 1) & 1);
+                if (L::Z && c == q && i >= 2) mbar_wait(z_free + (i & 1), ((i >> 1) + 1) & 1);
                 // X chunk row (tf32 hi/lo, MN-major): row rr = 2r + pt of the chunk
                 const int rr = 2 * r + pt;
                 const uint32_t xh = s_base + L::X_OFF + q * 2 * L::XST, xl = xh + L::XST;
@@ -1174,12 +1189,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
                     const uint32_t off = mn32_off(t * GC + 4 * cl, rr);
                     store_tf32x4(xh + off, xl + off, acc.m[t][0], acc.m[t][1]);
                 }
-                {   // G chunk row (tf32 hi/lo, MN-major over c')
-                    const uint32_t gh = s_base + L::G_OFF + q * 2 * L::GST, gl = gh + L::GST;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {  // G chunk rows (tf32 hi/lo, MN-major over c'), per c' tile
+                    const uint32_t gh = s_base + L::G_OFF + (q * MT + mt) * 2 * L::GST, gl = gh + L::GST;
                     const uint32_t off = mn32_off(4 * cl, rr);
-                    store_tf32x4(gh + off, gl + off, make_float2(gv.x, gv.y), make_float2(gv.z, gv.w));
+                    store_tf32x4(gh + off, gl + off, make_float2(gvs[mt].x, gvs[mt].y), make_float2(gvs[mt].z, gvs[mt].w));
                 }
-                {   // bias moments -> Xb tile row (fp16 hi/lo, per-row scale), K-major over c
+                if (L::Z) {   // bias moments -> Xb tile row (fp16 hi/lo, per-row scale), K-major over c
                     float inv = 1.f;
                     float m = 0.f;
                     m = fmaxf(fmaxf(fabsf(acc.m[3][0].x), fabsf(acc.m[3][0].y)), fmaxf(fabsf(acc.m[3][1].x), fabsf(acc.m[3][1].y)));
@@ -1204,14 +1220,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
                     // warp 15 (odd chunks) issues the MMAs of this chunk and the even one before it
                     issue_chunk(tl * 8 + c - 1);
                     issue_chunk(tl * 8 + c);
-                    if (c == 7) issue_z(i);
+                    if (L::Z && c == 7) issue_z(i);
                 }
             }
-            if (warp < kEpiWarps && i >= 1) epilogue_z(i - 1);
+            if (L::Z && warp < kEpiWarps && i >= 1) epilogue_z(i - 1);
         }
         if (warp == kMmaWarp && lane == 0) mma_commit(dt_done);
         __syncwarp();
-        if (warp < kEpiWarps && tiles_mine > 0) epilogue_z((int)tiles_mine - 1);
+        if (L::Z && warp < kEpiWarps && tiles_mine > 0) epilogue_z((int)tiles_mine - 1);
     }
     // ---------------------------------------------------------------- drain d_theta partials
     if (warp < kEpiWarps) {
@@ -1222,17 +1238,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
         // TMEM lane m = c' (hi part, warps 0-1) or 64 + c' (lo part, warps 2-3): two partial
         // slices per CTA, summed by dtheta_reduce_kernel with the other CTAs' (fixed order)
         const int m = warp * 32 + lane;
-        const int cp = m & 63;
         float *part = a.partial + ((int64_t)blockIdx.x * 2 + (m >> 6)) * (CO * 4 * GC);
 #pragma unroll 1
-        for (int n0 = 0; n0 < 4 * GC; n0 += 16) {
-            float v[16];
-            tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)n0, v);
+        for (int mt = 0; mt < MT; ++mt) {
+            const int cp = 64 * mt + (m & 63);
+#pragma unroll 1
+            for (int n0 = 0; n0 < 4 * GC; n0 += 16) {
+                float v[16];
+                tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(mt * 256 + n0), v);
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const int kx = n0 + q;  // k = t*64 + c
-                const int t = kx / GC, cc = kx % GC;
-                part[(int64_t)cp * (GC * 4) + cc * 4 + t] = tiles_mine > 0 ? v[q] : 0.f;
+                for (int q = 0; q < 16; ++q) {
+                    const int kx = n0 + q;  // k = t*64 + c
+                    const int t = kx / GC, cc = kx % GC;
+                    part[(int64_t)cp * (GC * 4) + cc * 4 + t] = tiles_mine > 0 ? v[q] : 0.f;
+                }
             }
         }
     }
@@ -1396,12 +1415,14 @@ int tc_fast_dtheta(int64_t total, int64_t n, const float *feat, const float *loc
 // d_theta_b point at the block's first channel; ld_* are the full row strides.  d_theta block
 // rows are written with row stride ld_dt (full c_in); centre is written (acc_centre = false)
 // or added to.
+template <int MT = 1>
 static int generic_dtheta_block(int64_t total, int64_t n, int k, const float *feat, int64_t ld_feat,
                                 const float *loc, const int32_t *nbr, const float *g, int64_t ld_g,
                                 const float *theta, const float *theta_b, int ld_cin, float *d_theta,
                                 float *d_theta_b, int ld_dt, float *centre, bool acc_centre, cudaStream_t st) {
-    using L = DtLayout;
-    constexpr int cin = 64, cout = 64;
+    using L = DtLayoutT<MT>;
+    constexpr int cin = 64, cout = 64 * MT;  // MT c' tiles of 64 (the centre term needs MT = 1)
+    if (MT > 1 && centre) return set_error(FC_ERR_UNSUPPORTED, "d_theta c' tiles > 1 without the centre term only");
     const int64_t num_tiles = ceil_div(total, kTcM);
     // at most 8 tiles (1024 points, 128 tf32 k-steps) accumulated in TMEM per CTA -- more
     // CTAs (waves) instead of a longer, truncating accumulation
@@ -1415,9 +1436,11 @@ static int generic_dtheta_block(int64_t total, int64_t n, int k, const float *fe
         return set_error(FC_ERR_CUDA, "scratch allocation failed (tc d_theta)");
     uint8_t *img = img_buf.as<uint8_t>();
     float *binv = reinterpret_cast<float *>(img + img_bytes);
-    tc_pack_b_kernel<true><<<(unsigned)ceil_div((int64_t)cout * 4 * cin, 1024), 1024, 0, st>>>(
-        cin, cout, ld_cin, theta, theta_b, 0, cout, cin, img, binv);
-    count_launch();
+    if (L::Z) {  // the forward image: B of the centre-role Z GEMM
+        tc_pack_b_kernel<true><<<(unsigned)ceil_div((int64_t)cout * 4 * cin, 1024), 1024, 0, st>>>(
+            cin, cout, ld_cin, theta, theta_b, 0, cout, cin, img, binv);
+        count_launch();
+    }
     DtArgs a{};
     a.total = total;
     a.n = n;
@@ -1438,12 +1461,12 @@ static int generic_dtheta_block(int64_t total, int64_t n, int k, const float *fe
     prof_begin("tc_dtheta", st);
     if (k == kSlots) {
         if (first_use_on_device(attr8))
-            cudaFuncSetAttribute(tc_dtheta_kernel<kSlots>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
-        tc_dtheta_kernel<kSlots><<<grid, kTcThreads, L::SMEM, st>>>(a);
+            cudaFuncSetAttribute(tc_dtheta_kernel<kSlots, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+        tc_dtheta_kernel<kSlots, MT><<<grid, kTcThreads, L::SMEM, st>>>(a);
     } else {
         if (first_use_on_device(attr0))
-            cudaFuncSetAttribute(tc_dtheta_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
-        tc_dtheta_kernel<0><<<grid, kTcThreads, L::SMEM, st>>>(a);
+            cudaFuncSetAttribute(tc_dtheta_kernel<0, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+        tc_dtheta_kernel<0, MT><<<grid, kTcThreads, L::SMEM, st>>>(a);
     }
     prof_end(st);
     count_launch();
@@ -1641,15 +1664,22 @@ int tc_blocked_backward(int mode, int64_t total, int64_t n, int c_in, int k, int
             centre_buf.alloc(sizeof(float) * total * 3, st);
             if (!centre_buf.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (blocked backward)");
         }
-        for (int j0 = 0; j0 < c_out; j0 += 64) {
+        // without the location gradient, c' tiles of 128 (each 64-channel feature block is
+        // gathered once per 128 upstream channels)
+        const int jb = (!d_locations && c_out % 128 == 0) ? 128 : 64;
+        for (int j0 = 0; j0 < c_out; j0 += jb) {
             for (int i0 = 0; i0 < c_in; i0 += 64) {
                 // the centre term needs every block pair; d_theta blocks are independent
                 const int64_t e0 = (int64_t)j0 * c_in + i0;
-                const int rc = generic_dtheta_block(total, n, k, feat + i0, c_in, loc, nbr, g + j0, c_out, theta + e0 * 3,
-                                                    theta_b + e0, c_in, d_theta ? d_theta + e0 * 3 : nullptr,
-                                                    d_theta_b ? d_theta_b + e0 : nullptr, c_in,
-                                                    d_locations ? centre_buf.as<float>() : nullptr,
-                                                    j0 > 0 || i0 > 0, st);
+                float *dtp = d_theta ? d_theta + e0 * 3 : nullptr, *dtbp = d_theta_b ? d_theta_b + e0 : nullptr;
+                const int rc =
+                    jb == 128 ? generic_dtheta_block<2>(total, n, k, feat + i0, c_in, loc, nbr, g + j0, c_out,
+                                                        theta + e0 * 3, theta_b + e0, c_in, dtp, dtbp, c_in, nullptr,
+                                                        false, st)
+                              : generic_dtheta_block<1>(total, n, k, feat + i0, c_in, loc, nbr, g + j0, c_out,
+                                                        theta + e0 * 3, theta_b + e0, c_in, dtp, dtbp, c_in,
+                                                        d_locations ? centre_buf.as<float>() : nullptr,
+                                                        j0 > 0 || i0 > 0, st);
                 if (rc) return rc;
             }
         }
