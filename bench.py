@@ -339,11 +339,15 @@ def make_workload(n, k, c, rank, dev, d=3):
     pos, feat, g, theta, theta_b, sort_ms = (w[x] for x in ("pos", "feat", "g", "theta", "theta_b", "sort_ms"))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    nbr = _ops.knn(pos, 1, n, k)
-    e1.record()
-    torch.cuda.synchronize()
-    knn_ms = e0.elapsed_time(e1)
+    nbr = _ops.knn(pos, 1, n, k)  # first call: scratch-pool growth, not reported
+    knn_times = []
+    for _ in range(3):  # the kNN builder (bbox, grid, bucket sort, query), median of 3 warm calls
+        e0.record()
+        nbr = _ops.knn(pos, 1, n, k)
+        e1.record()
+        torch.cuda.synchronize()
+        knn_times.append(e0.elapsed_time(e1))
+    knn_ms = statistics.median(knn_times)
     e0.record()
     csr = _ops.csr_build(nbr, 1, n)
     e1.record()
@@ -687,17 +691,19 @@ def run_e2e(args, torch, _ops, feat, pos, nbr, g, theta, theta_b, n, k, world, d
     d2h = sum(t.numel() * t.element_size() for t in host_out)
     steps = max(1, min(args.steps, 10))  # steady state: the pipeline fill / drain is amortised over the steps
 
-    # Copies overlap where the data dependencies allow: the inputs of the forward go first on
-    # a copy stream, the upstream gradient follows it while the forward runs, and the
-    # forward's output returns to the host (D2H) while the upstream gradient arrives (H2D).
-    # The reverse-neighbourhood build validates the indices (host-synchronising, like the
-    # reference's range check), so it runs on its own stream: the host waits for this step's
-    # neighbour table only, not for the previous step's result copies queued on the main stream.
+    # Copies overlap where the data dependencies allow, on two copy streams that never wait
+    # for each other: s_in carries every H2D back to back (the forward's inputs, then the
+    # upstream gradient; the next step's inputs queue right behind), s_out every D2H (the
+    # forward's output as soon as it exists, then the gradients).  The compute stream waits
+    # only for its inputs -- not for the previous step's result copies -- so the H2D link
+    # (3.9 GB per step) stays busy and the D2H (3.7 GB) runs underneath it.  The reverse-
+    # neighbourhood build validates the indices (host-synchronising, like the reference's
+    # range check) on its own stream: the host waits for this step's neighbour table only.
     main = torch.cuda.current_stream()
     s_in, s_out, s_csr = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
 
     def one():
-        with torch.cuda.stream(s_in):  # (no wait on main: overlaps the previous step's D2H)
+        with torch.cuda.stream(s_in):
             f, p, nb, th, tb = (host_in[i].to(dev, non_blocking=True) for i in (0, 1, 2, 4, 5))
             ev_in = torch.cuda.Event()
             ev_in.record(s_in)
@@ -715,15 +721,22 @@ def run_e2e(args, torch, _ops, feat, pos, nbr, g, theta, theta_b, n, k, world, d
         main.wait_stream(s_csr)
         main.wait_event(ev_in)
         out = _ops.conv_forward(f, p, nb, th, tb, 1, n, args.mode)
+        ev_f = torch.cuda.Event()
+        ev_f.record(main)
         with torch.cuda.stream(s_out):
-            s_out.wait_stream(main)
+            s_out.wait_event(ev_f)
             host_out[0].copy_(out, non_blocking=True)
         out.record_stream(s_out)
         main.wait_event(ev_g)
-        df, dth, dtb, dl = _ops.conv_backward(gg, f, p, nb, csr, th, tb, 1, n, mode=args.mode)
-        for h, dv in zip(host_out[1:], (df, dth, dtb, dl)):
-            h.copy_(dv, non_blocking=True)
-        main.wait_stream(s_out)
+        res = _ops.conv_backward(gg, f, p, nb, csr, th, tb, 1, n, mode=args.mode)
+        ev_b = torch.cuda.Event()
+        ev_b.record(main)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ev_b)
+            for h, dv in zip(host_out[1:], res):
+                h.copy_(dv, non_blocking=True)
+        for dv in res:
+            dv.record_stream(s_out)
 
     one()
     torch.cuda.synchronize()
@@ -733,6 +746,8 @@ def run_e2e(args, torch, _ops, feat, pos, nbr, g, theta, theta_b, n, k, world, d
     a.record()
     for _ in range(steps):
         one()
+    main.wait_stream(s_out)  # the stop event covers the last step's result copies
+    main.wait_stream(s_in)
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / steps
@@ -743,9 +758,9 @@ def run_e2e(args, torch, _ops, feat, pos, nbr, g, theta, theta_b, n, k, world, d
     return {"value": round(world * n / (ms / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3), "steps": steps,
             "path": "C ABI (fc_csr_build + fc_conv_forward + fc_conv_backward), pinned host fp32 buffers; "
-                    "forward-input H2D (overlapping the previous step's result D2H), then upstream-gradient H2D "
-                    "overlapped with the forward and its output D2H; the index-validating reverse-CSR build "
-                    "on a side stream"}
+                    "all H2D back to back on one copy stream, all D2H on another (forward output as soon as it "
+                    "exists, then the gradients), compute waiting only for its inputs; the index-validating "
+                    "reverse-CSR build on a side stream"}
 
 
 def run_reference(args, world, rank):
