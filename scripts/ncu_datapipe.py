@@ -1,6 +1,6 @@
 """Per-kernel L1 data-pipe budget from an `ncu --set full` report of the bench workload.
 
-    python scripts/ncu_datapipe.py gpurun_out/<report>.ncu-rep [--n 7000000] [--out profiles/ncu_datapipe.json]
+    python scripts/ncu_datapipe.py gpurun_out/<report>.ncu-rep [more reports] [--n 7000000] [--out profiles/ncu_datapipe.json]
 
 The warp-specialised kernels are bound by the SM's L1TEX data pipe (LSU wavefronts: global
 gathers, own-row loads/stores and shared-memory traffic), not by HBM.  For each kernel this
@@ -28,11 +28,23 @@ def bench_name(kernel: str):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("report")
+    ap.add_argument("report", nargs="+")
     ap.add_argument("--n", type=int, default=7_000_000)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "ncu_datapipe.json"))
     args = ap.parse_args()
-    raw = subprocess.run(["ncu", "-i", args.report, "--page", "raw", "--csv"], capture_output=True, text=True,
+    out = {"n": args.n, "report": ", ".join(os.path.basename(r) for r in args.report),
+           "source": "ncu --set full --clock-control none (one launch per kernel); wavefronts per point = "
+                     "SM-average x 148 SMs / n", "kernels": {}}
+    for rep in args.report:
+        one_report(rep, args, out)
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as fh:
+        json.dump(out, fh, indent=1)
+    print(json.dumps(out, indent=1))
+
+
+def one_report(report, args, out):
+    raw = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True,
                          check=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     hdr = rows[0]
@@ -44,9 +56,6 @@ def main():
         except (KeyError, ValueError):
             return None
 
-    out = {"n": args.n, "report": os.path.basename(args.report),
-           "source": "ncu --set full --clock-control none (one launch per kernel); wavefronts per point = "
-                     "SM-average x 148 SMs / n", "kernels": {}}
     for r in rows[2:]:
         name = bench_name(r[col["Kernel Name"]])
         if not name or name in out["kernels"]:
@@ -77,10 +86,6 @@ def main():
             "bank_conflict_wavefronts_per_point": (round(val(r, "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum") / args.n, 2)
                                                    if val(r, "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum") else None),
         }
-    os.makedirs(os.path.dirname(args.out), exist_ok=True)
-    with open(args.out, "w") as fh:
-        json.dump(out, fh, indent=1)
-    print(json.dumps(out, indent=1))
 
 
 if __name__ == "__main__":
