@@ -60,7 +60,7 @@ def build(verbose: bool = True) -> str:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         cmd = [NVCC, "-ccbin", HOST_CC, "-shared", "-o", LIB] + objs + ARCH + [
-            "-lcudart", "-lcuda", "-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+            "-lcudart", "-lcuda", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
         subprocess.check_call(cmd)
         if verbose:
             print(f"linked {LIB}")

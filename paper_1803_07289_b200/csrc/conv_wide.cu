@@ -19,7 +19,6 @@
 //                   Partials per chunk are reduced in fixed order by dtheta_reduce_kernel.
 #include "fc_common.cuh"
 
-#include <cublas_v2.h>
 
 #include <cstdlib>
 
@@ -638,15 +637,28 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-cublasHandle_t cublas_handle() {
-    static cublasHandle_t h[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!h[dev & 63]) {
-        if (cublasCreate(&h[dev & 63]) != CUBLAS_STATUS_SUCCESS) return nullptr;
-        cublasSetMathMode(h[dev & 63], CUBLAS_DEFAULT_MATH);  // FP32 FMA, no TF32
-    }
-    return h[dev & 63];
+// out [m, ncols] (row stride ldo) = A [m, k] (row stride lda) . B [k, ncols] (row-major, row
+// stride ldb) on the hand-written tcgen05 GEMM (gemm_tc.cu: tf32 hi/lo split operands, fp32
+// accumulation with K-block partials summed in registers); img: a packed image of B from
+// pack_b_rm (reused across point chunks).
+int pack_b_rm(const float *B, int64_t ldb, int k, int ncols, Scratch &img, cudaStream_t st) {
+    img.alloc((size_t)fc_gemm_image_bytes(ncols, (int)ceil_div(k, 32)), st);
+    if (!img.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (GEMM image)");
+    const int src = 0;
+    return fc_gemm_pack_b(1, ncols, 1, &src, &k, B, ldb, img.as<uint8_t>(), st);
+}
+int tc_gemm(const float *A, int64_t lda, int k, int64_t m, const Scratch &img, int ncols, float *out, int64_t ldo,
+            cudaStream_t st) {
+    const float *a = A;
+    float *o = out;
+    int64_t la = lda, lo = ldo;
+    int kk = k, c0 = 0, c1 = ncols;
+    return fc_gemm_rows(m, 1, &a, &la, &kk, nullptr, 0, img.as<uint8_t>(), ncols, nullptr, 1, &o, &lo, &c0, &c1,
+                        nullptr, 0, st);
+}
+__global__ void add_into_kernel(int64_t count, const float *__restrict__ src, float *__restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] += src[i];
 }
 
 bool gemm_route_enabled(int gc) {
@@ -672,27 +684,20 @@ template <int DP, bool REV>
 int launch_gemm_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, const float *rows, const float *loc,
                        const int32_t *nbr, Csr csr, const float *w, float *out, cudaStream_t st) {
     if (!gemm_route_enabled(gc) || (reinterpret_cast<uintptr_t>(rows) % 16) != 0) return FC_ERR_UNSUPPORTED;
-    cublasHandle_t h = cublas_handle();
-    if (!h) return FC_ERR_UNSUPPORTED;
     const int ktot = gc * (DP + 1);
     const int64_t chunk = gemm_chunk(total, ktot);
-    float *X = (float *)scratch_alloc(sizeof(float) * chunk * ktot, st);
-    if (!X) return set_error(FC_ERR_CUDA, "scratch allocation failed");
-    cublasSetStream(h, st);
-    prof_begin(REV ? "gemm_reverse" : "gemm_forward", st);
+    Scratch Xb(sizeof(float) * chunk * ktot, st), img;
+    if (!Xb.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+    float *X = Xb.as<float>();
+    if (int rc = pack_b_rm(w, cout, ktot, cout, img, st)) return rc;
     int rc = FC_OK;
     for (int64_t p0 = 0; p0 < total && rc == FC_OK; p0 += chunk) {
         const int64_t m = std::min(chunk, total - p0);
         const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)num_sms() * 8);
         moments_rows_kernel<DP, REV><<<grid, 256, 0, st>>>(p0, m, n, gc, k, rows, loc, nbr, csr, X);
         count_launch();
-        const float one = 1.f, zero = 0.f;
-        if (cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, cout, (int)m, ktot, &one, w, cout, X, ktot, &zero,
-                        out + p0 * cout, cout) != CUBLAS_STATUS_SUCCESS)
-            rc = set_error(FC_ERR_CUDA, "cublasSgemm failed");
+        rc = tc_gemm(X, ktot, ktot, m, img, cout, out + p0 * cout, cout, st);
     }
-    prof_end(st);
-    scratch_free(X, st);
     if (rc) return rc;
     return check_launch("moments + GEMM");
 }
@@ -703,31 +708,30 @@ template <int DP>
 int launch_gemm_dtheta_dp(int64_t total, int64_t n, int cin, int k, int cout, const float *feat, const float *loc,
                           const int32_t *nbr, const float *g, float *d_theta, float *d_theta_b, cudaStream_t st) {
     if (!gemm_route_enabled(cin) || (reinterpret_cast<uintptr_t>(feat) % 16) != 0) return FC_ERR_UNSUPPORTED;
-    cublasHandle_t h = cublas_handle();
-    if (!h) return FC_ERR_UNSUPPORTED;
     const int ktot = cin * (DP + 1);
     const int64_t chunk = gemm_chunk(total, ktot);
-    float *X = (float *)scratch_alloc(sizeof(float) * chunk * ktot, st);
-    float *P = (float *)scratch_alloc(sizeof(float) * (size_t)cout * ktot, st);
-    if (!X || !P) return set_error(FC_ERR_CUDA, "scratch allocation failed");
-    cublasSetStream(h, st);
-    prof_begin("gemm_dtheta", st);
+    const bool chunked = chunk < total;
+    Scratch Xb(sizeof(float) * chunk * ktot, st), Pb(sizeof(float) * (size_t)cout * ktot * (chunked ? 2 : 1), st);
+    if (!Xb.ok() || !Pb.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+    float *X = Xb.as<float>(), *P = Pb.as<float>(), *Pc = chunked ? P + (size_t)cout * ktot : P;
     int rc = FC_OK;
     for (int64_t p0 = 0; p0 < total && rc == FC_OK; p0 += chunk) {
         const int64_t m = std::min(chunk, total - p0);
         const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)num_sms() * 8);
         moments_rows_kernel<DP, false><<<grid, 256, 0, st>>>(p0, m, n, cin, k, feat, loc, nbr, Csr{nullptr, nullptr}, X);
         count_launch();
-        const float one = 1.f, beta = p0 == 0 ? 0.f : 1.f;
-        // column-major: P_cm (ktot x cout) = X_cm (ktot x m) . G_cm^T (m x cout)
-        if (cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, ktot, cout, (int)m, &one, X, ktot, g + p0 * cout, cout, &beta,
-                        P, ktot) != CUBLAS_STATUS_SUCCESS)
-            rc = set_error(FC_ERR_CUDA, "cublasSgemm failed");
+        // P [cout, ktot] = G^T X (fc_gemm_wgrad: fixed-order partial sums); chunks added in order
+        const float *xo = X;
+        int64_t lx = ktot;
+        int kx = ktot;
+        rc = fc_gemm_wgrad(m, g + p0 * cout, cout, nullptr, 0, cout, 1, &xo, &lx, &kx, p0 == 0 ? P : Pc, nullptr, st);
+        if (rc == FC_OK && p0 > 0) {
+            add_into_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)cout * ktot, 256), 1024), 256, 0, st>>>(
+                (int64_t)cout * ktot, Pc, P);
+            count_launch();
+        }
     }
     if (rc == FC_OK) rc = launch_dtheta_reduce<float>(1, cin, DP, cout, P, d_theta, d_theta_b, st);
-    prof_end(st);
-    scratch_free(X, st);
-    scratch_free(P, st);
     if (rc) return rc;
     return check_launch("moments + GEMM (d_theta)");
 }
@@ -792,44 +796,33 @@ int launch_gemm_rev_dloc_dp(int64_t total, int64_t n, int gc, int k, int cout, c
                             Csr csr, const float *w, float *out, const float *feat, const float *theta,
                             const float *centre, float *dloc, cudaStream_t st) {
     if (!gemm_route_enabled(gc) || (reinterpret_cast<uintptr_t>(rows) % 16) != 0) return FC_ERR_UNSUPPORTED;
-    cublasHandle_t h = cublas_handle();
-    if (!h) return FC_ERR_UNSUPPORTED;
     const int ktot = gc * (DP + 1);
     const int64_t chunk = gemm_chunk(total, ktot + DP * cout);
-    float *X = (float *)scratch_alloc(sizeof(float) * chunk * ktot, st);
-    float *U = (float *)scratch_alloc(sizeof(float) * chunk * DP * cout, st);
-    float *wt = (float *)scratch_alloc(sizeof(float) * (size_t)ktot * cout, st);
-    float *tcat = (float *)scratch_alloc(sizeof(float) * (size_t)gc * DP * cout, st);
-    if (!X || !U || !wt || !tcat) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+    Scratch Xb(sizeof(float) * chunk * ktot, st), Ub(sizeof(float) * chunk * DP * cout, st);
+    Scratch wtb(sizeof(float) * (size_t)ktot * cout, st), tcb(sizeof(float) * (size_t)gc * DP * cout, st);
+    Scratch img_w, img_t;
+    if (!Xb.ok() || !Ub.ok() || !wtb.ok() || !tcb.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+    float *X = Xb.as<float>(), *U = Ub.as<float>(), *wt = wtb.as<float>(), *tcat = tcb.as<float>();
     const unsigned pg = (unsigned)std::min<int64_t>(ceil_div((int64_t)ktot * cout, 256), 4096);
     repack_tmajor_kernel<<<pg, 256, 0, st>>>(gc, DP + 1, cout, w, wt);
     pack_theta_cat_kernel<<<pg, 256, 0, st>>>(gc, cout, DP, theta, tcat);
     count_launch();
     count_launch();
-    cublasSetStream(h, st);
-    prof_begin("gemm_reverse_dloc", st);
+    if (int rc = pack_b_rm(wt, cout, ktot, cout, img_w, st)) return rc;
+    if (int rc = pack_b_rm(tcat, DP * cout, gc, DP * cout, img_t, st)) return rc;
     int rc = FC_OK;
     for (int64_t p0 = 0; p0 < total && rc == FC_OK; p0 += chunk) {
         const int64_t m = std::min(chunk, total - p0);
         const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)num_sms() * 8);
         moments_rows_kernel<DP, true, true><<<grid, 256, 0, st>>>(p0, m, n, gc, k, rows, loc, nullptr, csr, X);
         count_launch();
-        const float one = 1.f, zero = 0.f;
-        if (cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, cout, (int)m, ktot, &one, wt, cout, X, ktot, &zero,
-                        out + p0 * cout, cout) != CUBLAS_STATUS_SUCCESS ||
-            cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, DP * cout, (int)m, gc, &one, tcat, DP * cout, X + DP * gc, ktot,
-                        &zero, U, DP * cout) != CUBLAS_STATUS_SUCCESS) {
-            rc = set_error(FC_ERR_CUDA, "cublasSgemm failed");
-            break;
-        }
+        rc = tc_gemm(X, ktot, ktot, m, img_w, cout, out + p0 * cout, cout, st);
+        // U = Yb . [theta_0 .. theta_{d-1}]: the bias-moment columns of X as the operand
+        if (rc == FC_OK) rc = tc_gemm(X + DP * gc, ktot, gc, m, img_t, DP * cout, U, DP * cout, st);
+        if (rc) break;
         dloc_nbr_kernel<DP><<<grid, 256, 0, st>>>(p0, m, cout, feat, U, centre, dloc);
         count_launch();
     }
-    prof_end(st);
-    scratch_free(X, st);
-    scratch_free(U, st);
-    scratch_free(wt, st);
-    scratch_free(tcat, st);
     if (rc) return rc;
     return check_launch("moments + GEMM (reverse, d_loc)");
 }
@@ -874,34 +867,24 @@ int launch_gemm_centre_dp(int64_t total, int64_t n, int cin, int k, int cout, co
         const char *e = getenv("FC_NO_GEMM");
         return e && e[0] == '1';
     }();
-    if (off || cout < 32) return FC_ERR_UNSUPPORTED;
-    cublasHandle_t h = cublas_handle();
-    if (!h) return FC_ERR_UNSUPPORTED;
+    if (off || cout < 32 || (reinterpret_cast<uintptr_t>(g) % 16) != 0 || cout % 4 != 0) return FC_ERR_UNSUPPORTED;
     const int64_t chunk = gemm_chunk(total, DP * cin);
-    float *Z = (float *)scratch_alloc(sizeof(float) * chunk * DP * cin, st);
-    float *tcat = (float *)scratch_alloc(sizeof(float) * (size_t)cout * DP * cin, st);
-    if (!Z || !tcat) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+    Scratch Zb(sizeof(float) * chunk * DP * cin, st), tcb(sizeof(float) * (size_t)cout * DP * cin, st), img;
+    if (!Zb.ok() || !tcb.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed");
+    float *Z = Zb.as<float>(), *tcat = tcb.as<float>();
     const unsigned pg = (unsigned)std::min<int64_t>(ceil_div((int64_t)cout * cin * DP, 256), 4096);
     pack_theta_cat_kernel<<<pg, 256, 0, st>>>(cout, cin, DP, theta, tcat);  // tcat[c'][t*cin + c]
     count_launch();
-    cublasSetStream(h, st);
-    prof_begin("gemm_centre", st);
+    if (int rc = pack_b_rm(tcat, DP * cin, cout, DP * cin, img, st)) return rc;
     int rc = FC_OK;
     for (int64_t p0 = 0; p0 < total && rc == FC_OK; p0 += chunk) {
         const int64_t m = std::min(chunk, total - p0);
-        const float one = 1.f, zero = 0.f;
-        if (cublasSgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, DP * cin, (int)m, cout, &one, tcat, DP * cin, g + p0 * cout, cout,
-                        &zero, Z, DP * cin) != CUBLAS_STATUS_SUCCESS) {
-            rc = set_error(FC_ERR_CUDA, "cublasSgemm failed");
-            break;
-        }
+        rc = tc_gemm(g + p0 * cout, cout, cout, m, img, DP * cin, Z, DP * cin, st);  // Z = G . tcat
+        if (rc) break;
         const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)num_sms() * 8);
         centre_dot_kernel<DP><<<grid, 256, 0, st>>>(p0, m, n, cin, k, feat, nbr, Z, centre);
         count_launch();
     }
-    prof_end(st);
-    scratch_free(Z, st);
-    scratch_free(tcat, st);
     if (rc) return rc;
     return check_launch("GEMM (d_loc centre)");
 }

@@ -20,6 +20,6 @@ for f in *.cu; do
 done
 wait
 /usr/local/cuda/bin/nvcc -ccbin /usr/bin/g++ -shared -o $OUT *.o -gencode arch=compute_100a,code=sm_100a \
-  -lcudart -lcuda -lcublas -Xlinker -rpath=/usr/local/cuda/lib64
+  -lcudart -lcuda -Xlinker -rpath=/usr/local/cuda/lib64
 rm -rf $W
 echo "built $OUT"
