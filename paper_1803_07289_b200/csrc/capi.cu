@@ -226,6 +226,8 @@ int fc_conv_forward_rows(int64_t n, int c_in, int d, int k, int c_out, const voi
     if (!(c_in == 64 && c_out == 64 && d == 3 && k == 8))
         return set_error(FC_ERR_UNSUPPORTED, "row-list forward covers c_in = c_out = 64, d = 3, k = 8");
     if (nrows < 0 || nrows > n) return set_error(FC_ERR_SHAPE, "nrows %lld outside [0, %lld]", (long long)nrows, (long long)n);
+    if (nrows == 0) return FC_OK;  // (an empty list's pointer may be null, which means "every row" below)
+    if (!rows) return set_error(FC_ERR_CONFIG, "row list is null");
     return fc::tc_fast_forward(true, n, n, (const float *)features, (const float *)locations, neighbors, (const float *)theta,
                            (const float *)theta_b, (float *)out, ST(stream), rows, nrows);
 }

@@ -545,11 +545,10 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
             mma_commit(mma_done + h);
             if (h == 1) mma_commit(acc_full + b);
         };
-        auto epilogue = [&](int i) {
+        auto epilogue = [&](int i, int64_t p) {  // p: this thread's row of tile i (from produce)
             const int b = i & 1;
             mbar_wait_sleep(acc_full + b, (uint32_t)((i >> 1) & 1));
             tc_fence_after();
-            const int64_t p = row_of(blockIdx.x + (int64_t)i * gridDim.x, t);
             const float s0 = exp2i(rs[(b * 2 + 0) * kTile + t]) * binv;
             const float s1 = exp2i(rs[(b * 2 + 1) * kTile + t]) * binv;
             const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(b * 256);
@@ -579,8 +578,7 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
             __syncwarp();
             if (lane == 0) mbar_arrive(acc_free + b);
         };
-        auto produce = [&](int i) {  // entries of tile i (one thread per row)
-            const int64_t p = row_of(blockIdx.x + (int64_t)i * gridDim.x, t);
+        auto produce = [&](int i, int64_t p) {  // entries of tile i (one thread per row p)
             const bool v = p < a.total;
             int4 n0 = make_int4(0, 0, 0, 0), n1 = n0;
             int32_t base = 0;
@@ -611,20 +609,37 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
             __syncwarp();
             if (lane == 0) mbar_arrive(e_full + st);
         };
-        if (T > 0) produce(0);
+        // row ids: in row-list mode a global load, issued two tiles ahead of its producer and
+        // kept in registers for the epilogue (a dependent load there would sit on the path
+        // that frees the accumulator; measured 2x slower forward before this)
+        auto row_id = [&](int i) -> int64_t { return i < T ? row_of(blockIdx.x + (int64_t)i * gridDim.x, t) : 0; };
+        int64_t pp = row_id(0), pp2 = row_id(1), pe_prev = 0, pe_cur = 0, pe_next = 0;
+        if (T > 0) {
+            produce(0, pp);
+            pe_cur = pp;
+            pp = pp2;
+            pp2 = row_id(2);
+        }
         for (int i = 0; i < T; ++i) {
-            if (i + 1 < T) produce(i + 1);
+            if (i + 1 < T) {
+                produce(i + 1, pp);
+                pe_next = pp;
+                pp = pp2;
+                pp2 = row_id(i + 3);
+            }
             if (warp == wCtlWarp0) {
                 if (lane == 0) issue_mma(i, 0);
                 __syncwarp();
             }
-            if (i >= 1) epilogue(i - 1);
+            if (i >= 1) epilogue(i - 1, pe_prev);
             if (warp == wCtlWarp0) {
                 if (lane == 0) issue_mma(i, 1);
                 __syncwarp();
             }
+            pe_prev = pe_cur;
+            pe_cur = pe_next;
         }
-        if (T > 0) epilogue(T - 1);
+        if (T > 0) epilogue(T - 1, pe_prev);
     } else {
         // ------------------------------------------------------------ gather warps
         // warp w: rows 8w .. 8w+7 of every tile, channel half h = 0 then 1.  Lane (pt, cl):

@@ -1,11 +1,14 @@
-"""C4 (7M-point cloud, point-chunk sharded with halos) measured on ONE B200 by emulation: for
-world = 2, 4, 8 the halo plans are built (parallel.HaloPlan), and every shard's local
-flex-conv forward and forward+backward run on the GPU on its [owned | halo] buffers, timed
-with CUDA events.  Reports the halo fraction, the halo bytes each rank receives per layer,
-and the slowest shard's compute time: the compute part of a strong-scaling run (the NVLink
-halo exchange itself needs N GPUs; its bytes are given so its time can be bounded).
+"""C4 (one 7M-point cloud, point-chunk sharded with halos) on ONE B200 by emulation: W ranks
+(torchrun, gloo, all on cuda:0) run the product path -- parallel.ShardedCloud.build (sharded
+exact kNN with the position ghost shell, device-resident halo plan) and ShardedFlexConv --
+and then, one rank at a time (the others wait at a barrier, so each shard has the GPU to
+itself), every rank times its own shard's kernels with CUDA events: the forward's interior
+rows + boundary rows (fc_conv_forward_rows) and the backward, on its [owned | halo] buffers.
+The halo exchange itself needs W GPUs (NVLink); its bytes are reported so its time can be
+bounded.
 
-  python scripts/shard_emulation.py [--n 7000000] > profiles/<round>_shard_emulation.json
+  python -m torch.distributed.run --nproc-per-node W --master-addr 127.0.0.1 \\
+      scripts/shard_emulation.py [--n 7000000]          (rank 0 prints one JSON object)
 """
 
 from __future__ import annotations
@@ -18,6 +21,7 @@ import sys
 import time
 
 import torch
+import torch.distributed as dist
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -45,56 +49,63 @@ def main():
     ap.add_argument("--k", type=int, default=8)
     ap.add_argument("--c", type=int, default=64)
     args = ap.parse_args()
-    n, k, c = args.n, args.k, args.c
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
+    n, k, c = args.n, args.k, args.c
     g = torch.Generator(device=dev)
     g.manual_seed(1234)
     pos = (torch.floor(torch.rand(n, 3, generator=g, device=dev, dtype=torch.float64) * 2 ** 24) / 2 ** 24).float()
     pos = pos[_ops.spatial_order(pos).long()].contiguous()
-    feat = torch.randn(n, c, generator=g, device=dev)
-    up = torch.randn(n, c, generator=g, device=dev)
+    lo, hi = parallel.shard_range(n, world, rank)
+    feat = torch.randn(n, c, generator=g, device=dev)[lo:hi].contiguous()
+    up = torch.randn(n, c, generator=g, device=dev)[lo:hi].contiguous()
     th = 0.1 * torch.randn(c, c, 3, generator=g, device=dev)
     tb = 0.1 * torch.randn(c, c, generator=g, device=dev)
-    nbr = _ops.knn(pos, 1, n, k)
-    csr = _ops.csr_build(nbr, 1, n)
-    res = {"n": n, "k": k, "channels": f"{c}->{c}", "device": torch.cuda.get_device_name(0),
-           "timing": "CUDA events, median of 5, per shard on its [owned | halo] buffers"}
-    res["world_1"] = {"fwd_ms": round(timed(lambda: _ops.conv_forward(feat, pos, nbr, th, tb, 1, n)), 4),
-                      "fwd_bwd_ms": round(timed(lambda: (_ops.conv_forward(feat, pos, nbr, th, tb, 1, n),
-                                                         _ops.conv_backward(up, feat, pos, nbr, csr, th, tb, 1, n))), 4)}
-    nbr_h = nbr.cpu().numpy()
-    for world in (2, 4, 8):
-        t0 = time.perf_counter()
-        plans = parallel.HaloPlan.build_all(nbr_h, world)
-        plan_s = time.perf_counter() - t0
-        shards = []
-        for p in plans:
-            sel = torch.cat([torch.arange(p.lo, p.hi, device=dev), torch.from_numpy(p.halo).to(dev)])
-            f_l, x_l, g_l = feat[sel].contiguous(), pos[sel].contiguous(), up[sel].contiguous()
-            g_l[p.n_own:] = 0
-            nb_l = torch.from_numpy(p.local_nbr).to(dev, torch.int32)
-            m = p.n_local
-            csr_l = _ops.csr_build(nb_l, 1, m)
-            fwd = timed(lambda: _ops.conv_forward(f_l, x_l, nb_l, th, tb, 1, m))
-            both = timed(lambda: (_ops.conv_forward(f_l, x_l, nb_l, th, tb, 1, m),
-                                  _ops.conv_backward(g_l, f_l, x_l, nb_l, csr_l, th, tb, 1, m)))
-            shards.append({"owned": p.n_own, "halo": int(len(p.halo)),
-                           "halo_frac": round(len(p.halo) / p.n_own, 4),
-                           "halo_recv_bytes_fwd": int(len(p.halo)) * (4 * c + 12),
-                           "fwd_ms": round(fwd, 4), "fwd_bwd_ms": round(both, 4)})
-            del f_l, x_l, g_l, nb_l, csr_l
-        torch.cuda.empty_cache()
+    pos = pos[lo:hi].contiguous()
+    torch.cuda.empty_cache()
+    comm = parallel.Comm(device=dev)
+    dist.barrier()
+    t0 = time.perf_counter()
+    cloud = parallel.ShardedCloud.build(pos, k, comm)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    f_l, g_l = cloud.local_buffer(feat), cloud.local_buffer(up)
+    cloud.fill_halo(f_l)
+    x_l = cloud.positions
+    out = torch.empty(cloud.n_local, c, device=dev)
+    stats = None
+    for r in range(world):
+        dist.barrier()
+        if r == rank:
+            fwd = timed(lambda: (_ops.conv_forward_rows(f_l, x_l, cloud.table, th, tb, cloud.interior_rows, out),
+                                 _ops.conv_forward_rows(f_l, x_l, cloud.table, th, tb, cloud.boundary_rows, out)))
+            bwd = timed(lambda: _ops.conv_backward(g_l, f_l, x_l, cloud.table, cloud.csr, th, tb, 1, cloud.n_local,
+                                                   need=(True, True, True, True)))
+            n_halo = cloud.n_local - cloud.n_own
+            stats = [float(cloud.n_own), float(n_halo), float(cloud.n_ghost), float(cloud.interior_rows.numel()),
+                     fwd, bwd, build_s, float(n_halo * (4 * c))]
+        torch.cuda.synchronize()
+    rows = [None] * world
+    dist.all_gather_object(rows, stats)
+    if rank == 0:
+        shards = [{"owned": int(s[0]), "halo": int(s[1]), "halo_frac": round(s[1] / s[0], 4),
+                   "ghost_frac": round(s[2] / s[0], 4), "interior_frac": round(s[3] / s[0], 4),
+                   "fwd_ms": round(s[4], 4), "bwd_ms": round(s[5], 4), "fwd_bwd_ms": round(s[4] + s[5], 4),
+                   "build_s": round(s[6], 2), "halo_recv_MB_fwd": round(s[7] / 1e6, 2)} for s in rows]
         worst = max(shards, key=lambda s: s["fwd_bwd_ms"])
-        res[f"world_{world}"] = {
-            "plan_build_s": round(plan_s, 2),
-            "max_halo_frac": max(s["halo_frac"] for s in shards),
-            "max_halo_recv_MB_fwd": round(max(s["halo_recv_bytes_fwd"] for s in shards) / 1e6, 2),
-            "slowest_shard_fwd_ms": max(s["fwd_ms"] for s in shards),
-            "slowest_shard_fwd_bwd_ms": worst["fwd_bwd_ms"],
-            "compute_speedup_fwd_bwd": round(res["world_1"]["fwd_bwd_ms"] / worst["fwd_bwd_ms"], 2),
-            "shards": shards,
-        }
-    print(json.dumps(res, indent=1))
+        print(json.dumps({"n": n, "k": k, "channels": f"{c}->{c}", "world": world,
+                          "device": torch.cuda.get_device_name(0),
+                          "timing": "each shard alone on the GPU (the others wait at a barrier), CUDA events, "
+                                    "median of 5; forward = interior rows + boundary rows (fc_conv_forward_rows)",
+                          "slowest_shard_fwd_ms": max(s["fwd_ms"] for s in shards),
+                          "slowest_shard_fwd_bwd_ms": worst["fwd_bwd_ms"],
+                          "max_halo_frac": max(s["halo_frac"] for s in shards),
+                          "max_ghost_frac": max(s["ghost_frac"] for s in shards),
+                          "sharded_knn_and_plan_s_max": max(s["build_s"] for s in shards),
+                          "shards": shards}))
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -250,4 +250,6 @@ def test_forward_rows_subset_equals_full_forward():
     assert torch.equal(out[a.long()], full[a.long()])
     _ops.conv_forward_rows(feat, pos, nbr, th, tb, b, out)
     assert torch.equal(out, full)
+    out.fill_(float("nan"))
     _ops.conv_forward_rows(feat, pos, nbr, th, tb, a[:0], out)  # empty list: no work
+    assert torch.isnan(out).all()
