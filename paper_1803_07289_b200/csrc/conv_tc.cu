@@ -1567,6 +1567,68 @@ int tc_reverse_gmc(int mode, int64_t total, int64_t n, int gc, int d, int k, int
 // location gradient's two roles accumulate over all block pairs.  The gathers are repeated
 // once per output block -- the price of keeping the moments on chip instead of writing
 // [points, 4 C] moment rows to HBM for a library GEMM.
+// ---- small clouds: the blocked passes run CONCURRENTLY on per-device side streams (each
+// pass is one latency-bound wave on tiles <= a few dozen SMs, e.g. C2's 8 K points are 64
+// tiles), every pass into its own buffer, then combined on the caller's stream in the same
+// order as the sequential accumulation (identical results; fork / join by events, so a CUDA
+// graph capture of the caller's stream includes them).
+struct ForkJoin {
+    cudaStream_t main;
+    int n = 0;
+    bool on = false;
+    cudaStream_t s[4];
+    cudaEvent_t fork_ev, join_ev[4];
+    ForkJoin(cudaStream_t m, int jobs, bool enable) : main(m), n(jobs), on(enable && jobs > 1 && jobs <= 4) {
+        for (int j = 0; j < 4; ++j) s[j] = m;
+        if (!on) return;
+        static cudaStream_t aux[64][4];
+        static cudaEvent_t evs[64][5];
+        static uint64_t made = 0;
+        const int dev = current_device() & 63;
+        if (first_use_on_device(made)) {
+            for (int j = 0; j < 4; ++j) cudaStreamCreateWithFlags(&aux[dev][j], cudaStreamNonBlocking);
+            for (int j = 0; j < 5; ++j) cudaEventCreateWithFlags(&evs[dev][j], cudaEventDisableTiming);
+        }
+        fork_ev = evs[dev][4];
+        cudaEventRecord(fork_ev, m);
+        for (int j = 0; j < n; ++j) {
+            s[j] = aux[dev][j];
+            join_ev[j] = evs[dev][j];
+            cudaStreamWaitEvent(s[j], fork_ev, 0);
+        }
+    }
+    cudaStream_t operator[](int j) const { return s[j]; }
+    void join() {
+        if (!on) return;
+        for (int j = 0; j < n; ++j) {
+            cudaEventRecord(join_ev[j], s[j]);
+            cudaStreamWaitEvent(main, join_ev[j], 0);
+        }
+    }
+};
+static bool concurrent_passes(int64_t total, int passes) {
+    static int off = -1;
+    if (off < 0) {
+        const char *e = getenv("FC_NO_CONCURRENT");
+        off = (e && e[0] == '1') ? 1 : 0;
+    }
+    return !off && passes > 1 && passes <= 4 && ceil_div(total, kTcM) * passes <= 2 * num_sms();
+}
+// dst[p, 0:w] (row stride ldd) += src[p, 0:w] (row stride lds), p < rows
+__global__ void add_rows_kernel(int64_t rows, int w, float *__restrict__ dst, int64_t ldd, const float *__restrict__ src,
+                                int64_t lds) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * w; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = e / w;
+        const int c = (int)(e - p * w);
+        dst[p * ldd + c] += src[p * lds + c];
+    }
+}
+static void add_rows(int64_t rows, int w, float *dst, int64_t ldd, const float *src, int64_t lds, cudaStream_t st) {
+    add_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows * w, 256), 4 * num_sms()), 256, 0, st>>>(rows, w, dst,
+                                                                                                          ldd, src, lds);
+    count_launch();
+}
+
 // output channels per pass of the channel-blocked engines: all of them up to 256
 static int blocked_out_block(int c) {
     if (c <= 256) return c % 64 == 0 && c != 192 ? c : 64;
@@ -1586,8 +1648,17 @@ int tc_blocked_forward(int mode, int64_t total, int64_t n, int c_in, int k, int 
     // output block
     const int ob = blocked_out_block(c_out);
     const int gb = ob > 64 ? 32 : 64;  // 64-channel gathers where the output block is 64 wide
-    for (int o0 = 0; o0 < c_out; o0 += ob) {
-        for (int i0 = 0; i0 < c_in; i0 += gb) {
+    const int nin = (int)ceil_div(c_in, gb), nout = (int)ceil_div(c_out, ob);
+    const bool conc = nout == 1 && concurrent_passes(total, nin);
+    Scratch tmp;
+    if (conc) {  // passes 1.. write [total, ob] partials, added to out in pass order afterwards
+        tmp.alloc(sizeof(float) * (size_t)(nin - 1) * total * ob, st);
+        if (!tmp.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (blocked forward)");
+    }
+    ForkJoin fj(st, nin, conc);
+    int rc = FC_OK;
+    for (int o0 = 0; o0 < c_out && rc == FC_OK; o0 += ob) {
+        for (int i0 = 0, b = 0; i0 < c_in; i0 += gb, ++b) {
             TcArgs a{};
             a.total = total;
             a.n = n;
@@ -1596,16 +1667,20 @@ int tc_blocked_forward(int mode, int64_t total, int64_t n, int c_in, int k, int 
             a.ld_rows = c_in;
             a.loc = loc;
             a.nbr = nbr;
-            a.out = out + o0;
-            a.ld_out = c_out;
-            a.acc = i0 > 0;
+            a.out = (conc && b > 0) ? tmp.as<float>() + (size_t)(b - 1) * total * ob : out + o0;
+            a.ld_out = (conc && b > 0) ? ob : c_out;
+            a.acc = !conc && i0 > 0;
             const float *th = theta + ((int64_t)o0 * c_in + i0) * 3, *tb = theta_b + (int64_t)o0 * c_in + i0;
-            const int rc = mode == FC_MODE_TC_BF16 ? dispatch_tc<false, false>(gb, ob, a, gb, ob, th, tb, st, c_in)
-                                                   : dispatch_tc<true, false>(gb, ob, a, gb, ob, th, tb, st, c_in);
-            if (rc) return rc;
+            const cudaStream_t sj = conc ? fj[b] : st;
+            rc = mode == FC_MODE_TC_BF16 ? dispatch_tc<false, false>(gb, ob, a, gb, ob, th, tb, sj, c_in)
+                                         : dispatch_tc<true, false>(gb, ob, a, gb, ob, th, tb, sj, c_in);
+            if (rc) break;
         }
     }
-    return FC_OK;
+    fj.join();
+    if (rc) return rc;
+    for (int b = 1; conc && b < nin; ++b) add_rows(total, ob, out, c_out, tmp.as<float>() + (size_t)(b - 1) * total * ob, ob, st);
+    return check_launch("blocked forward");
 }
 
 // Reverse pass over blocks: out [total, c_in] = sum over gathered c' blocks of the block
@@ -1619,8 +1694,24 @@ static int tc_blocked_reverse(int mode, int64_t total, int64_t n, int c_in, int 
     // epilogue, whose U accumulators need 4x the columns)
     const int ob = dloc ? 64 : blocked_out_block(c_in);
     const int gb = ob > 64 ? 32 : 64;
-    for (int i0 = 0; i0 < c_in; i0 += ob) {
-        for (int j0 = 0; j0 < c_out; j0 += gb) {
+    const int nj = (int)ceil_div(c_out, gb), ni = (int)ceil_div(c_in, ob);
+    const bool conc = ni == 1 && concurrent_passes(total, nj);
+    Scratch tmp, tdl, zero3;
+    if (conc) {  // passes 1.. write their d_features part and (-) location term to side buffers
+        tmp.alloc(sizeof(float) * (size_t)(nj - 1) * total * ob, st);
+        if (dloc) {
+            tdl.alloc(sizeof(float) * (size_t)(nj - 1) * total * 3, st);
+            zero3.alloc(sizeof(float) * (size_t)total * 3, st);
+        }
+        if (!tmp.ok() || (dloc && (!tdl.ok() || !zero3.ok())))
+            return set_error(FC_ERR_CUDA, "scratch allocation failed (blocked reverse)");
+        if (dloc) cudaMemsetAsync(zero3.p, 0, sizeof(float) * total * 3, st);
+    }
+    ForkJoin fj(st, nj, conc);
+    int rc = FC_OK;
+    for (int i0 = 0; i0 < c_in && rc == FC_OK; i0 += ob) {
+        for (int j0 = 0, b = 0; j0 < c_out; j0 += gb, ++b) {
+            const bool side = conc && b > 0;
             TcArgs a{};
             a.total = total;
             a.n = n;
@@ -1629,23 +1720,31 @@ static int tc_blocked_reverse(int mode, int64_t total, int64_t n, int c_in, int 
             a.ld_rows = c_out;
             a.loc = loc;
             a.csr = csr;
-            a.out = out + i0;
-            a.ld_out = c_in;
-            a.acc = j0 > 0;
+            a.out = side ? tmp.as<float>() + (size_t)(b - 1) * total * ob : out + i0;
+            a.ld_out = side ? ob : c_in;
+            a.acc = !conc && j0 > 0;
             if (dloc) {
                 a.feat = feat + i0;
                 a.ld_feat = c_in;
-                a.centre = centre;
-                a.dloc = dloc;
-                a.acc_dloc = (i0 > 0 || j0 > 0);
+                // side passes: dloc_b = 0 - term_b (exact negation), added below: (c - t0) - t1
+                a.centre = side ? zero3.as<float>() : centre;
+                a.dloc = side ? tdl.as<float>() + (size_t)(b - 1) * total * 3 : dloc;
+                a.acc_dloc = !conc && (i0 > 0 || j0 > 0);
             }
             const float *th = theta + ((int64_t)j0 * c_in + i0) * 3, *tb = theta_b + (int64_t)j0 * c_in + i0;
-            const int rc = mode == FC_MODE_TC_BF16 ? dispatch_tc<false, true>(gb, ob, a, ob, gb, th, tb, st, c_in)
-                                                   : dispatch_tc<true, true>(gb, ob, a, ob, gb, th, tb, st, c_in);
-            if (rc) return rc;
+            const cudaStream_t sj = conc ? fj[b] : st;
+            rc = mode == FC_MODE_TC_BF16 ? dispatch_tc<false, true>(gb, ob, a, ob, gb, th, tb, sj, c_in)
+                                         : dispatch_tc<true, true>(gb, ob, a, ob, gb, th, tb, sj, c_in);
+            if (rc) break;
         }
     }
-    return FC_OK;
+    fj.join();
+    if (rc) return rc;
+    for (int b = 1; conc && b < nj; ++b) {
+        add_rows(total, ob, out, c_in, tmp.as<float>() + (size_t)(b - 1) * total * ob, ob, st);
+        if (dloc) add_rows(total, 3, dloc, 3, tdl.as<float>() + (size_t)(b - 1) * total * 3, 3, st);
+    }
+    return check_launch("blocked reverse");
 }
 
 int tc_blocked_deconv(int mode, int64_t total, int64_t n, int c_in, int k, int c_out, const float *x,
@@ -1667,22 +1766,37 @@ int tc_blocked_backward(int mode, int64_t total, int64_t n, int c_in, int k, int
         // without the location gradient, c' tiles of 128 (each 64-channel feature block is
         // gathered once per 128 upstream channels)
         const int jb = (!d_locations && c_out % 128 == 0) ? 128 : 64;
-        for (int j0 = 0; j0 < c_out; j0 += jb) {
-            for (int i0 = 0; i0 < c_in; i0 += 64) {
+        const int npass = (int)(ceil_div(c_out, jb) * ceil_div(c_in, 64));
+        const bool conc = concurrent_passes(total, npass);
+        Scratch cside;  // concurrent passes 1..: their own centre terms, added in pass order below
+        if (conc && d_locations) {
+            cside.alloc(sizeof(float) * (size_t)(npass - 1) * total * 3, st);
+            if (!cside.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (blocked backward)");
+        }
+        ForkJoin fj(st, npass, conc);
+        int rc = FC_OK;
+        int b = 0;
+        for (int j0 = 0; j0 < c_out && rc == FC_OK; j0 += jb) {
+            for (int i0 = 0; i0 < c_in; i0 += 64, ++b) {
                 // the centre term needs every block pair; d_theta blocks are independent
                 const int64_t e0 = (int64_t)j0 * c_in + i0;
                 float *dtp = d_theta ? d_theta + e0 * 3 : nullptr, *dtbp = d_theta_b ? d_theta_b + e0 : nullptr;
-                const int rc =
-                    jb == 128 ? generic_dtheta_block<2>(total, n, k, feat + i0, c_in, loc, nbr, g + j0, c_out,
-                                                        theta + e0 * 3, theta_b + e0, c_in, dtp, dtbp, c_in, nullptr,
-                                                        false, st)
-                              : generic_dtheta_block<1>(total, n, k, feat + i0, c_in, loc, nbr, g + j0, c_out,
-                                                        theta + e0 * 3, theta_b + e0, c_in, dtp, dtbp, c_in,
-                                                        d_locations ? centre_buf.as<float>() : nullptr,
-                                                        j0 > 0 || i0 > 0, st);
-                if (rc) return rc;
+                const cudaStream_t sj = conc ? fj[b] : st;
+                float *cen = !d_locations ? nullptr
+                             : (conc && b > 0) ? cside.as<float>() + (size_t)(b - 1) * total * 3 : centre_buf.as<float>();
+                rc = jb == 128 ? generic_dtheta_block<2>(total, n, k, feat + i0, c_in, loc, nbr, g + j0, c_out,
+                                                         theta + e0 * 3, theta_b + e0, c_in, dtp, dtbp, c_in, nullptr,
+                                                         false, sj)
+                               : generic_dtheta_block<1>(total, n, k, feat + i0, c_in, loc, nbr, g + j0, c_out,
+                                                         theta + e0 * 3, theta_b + e0, c_in, dtp, dtbp, c_in, cen,
+                                                         !conc && (j0 > 0 || i0 > 0), sj);
+                if (rc) break;
             }
         }
+        fj.join();
+        if (rc) return rc;
+        for (int q = 1; conc && d_locations && q < npass; ++q)
+            add_rows(total, 3, centre_buf.as<float>(), 3, cside.as<float>() + (size_t)(q - 1) * total * 3, 3, st);
     }
     if (d_features || d_locations) {
         Scratch df_buf;

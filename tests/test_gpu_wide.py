@@ -8,6 +8,8 @@ fp64 backward / deconv 1e-12 relative; fp32 forward / deconv / d_features allclo
 fp32 N-long reductions (d_theta, d_theta_b, d_locations) with the stated floor + norm 1e-5.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -159,3 +161,23 @@ def test_wide_fp32_default_route_is_hand_written_tcgen05(fc, shape):
     assert not library, library
     assert any("tc_gmc_kernel" in k for k in names), names
     assert any("tc_dtheta_kernel" in k for k in names), names
+
+
+def test_concurrent_block_passes_bitwise_equal_sequential(tmp_path):
+    """Small clouds run the channel-blocked passes concurrently on side streams, each into its
+    own buffer, combined in the sequential accumulation order: bitwise the sequential result
+    (C2 shape: conv forward, backward with d_locations, flex_deconv)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = os.path.join(root, "scripts", "concurrent_passes_check.py")
+    outs = []
+    for flag in ("0", "1"):
+        f = tmp_path / f"c{flag}.npz"
+        env = dict(os.environ, FC_NO_CONCURRENT=flag)
+        subprocess.run([sys.executable, script, str(f)], check=True, cwd=root, env=env)
+        outs.append(np.load(f))
+    a, b = outs
+    for key in a.files:
+        assert np.array_equal(a[key], b[key]), key
