@@ -59,8 +59,8 @@ struct DtL {
     static constexpr int BZ_OFF = XB_OFF + 2 * 2 * XB; // [hi K-blocks 0..2][lo K-blocks 0..2]
     static constexpr int E_STAGE = dK * kTile * 16;
     static constexpr int E_OFF = BZ_OFF + 2 * 3 * BZ;
-    static constexpr int RS_OFF = E_OFF + 2 * E_STAGE;  // int8 [2 buf][128]
-    static constexpr int BAR_OFF = RS_OFF + 2 * kTile;
+    static constexpr int RS_OFF = E_OFF + 2 * E_STAGE;  // int8 [3 buf][128] (by tile % 3)
+    static constexpr int BAR_OFF = RS_OFF + 3 * kTile;
     static constexpr int SMEM = BAR_OFF + 128;
     static constexpr int SMEM_ALLOC = SMEM + 1024;
     static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
                 DT_CLK(1, mbar_wait_sleep(z_done, (uint32_t)(i & 1)));
                 tc_fence_after();
                 pz = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + row;
-                inv = exp2i(rs[(i & 1) * kTile + row]) * binv;
+                inv = exp2i(rs[(i % 3) * kTile + row]) * binv;
                 c0 = c1 = c2 = 0.f;
             }
             const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + 256u + (uint32_t)(8 * s);
@@ -490,7 +490,8 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
                 const int e = scale_exp(mx);
                 if (c == 0 && i >= 2) {  // Xb buffer / rs slot of tile i-2 consumed (Z MMAs done, epilogue read rs)
                     DT_CLK(1, mbar_wait(xb_free + (i & 1), (uint32_t)(((i >> 1) + 1) & 1)));
-                    DT_CLK(1, mbar_wait(z_free + (i & 1), (uint32_t)(((i >> 1) + 1) & 1)));
+                    // (no wait for the Z epilogue of tile i-2: the row scales it reads are
+                    // triple-buffered by tile % 3, and the Xb buffer is released by xb_free)
                 }
                 {
                     uint32_t lo;
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
                     const uint32_t xo = XB0 + (uint32_t)((i & 1) * 2 * L::XB) + sw128_offset(row, cc, kTile);
                     sts32u(xo, hi);
                     sts32u(xo + L::XB, lo);
-                    if (lane == 0) sts8(rs_s + (uint32_t)((i & 1) * kTile + row), e);
+                    if (lane == 0) sts8(rs_s + (uint32_t)((i % 3) * kTile + row), e);
                 }
                 // ---- X row (tf32 hi/lo) and G row into chunk stage u & 1
                 const int u = i * (kTile / dChunk) + c, st = u & 1;

@@ -16,7 +16,7 @@ done
 cd $W/pkg/csrc
 for f in *.cu; do
   /usr/local/cuda/bin/nvcc -ccbin /usr/bin/g++ -c $f -o ${f%.cu}.o -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
-    --expt-relaxed-constexpr -I $W/include -gencode arch=compute_100a,code=sm_100a &
+    --expt-relaxed-constexpr -I $W/include -gencode arch=compute_100a,code=sm_100a ${NVCC_EXTRA:-} &
 done
 wait
 /usr/local/cuda/bin/nvcc -ccbin /usr/bin/g++ -shared -o $OUT *.o -gencode arch=compute_100a,code=sm_100a \
