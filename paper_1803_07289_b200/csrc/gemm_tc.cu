@@ -342,15 +342,18 @@ struct WArgs {
     float *part;      // [nchunk][co][ci + 1]
 };
 // CTA (64 threads): 64 (co) x 64 (ci) outputs over one point chunk; thread: 8 x 8 outputs
-// (4 shared loads per 64 FMAs); 32-point slabs of G and X staged in shared memory.  Partial
-// sums per chunk, reduced in fixed order (deterministic).
+// (4 shared loads per 64 FMAs).  32-point slabs of G, X (and the ReLU mask) arrive by 4-byte
+// cp.async into a double-buffered shared tile, one slab ahead of the FMAs (no registers held
+// across the load latency).  Partial sums per chunk, reduced in fixed order (deterministic).
+template <bool MASKED>
 __global__ void __launch_bounds__(64) wgrad_kernel(WArgs a) {
-    __shared__ __align__(16) float Gs[32][64];
-    __shared__ __align__(16) float Xs[32][64];
+    __shared__ __align__(16) float Gs[2][32][64];
+    __shared__ __align__(16) float Xs[2][32][64];
+    __shared__ __align__(16) float Ms[MASKED ? 2 : 1][MASKED ? 32 : 1][MASKED ? 64 : 4];
     const int tid = threadIdx.x, ty = tid >> 3, tx = tid & 7;
     const int co0 = blockIdx.x * 64, ci0 = blockIdx.y * 64;
     const int64_t p0 = (int64_t)blockIdx.z * a.chunk, p1 = std::min<int64_t>(a.n, p0 + a.chunk);
-    const int gcol = co0 + tid, xcol = ci0 + tid;  // loader: column tid of both slabs
+    const int gcol = co0 + tid, xcol = ci0 + tid;  // loader: column tid of the slabs
     int xq = -1, xk = 0;
     if (xcol < a.ci)
         for (int q = 0; q < a.nops; ++q)
@@ -358,30 +361,49 @@ __global__ void __launch_bounds__(64) wgrad_kernel(WArgs a) {
     const float *xp = xq >= 0 ? a.ops[xq].a + xk : nullptr;
     const int64_t xld = xq >= 0 ? a.ops[xq].lda : 0;
     const bool gval = gcol < a.co;
-    float acc[8][8] = {};
-    for (int64_t pb = p0; pb < p1; pb += 32) {
-        float gv[32], xv[32];
-#pragma unroll
+    const bool ones = xcol == a.ci;  // the bias column
+    constexpr bool masked = MASKED;
+    auto issue = [&](int64_t pb, int buf) {
+#pragma unroll 4
         for (int rr = 0; rr < 32; ++rr) {
             const int64_t p = pb + rr;
             const bool pv = p < p1;
-            gv[rr] = (pv && gval) ? __ldg(a.g + p * a.ldg + gcol) : 0.f;
-            if (a.mask && pv && gval && !(__ldg(a.mask + p * a.mask_ld + gcol) > 0.f)) gv[rr] = 0.f;
-            xv[rr] = pv ? (xp ? __ldg(xp + p * xld) : (xcol == a.ci ? 1.f : 0.f)) : 0.f;
+            const uint32_t gs = smem_u32(&Gs[buf][rr][tid]), xs = smem_u32(&Xs[buf][rr][tid]);
+            cpa4(gs, pv && gval ? a.g + p * a.ldg + gcol : a.g, pv && gval);
+            if (ones)
+                Xs[buf][rr][tid] = pv ? 1.f : 0.f;  // (no async write pending on this slot)
+            else
+                cpa4(xs, xp && pv ? xp + p * xld : a.g, xp != nullptr && pv);
+            if constexpr (MASKED)
+                cpa4(smem_u32(&Ms[buf][rr][tid]), pv && gval ? a.mask + p * a.mask_ld + gcol : a.mask, pv && gval);
         }
-        __syncthreads();
-#pragma unroll
-        for (int rr = 0; rr < 32; ++rr) {
-            Gs[rr][tid] = gv[rr];
-            Xs[rr][tid] = xv[rr];
+        cpa_commit();
+    };
+    float acc[8][8] = {};
+    int buf = 0;
+    if (p0 < p1) issue(p0, 0);
+    for (int64_t pb = p0; pb < p1; pb += 32, buf ^= 1) {
+        if (pb + 32 < p1) {
+            issue(pb + 32, buf ^ 1);
+            cpa_wait<1>();
+        } else {
+            cpa_wait<0>();
         }
         __syncthreads();
 #pragma unroll 4
         for (int rr = 0; rr < 32; ++rr) {
-            const float4 g0 = *reinterpret_cast<const float4 *>(&Gs[rr][8 * ty]);
-            const float4 g1 = *reinterpret_cast<const float4 *>(&Gs[rr][8 * ty + 4]);
-            const float4 x0 = *reinterpret_cast<const float4 *>(&Xs[rr][8 * tx]);
-            const float4 x1 = *reinterpret_cast<const float4 *>(&Xs[rr][8 * tx + 4]);
+            float4 g0 = *reinterpret_cast<const float4 *>(&Gs[buf][rr][8 * ty]);
+            float4 g1 = *reinterpret_cast<const float4 *>(&Gs[buf][rr][8 * ty + 4]);
+            if constexpr (MASKED) {
+                const float4 m0 = *reinterpret_cast<const float4 *>(&Ms[buf][rr][8 * ty]);
+                const float4 m1 = *reinterpret_cast<const float4 *>(&Ms[buf][rr][8 * ty + 4]);
+                g0.x = m0.x > 0.f ? g0.x : 0.f, g0.y = m0.y > 0.f ? g0.y : 0.f, g0.z = m0.z > 0.f ? g0.z : 0.f,
+                g0.w = m0.w > 0.f ? g0.w : 0.f;
+                g1.x = m1.x > 0.f ? g1.x : 0.f, g1.y = m1.y > 0.f ? g1.y : 0.f, g1.z = m1.z > 0.f ? g1.z : 0.f,
+                g1.w = m1.w > 0.f ? g1.w : 0.f;
+            }
+            const float4 x0 = *reinterpret_cast<const float4 *>(&Xs[buf][rr][8 * tx]);
+            const float4 x1 = *reinterpret_cast<const float4 *>(&Xs[buf][rr][8 * tx + 4]);
             const float g8[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
             const float x8[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
@@ -389,6 +411,7 @@ __global__ void __launch_bounds__(64) wgrad_kernel(WArgs a) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(g8[i], x8[j], acc[i][j]);
         }
+        __syncthreads();  // buffer buf is refilled by the next iteration's issue
     }
     const int ldp = a.ci + 1;
     float *out = a.part + (int64_t)blockIdx.z * a.co * ldp;
@@ -522,7 +545,8 @@ extern "C" int fc_gemm_wgrad(int64_t n, const float *g, int64_t ldg, const float
     if (!part.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (gemm_wgrad)");
     a.part = part.as<float>();
     prof_begin("pointwise_wgrad", st);
-    gemm::wgrad_kernel<<<dim3(gx, gy, (unsigned)nchunk), 64, 0, st>>>(a);
+    if (mask) gemm::wgrad_kernel<true><<<dim3(gx, gy, (unsigned)nchunk), 64, 0, st>>>(a);
+    else gemm::wgrad_kernel<false><<<dim3(gx, gy, (unsigned)nchunk), 64, 0, st>>>(a);
     count_launch();
     gemm::wgrad_reduce_kernel<<<(int)std::min<int64_t>(ceil_div((int64_t)co * (ci + 1), 256), 1024), 256, 0, st>>>(
         a.part, (int)nchunk, co, ci, dw, db);
