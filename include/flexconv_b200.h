@@ -226,6 +226,22 @@ int fc_count_nonfinite(int dtype, const void *x, int64_t count, int32_t *bad, vo
 int fc_check_indices(const int32_t *idx, int64_t count, int64_t hi, int32_t *bad,
                      void *stream);
 
+/* flex_deconv backward (gradient of y = A(theta)^T x): upstream gy [B*N, c_in] ->
+ * d_x = A(theta) gy [B*N, c_out] (a flex_conv forward), d_theta / d_theta_b / d_locations =
+ * flex_conv backward with upstream = x and features = gy.  Nullable outputs are skipped.
+ * (The reference has no flex_deconv; this is the adjoint's exact gradient.) */
+int fc_deconv_backward(int dtype, int mode, int64_t batch, int64_t n, int c_in, int d, int k,
+                       int c_out, const void *upstream, const void *x, const void *locations,
+                       const int32_t *neighbors, const int32_t *rev_offsets,
+                       const int32_t *rev_entries, const void *theta, const void *theta_b,
+                       void *d_x, void *d_locations, void *d_theta, void *d_theta_b, void *stream);
+
+/* Workspace (SURVEY.md §8(b) workspace_bytes): every entry point takes its scratch from the
+ * device's stream-ordered memory pool; fc_scratch_peak_bytes() is the high-water mark (bytes)
+ * of that scratch for calls made on this host thread since fc_scratch_peak_reset(). */
+int64_t fc_scratch_peak_bytes(void);
+void fc_scratch_peak_reset(void);
+
 /* ---- pointwise (1x1) convolutions of the U-Net step: replace the
  * reference's pointwise_conv (flexops.py:206-226) and the concatenations that feed it
  * (network.py:94-122, 180-246).  fp32, tcgen05 kind::tf32 with hi/lo split operands.

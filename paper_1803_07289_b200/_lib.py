@@ -43,6 +43,9 @@ SIGNATURES = {
     "fc_conv_forward": [_I, _I, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P],
     "fc_conv_backward": [_I, _I, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "fc_conv_forward_rows": [_I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I64, _P, _P],
+    "fc_deconv_backward": [_I, _I, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "fc_scratch_peak_bytes": [],
+    "fc_scratch_peak_reset": [],
     "fc_deconv_forward": [_I, _I, _I64, _I64, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "fc_csr_build": [_I64, _I64, _I, _P, _P, _P, _P],
     "fc_csr_build_async": [_I64, _I64, _I, _P, _P, _P, _P, _P],
@@ -68,7 +71,8 @@ SIGNATURES = {
 }
 _RESTYPE = {"fc_last_error": ctypes.c_char_p, "fc_launch_count": ctypes.c_uint64, "fc_profile_enable": None,
             "fc_profile_reset": None, "fc_profile_name": ctypes.c_char_p, "fc_profile_ms": ctypes.c_float,
-            "fc_gemm_image_bytes": ctypes.c_int64}
+            "fc_gemm_image_bytes": ctypes.c_int64, "fc_scratch_peak_bytes": ctypes.c_int64,
+            "fc_scratch_peak_reset": None}
 
 _lib = None
 

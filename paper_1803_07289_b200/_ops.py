@@ -115,6 +115,43 @@ def conv_forward(feat, loc, nbr, theta, theta_b, batch, n, mode="auto"):
     return out
 
 
+def deconv_backward(gy, x, loc, nbr, csr, theta, theta_b, batch, n, need=(True, True, True, True), mode="auto"):
+    """Gradient of y = flex_deconv(x): (d_x, d_theta, d_theta_b, d_locations) for upstream gy
+    (fc_deconv_backward); entries not in `need` are None."""
+    gy = _need(gy, "upstream")
+    dt, dev = gy.dtype, gy.device
+    x = _need(x, "x", dt, dev)
+    loc = _need(loc, "locations", dt, dev)
+    nbr = _need(nbr, "neighbors", torch.int32, dev)
+    theta = _need(theta, "theta", dt, dev)
+    theta_b = _need(theta_b, "theta_b", dt, dev)
+    c_out, c_in, d = _conv_shapes(theta, theta_b)
+    k = nbr.shape[-1]
+    _shape(gy, (batch * n, c_in), "upstream")
+    _shape(x, (batch * n, c_out), "x")
+    _shape(loc, (batch * n, d), "locations")
+    _shape(nbr, (batch * n, k), "neighbors")
+    want_dx, want_dth, want_dtb, want_dl = need
+    dx = torch.empty(batch * n, c_out, dtype=dt, device=dev) if want_dx else None
+    dl = torch.empty(batch * n, d, dtype=dt, device=dev) if want_dl else None
+    dth = torch.empty(c_out, c_in, d, dtype=dt, device=dev) if want_dth else None
+    dtb = torch.empty(c_out, c_in, dtype=dt, device=dev) if want_dtb else None
+    off, ent = (csr if csr is not None else (None, None))
+    _call(dev, "fc_deconv_backward", _dtype(gy), _mode(mode), batch, n, c_in, d, k, c_out, _p(gy), _p(x), _p(loc),
+          _p(nbr), _p(off), _p(ent), _p(theta), _p(theta_b), _p(dx), _p(dl), _p(dth), _p(dtb), _stream(gy))
+    return dx, dth, dtb, dl
+
+
+def scratch_peak_bytes(reset: bool = False) -> int:
+    """Peak device scratch (bytes) the library's entry points took on this thread since the
+    last reset (fc_scratch_peak_bytes); reset=True starts a new measurement."""
+    lib = _lib.lib()
+    if reset:
+        lib.fc_scratch_peak_reset()
+        return 0
+    return int(lib.fc_scratch_peak_bytes())
+
+
 def conv_forward_rows_supported(c_in, d, k, c_out, dtype) -> bool:
     return dtype == torch.float32 and (c_in, d, k, c_out) == (64, 3, 8, 64)
 

@@ -4,6 +4,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <unordered_map>
 
 #include "fc_common.cuh"
 
@@ -58,6 +59,14 @@ void prof_end(cudaStream_t st) {
 
 // Stream-ordered scratch from the device's default memory pool (kept resident: the
 // release threshold is raised once so repeated calls do not return memory to the OS).
+// device scratch accounting (this thread): bytes live and the high-water mark since the last
+// fc_scratch_peak_reset() -- the workspace an entry point took from the pool
+static thread_local int64_t g_scratch_live = 0, g_scratch_peak = 0;
+static std::unordered_map<void *, size_t> &scratch_sizes() {
+    static thread_local std::unordered_map<void *, size_t> m;
+    return m;
+}
+
 void *scratch_alloc(size_t bytes, cudaStream_t st) {
     static uint64_t configured = 0;
     if (first_use_on_device(configured)) {
@@ -73,10 +82,19 @@ void *scratch_alloc(size_t bytes, cudaStream_t st) {
         cudaGetLastError();
         return nullptr;
     }
+    scratch_sizes()[p] = bytes;
+    g_scratch_live += (int64_t)bytes;
+    g_scratch_peak = std::max(g_scratch_peak, g_scratch_live);
     return p;
 }
 void scratch_free(void *p, cudaStream_t st) {
-    if (p) cudaFreeAsync(p, st);
+    if (!p) return;
+    auto it = scratch_sizes().find(p);
+    if (it != scratch_sizes().end()) {
+        g_scratch_live -= (int64_t)it->second;
+        scratch_sizes().erase(it);
+    }
+    cudaFreeAsync(p, st);
 }
 
 // conv_simt.cu
@@ -550,6 +568,33 @@ int fc_count_nonfinite(int dtype, const void *x, int64_t count, int32_t *bad, vo
 int fc_check_indices(const int32_t *idx, int64_t count, int64_t hi, int32_t *bad, void *stream) {
     if (count == 0) return FC_OK;
     return launch_check_indices(idx, count, hi, bad, ST(stream));
+}
+
+
+// Workspace query: the peak device scratch (bytes, stream-ordered pool) the
+// entry points called on this thread took since the last reset -- run an op once on the
+// shape of interest after fc_scratch_peak_reset() to size a pool.
+int64_t fc_scratch_peak_bytes(void) { return g_scratch_peak; }
+void fc_scratch_peak_reset(void) { g_scratch_peak = g_scratch_live; }
+
+// flex_deconv backward: y = A(theta)^T x, so with upstream gy = dL/dy:
+//   d_x = A(theta) gy (flex_conv forward of gy), and theta / theta_b / location gradients are
+//   flex_conv's backward with upstream = x and features = gy (<A^T x, gy> = <x, A gy>).
+int fc_deconv_backward(int dtype, int mode, int64_t batch, int64_t n, int c_in, int d, int k, int c_out,
+                       const void *upstream, const void *x, const void *locations, const int32_t *neighbors,
+                       const int32_t *rev_offsets, const int32_t *rev_entries, const void *theta,
+                       const void *theta_b, void *d_x, void *d_locations, void *d_theta, void *d_theta_b,
+                       void *stream) {
+    if (d_x) {
+        if (int rc = fc_conv_forward(dtype, mode, batch, n, c_in, d, k, c_out, upstream, locations, neighbors, theta,
+                                     theta_b, d_x, stream))
+            return rc;
+    }
+    if (d_locations || d_theta || d_theta_b)
+        return fc_conv_backward(dtype, mode, batch, n, c_in, d, k, c_out, x, upstream, locations, neighbors,
+                                rev_offsets, rev_entries, theta, theta_b, nullptr, d_locations, d_theta, d_theta_b,
+                                stream);
+    return FC_OK;
 }
 
 }  // extern "C"

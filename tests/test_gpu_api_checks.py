@@ -172,3 +172,30 @@ def test_knn_and_conv_step_capture_as_one_cuda_graph(fc):
     torch.cuda.synchronize()
     for a, b in zip(eager, captured):
         assert torch.equal(a, b)
+
+
+def test_deconv_backward_entry_point_and_workspace_query(fc):
+    """fc_deconv_backward equals its definition (flex_conv forward of the upstream for d_x,
+    flex_conv backward with upstream = x, features = gy for the parameter / location
+    gradients) bitwise, and the scratch high-water query reports the backward's workspace."""
+    import torch
+
+    from paper_1803_07289_b200 import _ops
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(4)
+    n, k, ci, co = 5000, 8, 64, 64
+    pos = torch.rand(n, 3, device="cuda", generator=g)
+    nbr = _ops.knn(pos, 1, n, k)
+    csr = _ops.csr_build(nbr, 1, n)
+    x = torch.randn(n, co, device="cuda", generator=g)
+    gy = torch.randn(n, ci, device="cuda", generator=g)
+    th = 0.1 * torch.randn(co, ci, 3, device="cuda", generator=g)
+    tb = 0.1 * torch.randn(co, ci, device="cuda", generator=g)
+    _ops.scratch_peak_bytes(reset=True)
+    dx, dth, dtb, dl = _ops.deconv_backward(gy, x, pos, nbr, csr, th, tb, 1, n)
+    assert _ops.scratch_peak_bytes() > 0
+    ref_dx = _ops.conv_forward(gy, pos, nbr, th, tb, 1, n)
+    _, rth, rtb, rdl = _ops.conv_backward(x, gy, pos, nbr, csr, th, tb, 1, n, need=(False, True, True, True))
+    for got, ref in ((dx, ref_dx), (dth, rth), (dtb, rtb), (dl, rdl)):
+        assert torch.equal(got, ref)
