@@ -15,6 +15,7 @@
 // Epilogue: + bias, the result to up to four column ranges (per-operand d_input outputs) and
 // optionally ReLU(result) to a second buffer (the ResBlock's r and relu(r) in one pass).
 #include <cstdio>
+#include <cstdlib>
 
 #include "fast_common.cuh"
 
@@ -29,7 +30,6 @@ using fast::lds128f;
 constexpr int kMaxOps = 4;
 constexpr int kMaxOuts = 4;
 constexpr int kThreads = 256;
-constexpr int kStages = 3;
 constexpr int kTileM = 128;
 constexpr int kA = kTileM * 128;  // one fp32 K-block image: 128 rows x 32 columns (16 KB)
 
@@ -143,7 +143,10 @@ __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %
 // in fp32 registers (round-to-nearest): the tensor pipe's fp32 accumulation truncates, so a
 // long K in one accumulator drifts (~2^-24 per MMA, biased; measured 3.5x the SGEMM error on
 // the U-Net's 387-wide merge GEMM before this change).
-__global__ void __launch_bounds__(kThreads, 1) gemm_rows_kernel(Args a) {
+// kStages: cp.async stages; 3 (1 CTA / SM, TMEM 512) or, for nc <= 64 (2 x 2nc <= 256 TMEM
+// columns), 2 (two CTAs / SM: twice the warps to hide the per-K-block dependency chain)
+template <int kStages>
+__global__ void __launch_bounds__(kThreads, kStages == 2 ? 2 : 1) gemm_rows_kernel(Args a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sb = smem_u32(smem);
@@ -160,7 +163,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_rows_kernel(Args a) {
         mbar_init(dfull + 1, 1);
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc(tmem_holder, 512);
+    constexpr uint32_t kCols = kStages == 3 ? 512 : 256;
+    if (warp == 0) tmem_alloc(tmem_holder, kCols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -324,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_rows_kernel(Args a) {
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        tmem_dealloc(tmem, kCols);
     }
 }
 
@@ -443,6 +447,15 @@ __global__ void wgrad_reduce_kernel(const float *__restrict__ part, int nchunk, 
 
 using namespace fc;
 
+static bool gemm_one_cta() {  // FC_GEMM_ONE_CTA=1: always the 3-stage, one-CTA-per-SM kernel (A/B)
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("FC_GEMM_ONE_CTA");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 extern "C" int64_t fc_gemm_image_bytes(int ncols, int kblocks) { return gemm::image_bytes(ncols, kblocks); }
 
 extern "C" int fc_gemm_pack_b(int transpose, int nrows, int nseg, const int *seg_src, const int *seg_k,
@@ -504,14 +517,20 @@ extern "C" int fc_gemm_rows(int64_t n, int nops, const float *const *a_ptr, cons
     }
     a.relu = relu_out;
     a.relu_ld = relu_ld;
-    const int smem = gemm::kStages * (2 * gemm::kA + 2 * a.nc * 128) + 1024 + 64;  // (1 CTA / SM: TMEM 512)
+    const bool two = a.nc <= 64 && !gemm_one_cta();  // 2 stages, TMEM 256: two CTAs per SM
+    const int stages = two ? 2 : 3;
+    const int smem = stages * (2 * gemm::kA + 2 * a.nc * 128) + 1024 + 64;
     static uint64_t attr = 0;
-    if (first_use_on_device(attr))
-        cudaFuncSetAttribute(gemm::gemm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             gemm::kStages * (2 * gemm::kA + 2 * 128 * 128) + 1024 + 64);
-    const int grid = (int)std::min<int64_t>(ceil_div(n, gemm::kTileM), num_sms());
+    if (first_use_on_device(attr)) {
+        cudaFuncSetAttribute(gemm::gemm_rows_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             3 * (2 * gemm::kA + 2 * 128 * 128) + 1024 + 64);
+        cudaFuncSetAttribute(gemm::gemm_rows_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             2 * (2 * gemm::kA + 2 * 64 * 128) + 1024 + 64);
+    }
+    const int grid = (int)std::min<int64_t>(ceil_div(n, gemm::kTileM), (two ? 2 : 1) * num_sms());
     prof_begin("tc_pointwise", (cudaStream_t)stream);
-    gemm::gemm_rows_kernel<<<grid, gemm::kThreads, smem, (cudaStream_t)stream>>>(a);
+    if (two) gemm::gemm_rows_kernel<2><<<grid, gemm::kThreads, smem, (cudaStream_t)stream>>>(a);
+    else gemm::gemm_rows_kernel<3><<<grid, gemm::kThreads, smem, (cudaStream_t)stream>>>(a);
     prof_end((cudaStream_t)stream);
     count_launch();
     return check_launch("gemm_rows");
