@@ -1581,9 +1581,10 @@ struct ForkJoin {
     ForkJoin(cudaStream_t m, int jobs, bool enable) : main(m), n(jobs), on(enable && jobs > 1 && jobs <= 4) {
         for (int j = 0; j < 4; ++j) s[j] = m;
         if (!on) return;
-        static cudaStream_t aux[64][4];
-        static cudaEvent_t evs[64][5];
-        static uint64_t made = 0;
+        // per host thread and device: two threads forking on one device must not share events
+        static thread_local cudaStream_t aux[64][4];
+        static thread_local cudaEvent_t evs[64][5];
+        static thread_local uint64_t made = 0;
         const int dev = current_device() & 63;
         if (first_use_on_device(made)) {
             for (int j = 0; j < 4; ++j) cudaStreamCreateWithFlags(&aux[dev][j], cudaStreamNonBlocking);
