@@ -548,7 +548,7 @@ void launch_pack_b(bool split, int cin, int cout, const float *theta, const floa
                    int gc, uint8_t *img, float *binv, cudaStream_t st);
 template <typename T>
 int launch_dtheta_reduce(int chunks, int cin, int d, int cout, const T *partial, T *d_theta, T *d_theta_b,
-                         cudaStream_t st, int tmajor = 0);
+                         cudaStream_t st, int tmajor = 0, int ld = 0);
 
 // d_theta / d_theta_b (reduced in fixed order) and the centre role of d_locations for
 // c_in = c_out = 64, k = 8, d = 3; centre may be null when d_locations is not wanted

@@ -278,34 +278,50 @@ __global__ void __launch_bounds__(256)
 // Partial layouts: tmajor = 0: element e = (c' * cin + c) * (d + 1) + t; tmajor = 1 (the
 // tensor-core accumulators' column order): e = c' * cin * (d + 1) + t * cin + c.
 template <typename T>
-__global__ void dtheta_reduce_kernel(int chunks, int cin, int d, int cout,
-                                     const T *__restrict__ partial, T *__restrict__ d_theta,
-                                     T *__restrict__ d_theta_b, int tmajor) {
-    // 8 lanes per output element: lane g adds the chunks of its contiguous block in ascending
-    // order (fp64), the 8 block sums are combined by a fixed xor tree -- a fixed order
-    // (deterministic), with 8x the loads in flight of one thread per element.
-    constexpr int G = 8;
+__global__ void __launch_bounds__(256) dtheta_reduce_kernel(int chunks, int cin, int d, int cout,
+                                                            const T *__restrict__ partial, T *__restrict__ d_theta,
+                                                            T *__restrict__ d_theta_b, int tmajor, int ld) {
+    // a CTA owns 32 consecutive elements; warp w adds the chunks of its contiguous block in
+    // ascending order (fp64, coalesced 32-element rows), the 8 block sums are then added in
+    // warp order -- a fixed order (deterministic) with 8 warps of loads in flight per element
+    constexpr int W = 8;
+    __shared__ double red[W][32];
     const int64_t E = (int64_t)cout * cin * (d + 1);
-    const int g = threadIdx.x % G;
-    const int per = (chunks + G - 1) / G;
-    const int c0 = g * per, c1 = min(chunks, c0 + per);
-    for (int64_t e0 = (int64_t)blockIdx.x * (blockDim.x / G); e0 < E; e0 += (int64_t)gridDim.x * (blockDim.x / G)) {
-        const int64_t e = e0 + threadIdx.x / G;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int per = (chunks + W - 1) / W;
+    const int c0 = min(chunks, w * per), c1 = min(chunks, c0 + per);
+    for (int64_t e0 = (int64_t)blockIdx.x * 32; e0 < E; e0 += (int64_t)gridDim.x * 32) {
+        const int64_t e = e0 + lane;
         double s = 0.0;
-        if (e < E)
-            for (int ch = c0; ch < c1; ++ch) s = __dadd_rn(s, (double)partial[(int64_t)ch * E + e]);
+        if (e < E) {
+            const T *src = partial + e;
+            int ch = c0;
+            for (; ch + 4 <= c1; ch += 4) {
+                const T v0 = src[(int64_t)ch * E], v1 = src[(int64_t)(ch + 1) * E];
+                const T v2 = src[(int64_t)(ch + 2) * E], v3 = src[(int64_t)(ch + 3) * E];
+                s = __dadd_rn(s, (double)v0);
+                s = __dadd_rn(s, (double)v1);
+                s = __dadd_rn(s, (double)v2);
+                s = __dadd_rn(s, (double)v3);
+            }
+            for (; ch < c1; ++ch) s = __dadd_rn(s, (double)src[(int64_t)ch * E]);
+        }
+        red[w][lane] = s;
+        __syncthreads();
+        if (w == 0 && e < E) {
+            double t = red[0][lane];
 #pragma unroll
-        for (int o = 1; o < G; o <<= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
-        if (g == 0 && e < E) {
+            for (int q = 1; q < W; ++q) t = __dadd_rn(t, red[q][lane]);
             const int cp = (int)(e / (cin * (d + 1)));
             const int kk = (int)(e % (cin * (d + 1)));
-            const int c = tmajor ? kk % cin : kk / (d + 1), t = tmajor ? kk / cin : kk % (d + 1);
-            if (t < d) {
-                if (d_theta) d_theta[((int64_t)cp * cin + c) * d + t] = (T)s;
+            const int c = tmajor ? kk % cin : kk / (d + 1), tt = tmajor ? kk / cin : kk % (d + 1);
+            if (tt < d) {
+                if (d_theta) d_theta[((int64_t)cp * ld + c) * d + tt] = (T)t;
             } else if (d_theta_b) {
-                d_theta_b[(int64_t)cp * cin + c] = (T)s;
+                d_theta_b[(int64_t)cp * ld + c] = (T)t;
             }
         }
+        __syncthreads();
     }
 }
 
@@ -498,7 +514,7 @@ static int launch_dtheta_dp(int64_t total, int64_t n, int cin, int k, int cout, 
     dtheta_partial_kernel<T, DP, RPT><<<dim3((unsigned)chunks, (unsigned)slices), 256, smem, st>>>(
         total, n, cin, k, cout, feat, loc, nbr, g, partial, chunk_pts, tile);
     count_launch();
-    dtheta_reduce_kernel<T><<<grid_for(E * 8, 256), 256, 0, st>>>((int)chunks, cin, DP, cout, partial, d_theta, d_theta_b, 0);
+    dtheta_reduce_kernel<T><<<(unsigned)ceil_div(E, 32), 256, 0, st>>>((int)chunks, cin, DP, cout, partial, d_theta, d_theta_b, 0, cin);
     count_launch();
     scratch_free(partial, st);
     return check_launch("dtheta kernels");
@@ -513,15 +529,16 @@ int launch_dtheta(int64_t total, int64_t n, int d, int cin, int k, int cout, con
 
 template <typename T>
 int launch_dtheta_reduce(int chunks, int cin, int d, int cout, const T *partial, T *d_theta, T *d_theta_b,
-                         cudaStream_t st, int tmajor) {
+                         cudaStream_t st, int tmajor, int ld) {
+    // ld: row stride (channels) of d_theta / d_theta_b, 0 = dense (cin); a block of a wider theta
     const int64_t E = (int64_t)cout * cin * (d + 1);
-    dtheta_reduce_kernel<T><<<grid_for(E * 8, 256), 256, 0, st>>>(chunks, cin, d, cout, partial, d_theta, d_theta_b,
-                                                                   tmajor);
+    dtheta_reduce_kernel<T><<<(unsigned)ceil_div(E, 32), 256, 0, st>>>(chunks, cin, d, cout, partial, d_theta, d_theta_b,
+                                                                        tmajor, ld > 0 ? ld : cin);
     count_launch();
     return check_launch("dtheta_reduce_kernel");
 }
-template int launch_dtheta_reduce<float>(int, int, int, int, const float *, float *, float *, cudaStream_t, int);
-template int launch_dtheta_reduce<double>(int, int, int, int, const double *, double *, double *, cudaStream_t, int);
+template int launch_dtheta_reduce<float>(int, int, int, int, const float *, float *, float *, cudaStream_t, int, int);
+template int launch_dtheta_reduce<double>(int, int, int, int, const double *, double *, double *, cudaStream_t, int, int);
 
 #define FC_INST(T)                                                                                   \
     template void launch_pack<T>(int, int, int, const T *, const T *, T *, T *, cudaStream_t);      \

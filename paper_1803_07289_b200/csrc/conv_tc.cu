@@ -21,6 +21,7 @@
 //   BF16: single bf16 MMA per k-step (stated 1e-2 relative tolerance).
 // REVERSE = the same kernel over the reverse neighbourhood (d_features of the backward
 // and flex_deconv): Y_j = sum_{(i,s) in R(j)} (l_i - l_j, 1) (x) g_i, out = Y_j . B_rev.
+#include <vector>
 #include <cstdlib>
 
 #include "fc_common.cuh"
@@ -108,11 +109,11 @@ struct TcLayout {
 //   forward: n = c' (rows = c_out), c = input channel   (GC = c_in)
 //   reverse: n = c  (rows = c_in),  c' = gathered chan  (GC = c_out)
 template <bool SPLIT>
-__global__ void __launch_bounds__(1024)
-    tc_pack_b_kernel(int cin, int cout, int ld_cin, const float *__restrict__ theta, const float *__restrict__ theta_b,
-                     int reverse, int nout, int gc, uint8_t *__restrict__ img, float *__restrict__ binv) {
+__device__ __forceinline__ void pack_b_body(int cin, int cout, int ld_cin, const float *__restrict__ theta,
+                                            const float *__restrict__ theta_b, int reverse, int nout, int gc,
+                                            uint8_t *__restrict__ img, float *__restrict__ binv, int bx, int gx) {
     // (cin, cout): the block of theta packed; ld_cin: theta's full c_in (row stride); theta /
-    // theta_b point at the block's first (c', c)
+    // theta_b point at the block's first (c', c); (bx, gx): this CTA's slice of the image
     __shared__ float red[32];
     float m = 0.f;
     const int ntb = cout * cin;
@@ -132,11 +133,11 @@ __global__ void __launch_bounds__(1024)
     __syncthreads();
     float inv = 1.f, s = 1.f;
     if (SPLIT) s = split_scale(red[0], inv);
-    if (blockIdx.x == 0 && threadIdx.x == 0) binv[0] = inv;
+    if (bx == 0 && threadIdx.x == 0) binv[0] = inv;
     const int KT = 4 * gc;
     const int bbytes = nout * KT * 2;
     // every block reduces the (L2-resident) max itself and packs its slice of the image
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nout * KT; idx += gridDim.x * blockDim.x) {
+    for (int idx = bx * blockDim.x + threadIdx.x; idx < nout * KT; idx += gx * blockDim.x) {
         const int nn = idx / KT, k = idx % KT;
         const int t = k / gc, c = k % gc;
         const int cp = reverse ? c : nn;
@@ -148,6 +149,28 @@ __global__ void __launch_bounds__(1024)
         *reinterpret_cast<uint16_t *>(img + off) = hi;
         if (SPLIT) *reinterpret_cast<uint16_t *>(img + bbytes + off) = lo;
     }
+}
+template <bool SPLIT>
+__global__ void __launch_bounds__(1024)
+    tc_pack_b_kernel(int cin, int cout, int ld_cin, const float *__restrict__ theta, const float *__restrict__ theta_b,
+                     int reverse, int nout, int gc, uint8_t *__restrict__ img, float *__restrict__ binv) {
+    pack_b_body<SPLIT>(cin, cout, ld_cin, theta, theta_b, reverse, nout, gc, img, binv, blockIdx.x, gridDim.x);
+}
+// the B images of all passes of a channel-blocked call in ONE launch (blockIdx.y = pass),
+// each identical to its own tc_pack_b_kernel launch: image j at img0 + j * stride, its
+// 1 / scale right after the image bytes
+constexpr int kPackBatch = 32;
+struct PackBatch {
+    const float *theta[kPackBatch];
+    const float *theta_b[kPackBatch];
+};
+template <bool SPLIT>
+__global__ void __launch_bounds__(1024)
+    tc_pack_b_batch_kernel(int cin, int cout, int ld_cin, int reverse, int nout, int gc, uint8_t *__restrict__ img0,
+                           int64_t stride, int64_t bbytes, const __grid_constant__ PackBatch jobs) {
+    uint8_t *img = img0 + (int64_t)blockIdx.y * stride;
+    pack_b_body<SPLIT>(cin, cout, ld_cin, jobs.theta[blockIdx.y], jobs.theta_b[blockIdx.y], reverse, nout, gc, img,
+                       reinterpret_cast<float *>(img + bbytes), blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------------
@@ -1270,14 +1293,17 @@ static int launch_tc(const TcArgs &a0, int cin, int cout, const float *theta, co
                      cudaStream_t st, int ld_cin = -1) {
     using L = TcLayout<GC, NOUT, SPLIT, DLOC>;
     TcArgs a = a0;
-    uint8_t *img = (uint8_t *)scratch_alloc((size_t)L::B_BYTES * L::NSPLIT + 256, st);
-    if (!img) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc)");
-    float *binv = reinterpret_cast<float *>(img + (size_t)L::B_BYTES * L::NSPLIT);
-    tc_pack_b_kernel<SPLIT><<<(unsigned)ceil_div(NOUT * 4 * GC, 1024), 1024, 0, st>>>(
-        cin, cout, ld_cin > 0 ? ld_cin : cin, theta, theta_b, REVERSE ? 1 : 0, NOUT, GC, img, binv);
-    count_launch();
-    a.bimg = img;
-    a.binv = binv;
+    uint8_t *img = nullptr;  // a0.bimg set: the caller packed this pass's image (pack_passes)
+    if (!a.bimg) {
+        img = (uint8_t *)scratch_alloc((size_t)L::B_BYTES * L::NSPLIT + 256, st);
+        if (!img) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc)");
+        float *binv = reinterpret_cast<float *>(img + (size_t)L::B_BYTES * L::NSPLIT);
+        tc_pack_b_kernel<SPLIT><<<(unsigned)ceil_div(NOUT * 4 * GC, 1024), 1024, 0, st>>>(
+            cin, cout, ld_cin > 0 ? ld_cin : cin, theta, theta_b, REVERSE ? 1 : 0, NOUT, GC, img, binv);
+        count_launch();
+        a.bimg = img;
+        a.binv = binv;
+    }
     a.num_tiles = ceil_div(a.total, kTcM);
     static uint64_t attr = 0;
     if (first_use_on_device(attr)) {
@@ -1289,7 +1315,7 @@ static int launch_tc(const TcArgs &a0, int cin, int cout, const float *theta, co
     tc_gmc_kernel<GC, NOUT, SPLIT, REVERSE, KFIX, DLOC><<<grid, kTcThreads, L::SMEM, st>>>(a);
     prof_end(st);
     count_launch();
-    scratch_free(img, st);
+    if (img) scratch_free(img, st);
     return check_launch("tc_gmc_kernel");
 }
 
@@ -1392,7 +1418,7 @@ int tc_reverse_supported(int mode, int gc, int d, int cout) { return tc_shape_ok
 
 template <typename T>
 int launch_dtheta_reduce(int chunks, int cin, int d, int cout, const T *partial, T *d_theta, T *d_theta_b,
-                         cudaStream_t st, int tmajor = 0);
+                         cudaStream_t st, int tmajor = 0, int ld = 0);
 
 // Full fp32 backward on the tensor cores (c_in = c_out = 64, d = 3):
 //   tc_dtheta_kernel : d_theta partials + centre term of d_locations
@@ -1419,7 +1445,9 @@ template <int MT = 1>
 static int generic_dtheta_block(int64_t total, int64_t n, int k, const float *feat, int64_t ld_feat,
                                 const float *loc, const int32_t *nbr, const float *g, int64_t ld_g,
                                 const float *theta, const float *theta_b, int ld_cin, float *d_theta,
-                                float *d_theta_b, int ld_dt, float *centre, bool acc_centre, cudaStream_t st) {
+                                float *d_theta_b, int ld_dt, float *centre, bool acc_centre, cudaStream_t st,
+                                const uint8_t *pimg = nullptr) {
+    // pimg: this block's forward image already packed (pack_passes), else packed here
     using L = DtLayoutT<MT>;
     constexpr int cin = 64, cout = 64 * MT;  // MT c' tiles of 64 (the centre term needs MT = 1)
     if (MT > 1 && centre) return set_error(FC_ERR_UNSUPPORTED, "d_theta c' tiles > 1 without the centre term only");
@@ -1428,15 +1456,12 @@ static int generic_dtheta_block(int64_t total, int64_t n, int k, const float *fe
     // CTAs (waves) instead of a longer, truncating accumulation
     const int grid = (int)std::min<int64_t>(num_tiles, std::max<int64_t>(num_sms(), ceil_div(num_tiles, 8)));
     const size_t img_bytes = (size_t)cout * 4 * cin * 2 * 2;
-    Scratch img_buf(img_bytes + 256, st);
+    Scratch img_buf((L::Z && !pimg) ? img_bytes + 256 : 16, st);
     Scratch partial_buf(sizeof(float) * 2 * grid * cout * cin * 4, st);
-    const bool dense = ld_dt == cin;
-    Scratch blk_buf(dense ? 16 : sizeof(float) * cout * cin * 4, st);
-    if (!img_buf.ok() || !partial_buf.ok() || !blk_buf.ok())
-        return set_error(FC_ERR_CUDA, "scratch allocation failed (tc d_theta)");
-    uint8_t *img = img_buf.as<uint8_t>();
+    if (!img_buf.ok() || !partial_buf.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc d_theta)");
+    uint8_t *img = pimg ? const_cast<uint8_t *>(pimg) : img_buf.as<uint8_t>();
     float *binv = reinterpret_cast<float *>(img + img_bytes);
-    if (L::Z) {  // the forward image: B of the centre-role Z GEMM
+    if (L::Z && !pimg) {  // the forward image: B of the centre-role Z GEMM
         tc_pack_b_kernel<true><<<(unsigned)ceil_div((int64_t)cout * 4 * cin, 1024), 1024, 0, st>>>(
             cin, cout, ld_cin, theta, theta_b, 0, cout, cin, img, binv);
         count_launch();
@@ -1472,18 +1497,8 @@ static int generic_dtheta_block(int64_t total, int64_t n, int k, const float *fe
     count_launch();
     int rc = check_launch("tc_dtheta_kernel");
     if (rc || !(d_theta || d_theta_b)) return rc;
-    if (dense) return launch_dtheta_reduce<float>(2 * grid, cin, 3, cout, a.partial, d_theta, d_theta_b, st);
-    // a block of a wider theta: reduce densely, then place the rows (row stride ld_dt)
-    float *bt = blk_buf.as<float>(), *btb = bt + cout * cin * 3;
-    rc = launch_dtheta_reduce<float>(2 * grid, cin, 3, cout, a.partial, bt, btb, st);
-    if (rc) return rc;
-    if (d_theta)
-        cudaMemcpy2DAsync(d_theta, sizeof(float) * 3 * ld_dt, bt, sizeof(float) * 3 * cin, sizeof(float) * 3 * cin, cout,
-                          cudaMemcpyDeviceToDevice, st);
-    if (d_theta_b)
-        cudaMemcpy2DAsync(d_theta_b, sizeof(float) * ld_dt, btb, sizeof(float) * cin, sizeof(float) * cin, cout,
-                          cudaMemcpyDeviceToDevice, st);
-    return check_launch("d_theta block copy");
+    // a block of a wider theta is written in place (row stride ld_dt)
+    return launch_dtheta_reduce<float>(2 * grid, cin, 3, cout, a.partial, d_theta, d_theta_b, st, 0, ld_dt);
 }
 
 int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int cout, const float *g,
@@ -1630,6 +1645,32 @@ static void add_rows(int64_t rows, int w, float *dst, int64_t ldd, const float *
     count_launch();
 }
 
+// The B images of a blocked call's passes (one shape, njobs blocks of theta) packed up front
+// in one launch instead of one small, latency-bound launch ahead of every pass: image j at
+// buf + j * stride, its 1 / scale right after its bytes.
+static int pack_passes(bool split, int cin, int cout, int ld_cin, int reverse, int nout, int gc, int njobs,
+                       const float *const *th, const float *const *tb, Scratch &buf, int64_t &stride, cudaStream_t st) {
+    const int64_t bbytes = (int64_t)nout * 4 * gc * 2 * (split ? 2 : 1);
+    stride = (bbytes + 256 + 1023) / 1024 * 1024;
+    buf.alloc((size_t)(stride * njobs), st);
+    if (!buf.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (pass images)");
+    const unsigned gx = (unsigned)ceil_div((int64_t)nout * 4 * gc, 1024);
+    for (int j0 = 0; j0 < njobs; j0 += kPackBatch) {
+        const int nj = std::min(kPackBatch, njobs - j0);
+        PackBatch pb{};
+        for (int j = 0; j < nj; ++j) {
+            pb.theta[j] = th[j0 + j];
+            pb.theta_b[j] = tb[j0 + j];
+        }
+        uint8_t *img0 = buf.as<uint8_t>() + (int64_t)j0 * stride;
+        const dim3 grid(gx, (unsigned)nj);
+        if (split) tc_pack_b_batch_kernel<true><<<grid, 1024, 0, st>>>(cin, cout, ld_cin, reverse, nout, gc, img0, stride, bbytes, pb);
+        else tc_pack_b_batch_kernel<false><<<grid, 1024, 0, st>>>(cin, cout, ld_cin, reverse, nout, gc, img0, stride, bbytes, pb);
+        count_launch();
+    }
+    return check_launch("pack passes");
+}
+
 // output channels per pass of the channel-blocked engines: all of them up to 256
 static int blocked_out_block(int c) {
     if (c <= 256) return c % 64 == 0 && c != 192 ? c : 64;
@@ -1656,8 +1697,22 @@ int tc_blocked_forward(int mode, int64_t total, int64_t n, int c_in, int k, int 
         tmp.alloc(sizeof(float) * (size_t)(nin - 1) * total * ob, st);
         if (!tmp.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (blocked forward)");
     }
+    Scratch imgs;
+    int64_t istride = 0;
+    {
+        std::vector<const float *> th, tb;
+        for (int o0 = 0; o0 < c_out; o0 += ob)
+            for (int i0 = 0; i0 < c_in; i0 += gb) {
+                th.push_back(theta + ((int64_t)o0 * c_in + i0) * 3);
+                tb.push_back(theta_b + (int64_t)o0 * c_in + i0);
+            }
+        const int rc0 = pack_passes(mode != FC_MODE_TC_BF16, gb, ob, c_in, 0, ob, gb, (int)th.size(), th.data(), tb.data(),
+                                    imgs, istride, st);
+        if (rc0) return rc0;
+    }
     ForkJoin fj(st, nin, conc);
     int rc = FC_OK;
+    int pass = 0;
     for (int o0 = 0; o0 < c_out && rc == FC_OK; o0 += ob) {
         for (int i0 = 0, b = 0; i0 < c_in; i0 += gb, ++b) {
             TcArgs a{};
@@ -1671,6 +1726,9 @@ int tc_blocked_forward(int mode, int64_t total, int64_t n, int c_in, int k, int 
             a.out = (conc && b > 0) ? tmp.as<float>() + (size_t)(b - 1) * total * ob : out + o0;
             a.ld_out = (conc && b > 0) ? ob : c_out;
             a.acc = !conc && i0 > 0;
+            a.bimg = imgs.as<uint8_t>() + pass * istride;
+            a.binv = reinterpret_cast<const float *>(a.bimg + (ob * 4 * gb * 2 * (mode != FC_MODE_TC_BF16 ? 2 : 1)));
+            ++pass;
             const float *th = theta + ((int64_t)o0 * c_in + i0) * 3, *tb = theta_b + (int64_t)o0 * c_in + i0;
             const cudaStream_t sj = conc ? fj[b] : st;
             rc = mode == FC_MODE_TC_BF16 ? dispatch_tc<false, false>(gb, ob, a, gb, ob, th, tb, sj, c_in)
@@ -1708,8 +1766,22 @@ static int tc_blocked_reverse(int mode, int64_t total, int64_t n, int c_in, int 
             return set_error(FC_ERR_CUDA, "scratch allocation failed (blocked reverse)");
         if (dloc) cudaMemsetAsync(zero3.p, 0, sizeof(float) * total * 3, st);
     }
+    Scratch imgs;
+    int64_t istride = 0;
+    {
+        std::vector<const float *> th, tb;
+        for (int i0 = 0; i0 < c_in; i0 += ob)
+            for (int j0 = 0; j0 < c_out; j0 += gb) {
+                th.push_back(theta + ((int64_t)j0 * c_in + i0) * 3);
+                tb.push_back(theta_b + (int64_t)j0 * c_in + i0);
+            }
+        const int rc0 = pack_passes(mode != FC_MODE_TC_BF16, ob, gb, c_in, 1, ob, gb, (int)th.size(), th.data(), tb.data(),
+                                    imgs, istride, st);
+        if (rc0) return rc0;
+    }
     ForkJoin fj(st, nj, conc);
     int rc = FC_OK;
+    int pass = 0;
     for (int i0 = 0; i0 < c_in && rc == FC_OK; i0 += ob) {
         for (int j0 = 0, b = 0; j0 < c_out; j0 += gb, ++b) {
             const bool side = conc && b > 0;
@@ -1732,6 +1804,9 @@ static int tc_blocked_reverse(int mode, int64_t total, int64_t n, int c_in, int 
                 a.dloc = side ? tdl.as<float>() + (size_t)(b - 1) * total * 3 : dloc;
                 a.acc_dloc = !conc && (i0 > 0 || j0 > 0);
             }
+            a.bimg = imgs.as<uint8_t>() + pass * istride;
+            a.binv = reinterpret_cast<const float *>(a.bimg + (ob * 4 * gb * 2 * (mode != FC_MODE_TC_BF16 ? 2 : 1)));
+            ++pass;
             const float *th = theta + ((int64_t)j0 * c_in + i0) * 3, *tb = theta_b + (int64_t)j0 * c_in + i0;
             const cudaStream_t sj = conc ? fj[b] : st;
             rc = mode == FC_MODE_TC_BF16 ? dispatch_tc<false, true>(gb, ob, a, ob, gb, th, tb, sj, c_in)
@@ -1774,6 +1849,18 @@ int tc_blocked_backward(int mode, int64_t total, int64_t n, int c_in, int k, int
             cside.alloc(sizeof(float) * (size_t)(npass - 1) * total * 3, st);
             if (!cside.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (blocked backward)");
         }
+        Scratch imgs;  // the forward images of the centre-role Z GEMMs (64-wide c' tiles only)
+        int64_t istride = 0;
+        if (jb == 64) {
+            std::vector<const float *> th, tb;
+            for (int j0 = 0; j0 < c_out; j0 += jb)
+                for (int i0 = 0; i0 < c_in; i0 += 64) {
+                    th.push_back(theta + ((int64_t)j0 * c_in + i0) * 3);
+                    tb.push_back(theta_b + (int64_t)j0 * c_in + i0);
+                }
+            const int rc0 = pack_passes(true, 64, 64, c_in, 0, 64, 64, (int)th.size(), th.data(), tb.data(), imgs, istride, st);
+            if (rc0) return rc0;
+        }
         ForkJoin fj(st, npass, conc);
         int rc = FC_OK;
         int b = 0;
@@ -1790,7 +1877,7 @@ int tc_blocked_backward(int mode, int64_t total, int64_t n, int c_in, int k, int
                                                          false, sj)
                                : generic_dtheta_block<1>(total, n, k, feat + i0, c_in, loc, nbr, g + j0, c_out,
                                                          theta + e0 * 3, theta_b + e0, c_in, dtp, dtbp, c_in, cen,
-                                                         !conc && (j0 > 0 || i0 > 0), sj);
+                                                         !conc && (j0 > 0 || i0 > 0), sj, imgs.as<uint8_t>() + b * istride);
                 if (rc) break;
             }
         }

@@ -26,7 +26,7 @@ namespace fc {
 
 template <typename T>
 int launch_dtheta_reduce(int chunks, int cin, int d, int cout, const T *partial, T *d_theta, T *d_theta_b,
-                         cudaStream_t st, int tmajor = 0);
+                         cudaStream_t st, int tmajor = 0, int ld = 0);
 
 namespace {
 
