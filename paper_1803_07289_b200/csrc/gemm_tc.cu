@@ -26,6 +26,7 @@ namespace gemm {
 using fast::ldg_nc4;
 using fast::sts128f;
 using fast::lds128f;
+using fast::ffma2;
 
 constexpr int kMaxOps = 4;
 constexpr int kMaxOuts = 4;
@@ -346,44 +347,122 @@ struct WArgs {
     float *part;      // [nchunk][co][ci + 1]
 };
 // CTA (64 threads): 64 (co) x 64 (ci) outputs over one point chunk; thread: 8 x 8 outputs
-// (4 shared loads per 64 FMAs).  32-point slabs of G, X (and the ReLU mask) arrive by 4-byte
+// (4 shared loads per 32 FFMA2).  32-point slabs of G, X (and the ReLU mask) arrive by 4-byte
 // cp.async into a double-buffered shared tile, one slab ahead of the FMAs (no registers held
 // across the load latency).  Partial sums per chunk, reduced in fixed order (deterministic).
-template <bool MASKED>
+// TAIL: the last ci tile also carries up to 8 more columns (64 + 3 coordinates + the bias
+// column of a ResBlock is one tile plus a 4-column tail, not two tiles): thread (ty, tx) adds
+// co 8 ty .. +7 x tail column tx.
+template <bool MASKED, bool TAIL>
+struct WgradSmem {
+    static constexpr int XW = TAIL ? 72 : 64;
+    float Gs[2][32][64];
+    float Xs[2][32][XW];
+    float Ms[MASKED ? 2 : 1][MASKED ? 32 : 1][MASKED ? 64 : 4];
+};
+template <bool MASKED, bool TAIL>
 __global__ void __launch_bounds__(64) wgrad_kernel(WArgs a) {
-    __shared__ __align__(16) float Gs[2][32][64];
-    __shared__ __align__(16) float Xs[2][32][64];
-    __shared__ __align__(16) float Ms[MASKED ? 2 : 1][MASKED ? 32 : 1][MASKED ? 64 : 4];
+    extern __shared__ __align__(16) uint8_t wg_smem[];
+    auto &sm = *reinterpret_cast<WgradSmem<MASKED, TAIL> *>(wg_smem);
+    auto &Gs = sm.Gs;
+    auto &Xs = sm.Xs;
+    auto &Ms = sm.Ms;
     const int tid = threadIdx.x, ty = tid >> 3, tx = tid & 7;
     const int co0 = blockIdx.x * 64, ci0 = blockIdx.y * 64;
     const int64_t p0 = (int64_t)blockIdx.z * a.chunk, p1 = std::min<int64_t>(a.n, p0 + a.chunk);
-    const int gcol = co0 + tid, xcol = ci0 + tid;  // loader: column tid of the slabs
-    int xq = -1, xk = 0;
-    if (xcol < a.ci)
+    // loader: thread tid copies the column quad qd = tid & 15 (columns 4 qd .. +3) of rows
+    // rg + 4 k (rg = tid >> 4, k < 8) of every slab -- one 16-byte copy where the quad lies in
+    // one 16-byte-aligned operand row, else four 4-byte copies; the tail columns 64 + tx
+    // (tx = tid & 7 < ntail) of rows (tid >> 3) + 8 k (k < 4)
+    const int qd = tid & 15, rg = tid >> 4;
+    const int gc4 = co0 + 4 * qd;
+    const bool gvec = (a.ldg & 3) == 0 && (reinterpret_cast<uintptr_t>(a.g) & 15) == 0 && gc4 + 4 <= a.co;
+    const bool mvec = MASKED && (a.mask_ld & 3) == 0 && (reinterpret_cast<uintptr_t>(a.mask) & 15) == 0 && gc4 + 4 <= a.co;
+    auto col_src = [&](int col, int64_t &ld) -> const float * {  // operand column (null: bias / past ci)
+        ld = 0;
+        if (col >= a.ci) return nullptr;
         for (int q = 0; q < a.nops; ++q)
-            if (xcol >= a.ops[q].kb0 && xcol < a.ops[q].kb0 + a.ops[q].k) xq = q, xk = xcol - a.ops[q].kb0;
-    const float *xp = xq >= 0 ? a.ops[xq].a + xk : nullptr;
-    const int64_t xld = xq >= 0 ? a.ops[xq].lda : 0;
-    const bool gval = gcol < a.co;
-    const bool ones = xcol == a.ci;  // the bias column
+            if (col >= a.ops[q].kb0 && col < a.ops[q].kb0 + a.ops[q].k) {
+                ld = a.ops[q].lda;
+                return a.ops[q].a + (col - a.ops[q].kb0);
+            }
+        return nullptr;
+    };
+    const int xc4 = ci0 + 4 * qd;
+    const float *xe[4];
+    int64_t xl[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) xe[e] = col_src(xc4 + e, xl[e]);
+    const bool xvec = xe[0] && xe[3] == xe[0] + 3 && xl[3] == xl[0] && (xl[0] & 3) == 0 &&
+                      (reinterpret_cast<uintptr_t>(xe[0]) & 15) == 0;
+    const int ntail = (TAIL && blockIdx.y == gridDim.y - 1) ? a.ci + 1 - (ci0 + 64) : 0;
+    const int tcol = ci0 + 64 + tx;
+    const bool tload = tx < ntail;
+    int64_t tld = 0;
+    const float *tp = tload ? col_src(tcol, tld) : nullptr;
+    const bool tones = tload && tcol == a.ci;
     constexpr bool masked = MASKED;
     auto issue = [&](int64_t pb, int buf) {
-#pragma unroll 4
-        for (int rr = 0; rr < 32; ++rr) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int rr = rg + 4 * k;
             const int64_t p = pb + rr;
             const bool pv = p < p1;
-            const uint32_t gs = smem_u32(&Gs[buf][rr][tid]), xs = smem_u32(&Xs[buf][rr][tid]);
-            cpa4(gs, pv && gval ? a.g + p * a.ldg + gcol : a.g, pv && gval);
-            if (ones)
-                Xs[buf][rr][tid] = pv ? 1.f : 0.f;  // (no async write pending on this slot)
-            else
-                cpa4(xs, xp && pv ? xp + p * xld : a.g, xp != nullptr && pv);
-            if constexpr (MASKED)
-                cpa4(smem_u32(&Ms[buf][rr][tid]), pv && gval ? a.mask + p * a.mask_ld + gcol : a.mask, pv && gval);
+            const uint32_t gs = smem_u32(&Gs[buf][rr][4 * qd]), xs = smem_u32(&Xs[buf][rr][4 * qd]);
+            if (gvec) {
+                cpa16(gs, pv ? a.g + p * a.ldg + gc4 : a.g, pv);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const bool v = pv && gc4 + e < a.co;
+                    cpa4(gs + 4u * e, v ? a.g + p * a.ldg + gc4 + e : a.g, v);
+                }
+            }
+            if (xvec) {
+                cpa16(xs, pv ? xe[0] + p * xl[0] : a.g, pv);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (xc4 + e == a.ci)
+                        Xs[buf][rr][4 * qd + e] = pv ? 1.f : 0.f;  // the bias column (no async write pending here)
+                    else
+                        cpa4(xs + 4u * e, xe[e] && pv ? xe[e] + p * xl[e] : a.g, xe[e] != nullptr && pv);
+                }
+            }
+            if constexpr (MASKED) {
+                const uint32_t ms = smem_u32(&Ms[buf][rr][4 * qd]);
+                if (mvec) {
+                    cpa16(ms, pv ? a.mask + p * a.mask_ld + gc4 : a.mask, pv);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const bool v = pv && gc4 + e < a.co;
+                        cpa4(ms + 4u * e, v ? a.mask + p * a.mask_ld + gc4 + e : a.mask, v);
+                    }
+                }
+            }
+        }
+        if constexpr (TAIL) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int rr = (tid >> 3) + 8 * k;
+                const int64_t p = pb + rr;
+                const bool pv = p < p1;
+                if (tones)
+                    Xs[buf][rr][64 + tx] = pv ? 1.f : 0.f;
+                else if (tload)
+                    cpa4(smem_u32(&Xs[buf][rr][64 + tx]), tp && pv ? tp + p * tld : a.g, tp != nullptr && pv);
+            }
         }
         cpa_commit();
     };
-    float acc[8][8] = {};
+    float2 acc[8][4], acct[4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acct[i] = make_float2(0.f, 0.f);
     int buf = 0;
     if (p0 < p1) issue(p0, 0);
     for (int64_t pb = p0; pb < p1; pb += 32, buf ^= 1) {
@@ -409,11 +488,17 @@ __global__ void __launch_bounds__(64) wgrad_kernel(WArgs a) {
             const float4 x0 = *reinterpret_cast<const float4 *>(&Xs[buf][rr][8 * tx]);
             const float4 x1 = *reinterpret_cast<const float4 *>(&Xs[buf][rr][8 * tx + 4]);
             const float g8[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-            const float x8[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+            const float2 x2[4] = {make_float2(x0.x, x0.y), make_float2(x0.z, x0.w), make_float2(x1.x, x1.y),
+                                  make_float2(x1.z, x1.w)};
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(g8[i], x8[j], acc[i][j]);
+                for (int j = 0; j < 4; ++j) acc[i][j] = ffma2(make_float2(g8[i], g8[i]), x2[j], acc[i][j]);
+            if constexpr (TAIL) {
+                const float xt = Xs[buf][rr][64 + tx];  // (columns past the tail: never written out)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acct[i] = ffma2(make_float2(g8[2 * i], g8[2 * i + 1]), make_float2(xt, xt), acct[i]);
+            }
         }
         __syncthreads();  // buffer buf is refilled by the next iteration's issue
     }
@@ -424,21 +509,56 @@ __global__ void __launch_bounds__(64) wgrad_kernel(WArgs a) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int o = co0 + 8 * ty + i, c = ci0 + 8 * tx + j;
-            if (o < a.co && c <= a.ci) out[(int64_t)o * ldp + c] = acc[i][j];
+            if (o < a.co && c <= a.ci) out[(int64_t)o * ldp + c] = (j & 1) ? acc[i][j >> 1].y : acc[i][j >> 1].x;
         }
+    if (TAIL && tx < ntail) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int o = co0 + 8 * ty + i;
+            if (o < a.co) out[(int64_t)o * ldp + ci0 + 64 + tx] = (i & 1) ? acct[i >> 1].y : acct[i >> 1].x;
+        }
+    }
 }
-__global__ void wgrad_reduce_kernel(const float *__restrict__ part, int nchunk, int co, int ci, float *__restrict__ dw,
-                                    float *__restrict__ db) {
+// fixed-order chunk reduction (fp64): a CTA owns 32 consecutive outputs, warp w adds the
+// chunks of its contiguous block in ascending order, the 8 block sums are added in warp order
+__global__ void __launch_bounds__(256) wgrad_reduce_kernel(const float *__restrict__ part, int nchunk, int co, int ci,
+                                                           float *__restrict__ dw, float *__restrict__ db) {
+    constexpr int W = 8;
+    __shared__ double red[W][32];
     const int ldp = ci + 1;
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < co * ldp; idx += gridDim.x * blockDim.x) {
+    const int64_t E = (int64_t)co * ldp;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int per = (nchunk + W - 1) / W;
+    const int z0 = min(nchunk, w * per), z1 = min(nchunk, z0 + per);
+    for (int64_t e0 = (int64_t)blockIdx.x * 32; e0 < E; e0 += (int64_t)gridDim.x * 32) {
+        const int64_t idx = e0 + lane;
         double s = 0.0;
-        for (int z = 0; z < nchunk; ++z) s += (double)part[(int64_t)z * co * ldp + idx];
-        const int o = idx / ldp, c = idx % ldp;
-        if (c < ci) {
-            if (dw) dw[(int64_t)o * ci + c] = (float)s;
-        } else if (db) {
-            db[o] = (float)s;
+        if (idx < E) {
+            int z = z0;
+            for (; z + 4 <= z1; z += 4) {
+                const float v0 = part[(int64_t)z * E + idx], v1 = part[(int64_t)(z + 1) * E + idx];
+                const float v2 = part[(int64_t)(z + 2) * E + idx], v3 = part[(int64_t)(z + 3) * E + idx];
+                s += (double)v0;
+                s += (double)v1;
+                s += (double)v2;
+                s += (double)v3;
+            }
+            for (; z < z1; ++z) s += (double)part[(int64_t)z * E + idx];
         }
+        red[w][lane] = s;
+        __syncthreads();
+        if (w == 0 && idx < E) {
+            double t = red[0][lane];
+#pragma unroll
+            for (int q = 1; q < W; ++q) t += red[q][lane];
+            const int o = (int)(idx / ldp), c = (int)(idx % ldp);
+            if (c < ci) {
+                if (dw) dw[(int64_t)o * ci + c] = (float)t;
+            } else if (db) {
+                db[o] = (float)t;
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -555,19 +675,50 @@ extern "C" int fc_gemm_wgrad(int64_t n, const float *g, int64_t ldg, const float
         ci += kx[q];
     }
     a.ci = ci;
-    const int gx = (int)ceil_div(co, 64), gy = (int)ceil_div(ci + 1, 64);
-    int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(n, 1), 512),
-                                                            ceil_div(8 * num_sms(), gx * gy)));
-    a.chunk = ceil_div(std::max<int64_t>(n, 1), nchunk);
-    nchunk = ceil_div(std::max<int64_t>(n, 1), a.chunk);
+    // ci + 1 columns (the bias last) in tiles of 64; a remainder of <= 8 rides on the last tile
+    const int nfull = (ci + 1) / 64, rem = (ci + 1) % 64;
+    const bool tail = nfull >= 1 && rem > 0 && rem <= 8;
+    const int gx = (int)ceil_div(co, 64), gy = tail ? nfull : (int)ceil_div(ci + 1, 64);
+    // point chunks: one full wave of resident CTAs (the kernel is latency-bound; partials
+    // are reduced in fixed order afterwards), at least 64 and at most 4096 points per chunk
+    size_t smem_b = 0;
+    const void *kfn = nullptr;
+    if (mask) {
+        smem_b = tail ? sizeof(gemm::WgradSmem<true, true>) : sizeof(gemm::WgradSmem<true, false>);
+        kfn = tail ? (const void *)gemm::wgrad_kernel<true, true> : (const void *)gemm::wgrad_kernel<true, false>;
+    } else {
+        smem_b = tail ? sizeof(gemm::WgradSmem<false, true>) : sizeof(gemm::WgradSmem<false, false>);
+        kfn = tail ? (const void *)gemm::wgrad_kernel<false, true> : (const void *)gemm::wgrad_kernel<false, false>;
+    }
+    static uint64_t wattr = 0;
+    if (first_use_on_device(wattr)) {  // the masked tail variant needs > 48 KB
+        cudaFuncSetAttribute(gemm::wgrad_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(gemm::WgradSmem<true, true>));
+        cudaFuncSetAttribute(gemm::wgrad_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(gemm::WgradSmem<true, false>));
+    }
+    static int occ_cache[4] = {0, 0, 0, 0};  // resident CTAs per SM of each variant
+    int &occ = occ_cache[(mask ? 2 : 0) + (tail ? 1 : 0)];
+    if (occ < 1 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 64, smem_b) != cudaSuccess || occ < 1)) occ = 1;
+    const int64_t nn = std::max<int64_t>(n, 1), tiles = (int64_t)gx * gy;
+    int64_t nchunk = std::max<int64_t>(1, (int64_t)occ * num_sms() / tiles);
+    nchunk = std::min<int64_t>(std::max<int64_t>(nchunk, ceil_div(nn, 4096)), ceil_div(nn, 64));
+    a.chunk = ceil_div(nn, nchunk);
+    nchunk = ceil_div(nn, a.chunk);
     Scratch part((size_t)nchunk * co * (ci + 1) * sizeof(float), st);
     if (!part.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (gemm_wgrad)");
     a.part = part.as<float>();
     prof_begin("pointwise_wgrad", st);
-    if (mask) gemm::wgrad_kernel<true><<<dim3(gx, gy, (unsigned)nchunk), 64, 0, st>>>(a);
-    else gemm::wgrad_kernel<false><<<dim3(gx, gy, (unsigned)nchunk), 64, 0, st>>>(a);
+    const dim3 grid(gx, gy, (unsigned)nchunk);
+    if (mask) {
+        if (tail) gemm::wgrad_kernel<true, true><<<grid, 64, sizeof(gemm::WgradSmem<true, true>), st>>>(a);
+        else gemm::wgrad_kernel<true, false><<<grid, 64, sizeof(gemm::WgradSmem<true, false>), st>>>(a);
+    } else {
+        if (tail) gemm::wgrad_kernel<false, true><<<grid, 64, sizeof(gemm::WgradSmem<false, true>), st>>>(a);
+        else gemm::wgrad_kernel<false, false><<<grid, 64, sizeof(gemm::WgradSmem<false, false>), st>>>(a);
+    }
     count_launch();
-    gemm::wgrad_reduce_kernel<<<(int)std::min<int64_t>(ceil_div((int64_t)co * (ci + 1), 256), 1024), 256, 0, st>>>(
+    gemm::wgrad_reduce_kernel<<<(unsigned)ceil_div((int64_t)co * (ci + 1), 32), 256, 0, st>>>(
         a.part, (int)nchunk, co, ci, dw, db);
     count_launch();
     prof_end(st);
