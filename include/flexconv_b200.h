@@ -267,6 +267,13 @@ int fc_gemm_wgrad(int64_t n, const float *g, int64_t ldg, const float *mask, int
                   int co, int nops, const float *const *x, const int64_t *ldx, const int *kx,
                   float *dw, float *db, void *stream);
 
+/* ---- ReLU gradient of the U-Net blocks (the reference's tf.nn.relu inside its residual and
+ * merge blocks, network.py:404-416 / :261-280) in one pass: out[i] = g[i] * (z[i] > 0 ? 1 : 0)
+ * (+ add[i] when add is non-null) -- the arithmetic of `g * (z > 0) + add`; n elements of
+ * dtype FC_F32 / FC_F64; out may alias g. */
+int fc_relu_backward(int dtype, int64_t n, const void *g, const void *z, const void *add, void *out,
+                     void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -68,6 +68,7 @@ SIGNATURES = {
     "fc_gemm_pack_b": [_I, _I, _I, _P, _P, _P, _I64, _P, _P],
     "fc_gemm_rows": [_I64, _I, _P, _P, _P, _P, _I64, _P, _I, _P, _I, _P, _P, _P, _P, _P, _I64, _P],
     "fc_gemm_wgrad": [_I64, _P, _I64, _P, _I64, _I, _I, _P, _P, _P, _P, _P, _P],
+    "fc_relu_backward": [_I, _I64, _P, _P, _P, _P, _P],
 }
 _RESTYPE = {"fc_last_error": ctypes.c_char_p, "fc_launch_count": ctypes.c_uint64, "fc_profile_enable": None,
             "fc_profile_reset": None, "fc_profile_name": ctypes.c_char_p, "fc_profile_ms": ctypes.c_float,

@@ -177,9 +177,17 @@ def conv_forward_rows(feat, loc, nbr, theta, theta_b, rows, out):
     return out
 
 
+def _out_ok(t, shape, dt, dev, name):
+    if tuple(t.shape) != tuple(shape) or t.dtype != dt or t.device != dev or not t.is_contiguous():
+        raise ShapeMismatchError(f"{name}: expected contiguous {dt} {tuple(shape)} on {dev}, got {t.dtype} "
+                                 f"{tuple(t.shape)} on {t.device}")
+
+
 def conv_backward(g, feat, loc, nbr, csr, theta, theta_b, batch, n, need=(True, True, True, True),
-                  mode="auto"):
-    """Returns (d_features, d_theta, d_theta_b, d_locations); entries not in `need` are None."""
+                  mode="auto", d_theta_out=None, d_theta_b_out=None):
+    """Returns (d_features, d_theta, d_theta_b, d_locations); entries not in `need` are None.
+    d_theta_out / d_theta_b_out: contiguous tensors to write the parameter gradients into
+    (e.g. views of a flat gradient vector) instead of new ones."""
     feat = _need(feat, "features")
     dt, dev = feat.dtype, feat.device
     g = _need(g, "upstream", dt, dev)
@@ -199,8 +207,13 @@ def conv_backward(g, feat, loc, nbr, csr, theta, theta_b, batch, n, need=(True, 
     want_df, want_dth, want_dtb, want_dl = need
     df = torch.empty(batch * n, c_in, dtype=dt, device=dev) if want_df else None
     dl = torch.empty(batch * n, d, dtype=dt, device=dev) if want_dl else None
-    dth = torch.empty(c_out, c_in, d, dtype=dt, device=dev) if want_dth else None
-    dtb = torch.empty(c_out, c_in, dtype=dt, device=dev) if want_dtb else None
+    dth = dtb = None
+    if want_dth:
+        dth = d_theta_out if d_theta_out is not None else torch.empty(c_out, c_in, d, dtype=dt, device=dev)
+        _out_ok(dth, (c_out, c_in, d), dt, dev, "d_theta_out")
+    if want_dtb:
+        dtb = d_theta_b_out if d_theta_b_out is not None else torch.empty(c_out, c_in, dtype=dt, device=dev)
+        _out_ok(dtb, (c_out, c_in), dt, dev, "d_theta_b_out")
     off, ent = csr if csr is not None else (None, None)
     _call(feat.device, "fc_conv_backward", _dtype(feat), _mode(mode), batch, n, c_in, d, k, c_out, _p(g), _p(feat),
               _p(loc), _p(nbr), _p(off), _p(ent), _p(theta), _p(theta_b), _p(df), _p(dl), _p(dth), _p(dtb),
@@ -425,6 +438,24 @@ def gemm_rows(operands, img: torch.Tensor, ncols: int, bias=None, outs=None, rel
           _carr(ctypes.c_int, [c0 for c0, _ in outs]), _carr(ctypes.c_int, [c1 for _, c1 in outs]),
           _p(rl), rl.stride(0) if rl is not None else 0, _stream(ops[0]))
     return res + ([rl] if relu else [])
+
+
+def relu_backward(g: torch.Tensor, z: torch.Tensor, add: torch.Tensor | None = None, out=None) -> torch.Tensor:
+    """g * (z > 0) [+ add] in one pass (out may be g itself: in place)."""
+    g = _need(g, "g")
+    z = _need(z, "z", g.dtype, g.device)
+    if z.shape != g.shape or not g.is_contiguous() or not z.is_contiguous():
+        raise ShapeMismatchError(f"relu_backward: g {tuple(g.shape)} and z {tuple(z.shape)} must be contiguous, same shape")
+    if add is not None:
+        add = _need(add, "add", g.dtype, g.device)
+        if add.shape != g.shape or not add.is_contiguous():
+            raise ShapeMismatchError("relu_backward: add must be contiguous, same shape as g")
+    if out is None:
+        out = torch.empty_like(g)
+    elif out.shape != g.shape or out.dtype != g.dtype or not out.is_contiguous():
+        raise ShapeMismatchError("relu_backward: bad out")
+    _call(g.device, "fc_relu_backward", _dtype(g), g.numel(), _p(g), _p(z), _p(add), _p(out), _stream(g))
+    return out
 
 
 def gemm_wgrad(g: torch.Tensor, operands, dw=None, db=None, mask=None) -> None:

@@ -94,3 +94,28 @@ def test_pointwise_large_values_no_scaling_issue():
     rel = ((y.double() - ref).norm(dim=1) / ref.norm(dim=1)).max()
     assert float(rel) < 1e-5
     assert np.isfinite(y.cpu().numpy()).all()
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("n", [1, 7, 4096, 262_147])
+def test_relu_backward_matches_torch_bitwise(dtype, n):
+    """fc_relu_backward == `g * (z > 0) + add` bit for bit (NaN, inf and signed zeros
+    included), in place or not, vectorised (n % 4 == 0) and scalar paths."""
+    dev = torch.device("cuda", 0)
+    torch.manual_seed(n)
+    g = torch.randn(n, dtype=dtype, device=dev)
+    z = torch.randn(n, dtype=dtype, device=dev)
+    add = torch.randn(n, dtype=dtype, device=dev)
+    if n >= 7:
+        g[:4] = torch.tensor([float("nan"), float("inf"), -0.0, -1.0], dtype=dtype)
+        z[:7] = torch.tensor([-1.0, -2.0, 3.0, 0.0, float("nan"), -0.0, 5.0], dtype=dtype)
+    want = g * (z > 0)
+    assert torch.equal(_ops.relu_backward(g, z).view(torch.int64 if dtype == torch.float64 else torch.int32),
+                       want.view(torch.int64 if dtype == torch.float64 else torch.int32))
+    want_add = g * (z > 0) + add
+    got = g.clone()
+    _ops.relu_backward(got, z, add=add, out=got)  # in place
+    iv = torch.int64 if dtype == torch.float64 else torch.int32
+    assert torch.equal(got.view(iv), want_add.view(iv))
+    with pytest.raises(ShapeMismatchError):
+        _ops.relu_backward(g, z[: max(n - 1, 0)] if n > 1 else z.repeat(2))
