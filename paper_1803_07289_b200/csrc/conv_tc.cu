@@ -44,6 +44,7 @@ struct TcArgs {
     int64_t total;  // points (B*N)
     int64_t n;      // points per cloud
     int k;          // forward neighbourhood size (slot divisor for reverse entries)
+    int no_pipe32;  // FC_NO_REVPIPE32=1: the unpipelined reverse gather for GC = 32 (A/B)
     const float *rows;
     const float *loc;
     const int32_t *nbr;
@@ -572,6 +573,169 @@ struct RevPipe16 {
     __device__ __forceinline__ void advance() { make_cur(); }
 };
 
+// Software-pipelined REVERSE gather for GC = 32: 4 points per item, 8 lanes per point
+// (lane = point * 8 + slot), each index lane holding TWO list slots (slot, slot + 8), so the
+// first 16 entries of every list are pipelined like RevPipe16's: off[] of item w+3, ent[]
+// (+ centre position) of w+2, source positions of w+1 issued during w; rows of w loaded in
+// 8-slot sub-batches and accumulated in list order; lists longer than 16 finish unpipelined.
+struct RevPipe8x2 {
+    static constexpr int GC = 32;
+    const float *rows, *loc;
+    int64_t ld;
+    Csr csr;
+    int64_t total;
+    int k;
+    ItemMap im;
+    int64_t items;
+    int pt, cl, slot;
+    int32_t oq0_3, ocnt_3;                      // item w+3
+    int32_t eq0_2, ecnt_2, ent_2[2];            // item w+2
+    float lp0_2, lp1_2, lp2_2;
+    int32_t pq0_1, pcnt_1, j_1[2];              // item w+1
+    float lp0_1, lp1_1, lp2_1, nl_1[2][3];
+    int32_t q0, cnt, j[2];                      // item w
+    float o[2][3];
+
+    __device__ __forceinline__ void load_off(int64_t w, int32_t &q0o, int32_t &cnto) const {
+        q0o = 0;
+        cnto = 0;
+        if (w < items) {
+            const int64_t myp = im.p0(w) + pt;
+            if (myp < total) {
+                q0o = __ldg(csr.off + myp);
+                cnto = __ldg(csr.off + myp + 1) - q0o;
+            }
+        }
+    }
+    __device__ __forceinline__ void load_ent(int64_t w, int32_t q0i, int32_t cnti) {
+        eq0_2 = q0i;
+        ecnt_2 = cnti;
+        ent_2[0] = ent_2[1] = -1;
+        lp0_2 = lp1_2 = lp2_2 = 0.f;
+        if (w < items) {
+            const int64_t myp = im.p0(w) + pt;
+            if (myp < total) {
+                lp0_2 = __ldg(loc + myp * 3 + 0);
+                lp1_2 = __ldg(loc + myp * 3 + 1);
+                lp2_2 = __ldg(loc + myp * 3 + 2);
+                if (slot < cnti) ent_2[0] = __ldg(csr.ent + q0i + slot);
+                if (slot + 8 < cnti) ent_2[1] = __ldg(csr.ent + q0i + slot + 8);
+            }
+        }
+    }
+    __device__ __forceinline__ void load_pos() {
+        pq0_1 = eq0_2;
+        pcnt_1 = ecnt_2;
+        lp0_1 = lp0_2, lp1_1 = lp1_2, lp2_1 = lp2_2;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            j_1[h] = ent_2[h] >= 0 ? ent_2[h] / k : 0;
+            nl_1[h][0] = nl_1[h][1] = nl_1[h][2] = 0.f;
+            if (ent_2[h] >= 0) {
+                nl_1[h][0] = __ldg(loc + (int64_t)j_1[h] * 3 + 0);
+                nl_1[h][1] = __ldg(loc + (int64_t)j_1[h] * 3 + 1);
+                nl_1[h][2] = __ldg(loc + (int64_t)j_1[h] * 3 + 2);
+            }
+        }
+    }
+    __device__ __forceinline__ void make_cur() {
+        q0 = pq0_1;
+        cnt = pcnt_1;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            j[h] = j_1[h];
+            const bool v = slot + 8 * h < pcnt_1;
+            o[h][0] = v ? nl_1[h][0] - lp0_1 : 0.f;
+            o[h][1] = v ? nl_1[h][1] - lp1_1 : 0.f;
+            o[h][2] = v ? nl_1[h][2] - lp2_1 : 0.f;
+        }
+    }
+    __device__ __forceinline__ void start(const float *rows_, int64_t ld_, const float *loc_, Csr csr_, int64_t total_,
+                                          int k_, ItemMap map, int64_t n_items, int lane) {
+        rows = rows_;
+        ld = ld_;
+        loc = loc_;
+        csr = csr_;
+        total = total_;
+        k = k_;
+        im = map;
+        items = n_items;
+        pt = lane >> 3;
+        cl = lane & 7;
+        slot = lane & 7;
+        int32_t a0, c0;
+        load_off(0, a0, c0);
+        load_ent(0, a0, c0);
+        load_pos();
+        make_cur();  // item 0 (blocking, once)
+        load_off(1, a0, c0);
+        load_ent(1, a0, c0);
+        load_off(2, oq0_3, ocnt_3);
+    }
+    template <int H>
+    __device__ __forceinline__ void half_batch(int mycnt, Mom &acc, const float4 (&v)[8]) const {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const float w0 = __shfl_sync(0xffffffffu, o[H][0], pt * 8 + q);
+            const float w1 = __shfl_sync(0xffffffffu, o[H][1], pt * 8 + q);
+            const float w2 = __shfl_sync(0xffffffffu, o[H][2], pt * 8 + q);
+            if (8 * H + q < mycnt) mom_add(acc, v[q], w0, w1, w2);
+        }
+    }
+    template <int H>
+    __device__ __forceinline__ void load_rows(int mycnt, float4 (&v)[8]) const {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int32_t jj = __shfl_sync(0xffffffffu, j[H], pt * 8 + q);
+            v[q] = (8 * H + q < mycnt) ? __ldg(reinterpret_cast<const float4 *>(rows + (int64_t)jj * ld) + cl)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+    __device__ __forceinline__ void gather(int64_t w, Mom &acc) {
+        const int mycnt = __shfl_sync(0xffffffffu, cnt, pt * 8);
+        const int maxcnt = (int)__reduce_max_sync(0xffffffffu, (uint32_t)max(cnt, 0));
+        mom_zero(acc);
+        float4 v[8];
+        load_rows<0>(mycnt, v);
+        load_pos();                      // item w+1: source positions
+        load_ent(w + 2, oq0_3, ocnt_3);  // item w+2: list entries
+        load_off(w + 3, oq0_3, ocnt_3);  // item w+3: list ranges
+        half_batch<0>(mycnt, acc, v);
+        if (maxcnt > 8) {
+            load_rows<1>(mycnt, v);
+            half_batch<1>(mycnt, acc, v);
+        }
+        if (maxcnt > 16) {
+            // tail: lists longer than 16 entries, unpipelined, still in list order
+            const int64_t myp = im.p0(w) + pt;
+            const float lp0 = myp < total ? __ldg(loc + myp * 3 + 0) : 0.f;
+            const float lp1 = myp < total ? __ldg(loc + myp * 3 + 1) : 0.f;
+            const float lp2 = myp < total ? __ldg(loc + myp * 3 + 2) : 0.f;
+            for (int b0 = 16; b0 < maxcnt; b0 += 8) {
+                int32_t jt = 0;
+                float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+                if (b0 + slot < cnt) {
+                    jt = __ldg(csr.ent + q0 + b0 + slot) / k;
+                    t0 = __ldg(loc + (int64_t)jt * 3 + 0) - lp0;
+                    t1 = __ldg(loc + (int64_t)jt * 3 + 1) - lp1;
+                    t2 = __ldg(loc + (int64_t)jt * 3 + 2) - lp2;
+                }
+                for (int q = 0; q < 8; ++q) {
+                    const int32_t jj = __shfl_sync(0xffffffffu, jt, pt * 8 + q);
+                    const float w0 = __shfl_sync(0xffffffffu, t0, pt * 8 + q);
+                    const float w1 = __shfl_sync(0xffffffffu, t1, pt * 8 + q);
+                    const float w2 = __shfl_sync(0xffffffffu, t2, pt * 8 + q);
+                    if (b0 + q < mycnt) {
+                        const float4 x = __ldg(reinterpret_cast<const float4 *>(rows + (int64_t)jj * ld) + cl);
+                        mom_add(acc, x, w0, w1, w2);
+                    }
+                }
+            }
+        }
+    }
+    __device__ __forceinline__ void advance() { make_cur(); }
+};
+
 // ---------------------------------------------------------------------------------
 // Accumulator drain of tile i by one epilogue warp (TMEM lane quadrant = warp % 4): one
 // thread per output row.  Kept out of line so that its registers do not add to the live
@@ -845,6 +1009,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gmc_kernel(TcArgs a) {
             FwdPipe8<GC> pipe;
             pipe.start(GatherSrc{a.rows, a.loc, a.nbr, a.total, a.n, a.ld_rows},
                        ItemMap{G::GPW, gw * G::PPI, kGatherWarps * G::PPI}, items, lane);
+            for (int64_t w = 0; w < items; ++w) {
+                Mom acc;
+                pipe.gather(w, acc);
+                finish(w, item_p0(w), acc);
+                pipe.advance();
+            }
+        } else if (REVERSE && GC == 32 && !a.no_pipe32) {
+            RevPipe8x2 pipe;
+            pipe.start(a.rows, a.ld_rows, a.loc, a.csr, a.total, a.k, ItemMap{G::GPW, gw * G::PPI, kGatherWarps * G::PPI}, items,
+                       lane);
             for (int64_t w = 0; w < items; ++w) {
                 Mom acc;
                 pipe.gather(w, acc);
@@ -1305,6 +1479,14 @@ static int launch_tc(const TcArgs &a0, int cin, int cout, const float *theta, co
         a.binv = binv;
     }
     a.num_tiles = ceil_div(a.total, kTcM);
+    {
+        static int off = -1;
+        if (off < 0) {
+            const char *e = getenv("FC_NO_REVPIPE32");
+            off = (e && e[0] == '1') ? 1 : 0;
+        }
+        a.no_pipe32 = off;
+    }
     static uint64_t attr = 0;
     if (first_use_on_device(attr)) {
         cudaFuncSetAttribute(tc_gmc_kernel<GC, NOUT, SPLIT, REVERSE, KFIX, DLOC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
