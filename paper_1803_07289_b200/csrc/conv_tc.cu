@@ -1683,12 +1683,53 @@ static int generic_dtheta_block(int64_t total, int64_t n, int k, const float *fe
     return launch_dtheta_reduce<float>(2 * grid, cin, 3, cout, a.partial, d_theta, d_theta_b, st, 0, ld_dt);
 }
 
+// Without the location gradient, d_theta and d_features of a backward are independent: the
+// d_theta kernels go to a side stream while the reverse pass runs on the caller's, so one
+// latency-bound kernel's tail overlaps the other's start (fork / join by events, so a graph
+// capture of the caller's stream includes it; FC_NO_SIDE_BWD=1 runs them in sequence).
+struct SideFork {
+    cudaStream_t main, side;
+    bool on;
+    cudaEvent_t join_ev{};
+    SideFork(cudaStream_t m, bool enable) : main(m), side(m), on(false) {
+        static int off = -1;
+        if (off < 0) {
+            const char *e = getenv("FC_NO_SIDE_BWD");
+            off = (e && e[0] == '1') ? 1 : 0;
+        }
+        if (!enable || off) return;
+        static thread_local cudaStream_t ss[64];
+        static thread_local cudaEvent_t ev[64][2];
+        static thread_local uint64_t made = 0;
+        const int dev = current_device() & 63;
+        if (first_use_on_device(made)) {
+            cudaStreamCreateWithFlags(&ss[dev], cudaStreamNonBlocking);
+            cudaEventCreateWithFlags(&ev[dev][0], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&ev[dev][1], cudaEventDisableTiming);
+        }
+        on = true;
+        side = ss[dev];
+        join_ev = ev[dev][1];
+        cudaEventRecord(ev[dev][0], m);
+        cudaStreamWaitEvent(side, ev[dev][0], 0);
+    }
+    void join() {
+        if (!on) return;
+        cudaEventRecord(join_ev, side);
+        cudaStreamWaitEvent(main, join_ev, 0);
+        on = false;
+    }
+    ~SideFork() { join(); }
+};
+
 int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int cout, const float *g,
                 const float *feat, const float *loc, const int32_t *nbr, Csr csr, const float *theta,
                 const float *theta_b, float *d_features, float *d_locations, float *d_theta, float *d_theta_b,
                 cudaStream_t st) {
     (void)d;
     using L = DtLayout;
+    // without d_locations the d_theta kernels run on a side stream beside the reverse pass
+    SideFork sf(st, !d_locations && d_features && (d_theta || d_theta_b));
     const int64_t num_tiles = ceil_div(total, kTcM);
     // generic d_theta kernel: at most 8 tiles (1024 points, 128 tf32 k-steps) accumulated in
     // TMEM per CTA -- more CTAs (waves) instead of a longer truncating accumulation
@@ -1702,14 +1743,14 @@ int tc_backward(int mode, int64_t total, int64_t n, int cin, int d, int k, int c
             if (!centre_buf.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc backward)");
             centre = centre_buf.as<float>();
         }
-        rc = tc_fast_dtheta(total, n, feat, loc, nbr, g, theta, theta_b, d_theta, d_theta_b, centre, st);
+        rc = tc_fast_dtheta(total, n, feat, loc, nbr, g, theta, theta_b, d_theta, d_theta_b, centre, sf.side);
         if (rc) return rc;
     } else if (d_theta || d_theta_b || d_locations) {
-        centre_buf.alloc(sizeof(float) * total * 3, st);
+        centre_buf.alloc(sizeof(float) * total * 3, sf.side);
         if (!centre_buf.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc backward)");
         centre = centre_buf.as<float>();
         rc = generic_dtheta_block(total, n, k, feat, cin, loc, nbr, g, cout, theta, theta_b, cin, d_theta, d_theta_b,
-                                  cin, centre, false, st);
+                                  cin, centre, false, sf.side);
         if (rc) return rc;
     }
     if (d_features || d_locations) {
@@ -1812,6 +1853,7 @@ static bool concurrent_passes(int64_t total, int passes) {
     }
     return !off && passes > 1 && passes <= 4 && ceil_div(total, kTcM) * passes <= 2 * num_sms();
 }
+
 // dst[p, 0:w] (row stride ldd) += src[p, 0:w] (row stride lds), p < rows
 __global__ void add_rows_kernel(int64_t rows, int w, float *__restrict__ dst, int64_t ldd, const float *__restrict__ src,
                                 int64_t lds) {
@@ -2014,8 +2056,10 @@ int tc_blocked_deconv(int mode, int64_t total, int64_t n, int c_in, int k, int c
 int tc_blocked_backward(int mode, int64_t total, int64_t n, int c_in, int k, int c_out, const float *g,
                         const float *feat, const float *loc, const int32_t *nbr, Csr csr, const float *theta,
                         const float *theta_b, float *d_features, float *d_locations, float *d_theta,
-                        float *d_theta_b, cudaStream_t st) {
+                        float *d_theta_b, cudaStream_t st0) {
     Scratch centre_buf;
+    SideFork sf(st0, !d_locations && d_features && (d_theta || d_theta_b));
+    const cudaStream_t st = sf.side;  // d_theta section (the caller's stream unless forked)
     if (d_theta || d_theta_b || d_locations) {
         if (d_locations) {
             centre_buf.alloc(sizeof(float) * total * 3, st);
@@ -2072,12 +2116,14 @@ int tc_blocked_backward(int mode, int64_t total, int64_t n, int c_in, int k, int
         Scratch df_buf;
         float *df = d_features;
         if (!df) {
-            df_buf.alloc(sizeof(float) * total * c_in, st);
+            df_buf.alloc(sizeof(float) * total * c_in, st0);
             if (!df_buf.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (blocked backward)");
             df = df_buf.as<float>();
         }
-        return tc_blocked_reverse(mode, total, n, c_in, k, c_out, g, loc, csr, theta, theta_b, df, feat,
-                                  centre_buf.as<float>(), d_locations, st);
+        const int rc = tc_blocked_reverse(mode, total, n, c_in, k, c_out, g, loc, csr, theta, theta_b, df, feat,
+                                          centre_buf.as<float>(), d_locations, st0);
+        sf.join();
+        return rc;
     }
     return FC_OK;
 }
