@@ -163,10 +163,7 @@ def test_wide_fp32_default_route_is_hand_written_tcgen05(fc, shape):
     assert any("tc_dtheta_kernel" in k for k in names), names
 
 
-def test_concurrent_block_passes_bitwise_equal_sequential(tmp_path):
-    """Small clouds run the channel-blocked passes concurrently on side streams, each into its
-    own buffer, combined in the sequential accumulation order: bitwise the sequential result
-    (C2 shape: conv forward, backward with d_locations, flex_deconv)."""
+def _run_check_twice(tmp_path, knob):
     import subprocess
     import sys
 
@@ -174,10 +171,24 @@ def test_concurrent_block_passes_bitwise_equal_sequential(tmp_path):
     script = os.path.join(root, "scripts", "concurrent_passes_check.py")
     outs = []
     for flag in ("0", "1"):
-        f = tmp_path / f"c{flag}.npz"
-        env = dict(os.environ, FC_NO_CONCURRENT=flag)
+        f = tmp_path / f"{knob}{flag}.npz"
+        env = dict(os.environ, **{knob: flag})
         subprocess.run([sys.executable, script, str(f)], check=True, cwd=root, env=env)
         outs.append(np.load(f))
     a, b = outs
+    assert a.files == b.files and len(a.files) >= 10
     for key in a.files:
         assert np.array_equal(a[key], b[key]), key
+
+
+def test_concurrent_block_passes_bitwise_equal_sequential(tmp_path):
+    """Small clouds run the channel-blocked passes concurrently on side streams, each into its
+    own buffer, combined in the sequential accumulation order: bitwise the sequential result
+    (C2 shape: conv forward, backward with / without d_locations, flex_deconv)."""
+    _run_check_twice(tmp_path, "FC_NO_CONCURRENT")
+
+
+def test_side_stream_dtheta_bitwise_equal_sequential(tmp_path):
+    """Without d_locations, fc_conv_backward runs d_theta on a side stream beside the reverse
+    pass: bitwise the in-order result (C2 blocked, 64->64 fast kernels, 128->128 blocked)."""
+    _run_check_twice(tmp_path, "FC_NO_SIDE_BWD")
