@@ -74,6 +74,10 @@ struct FwdArgs {
     // e.g. the interior rows of a shard while its halo is in flight; null = every row
     const int32_t *rows;
     int64_t nrows;
+    // one 64 x 64 block of a wider conv (wide kernel): feature rows / output rows with these
+    // strides, the block's product added to out (acc) -- the channel-blocked engine's passes
+    int64_t ld_feat, ld_out;
+    int acc;
     int dbg;                    // timing-probe variants (FC_DBG): 2 no MMA, 8 gather+index only, 32 CTA-0 trace
     unsigned long long *trace;  // [24 warps][kTraceN]
 };
@@ -83,11 +87,17 @@ struct FwdArgs {
 template <bool SPLIT>
 __global__ void __launch_bounds__(1024) fwd_pack_b_kernel(const float *__restrict__ theta,
                                                           const float *__restrict__ theta_b, uint8_t *__restrict__ img,
-                                                          float *__restrict__ binv) {
+                                                          float *__restrict__ binv, int ld_cin) {
+    // theta / theta_b: the 64 x 64 block's first (c', c) of a theta with ld_cin input channels
     __shared__ float red[32];
     float m = 0.f;
-    for (int i = threadIdx.x; i < 64 * 64 * 3; i += blockDim.x) m = fmaxf(m, fabsf(theta[i]));
-    for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) m = fmaxf(m, fabsf(theta_b[i]));
+#pragma unroll 4
+    for (int i = threadIdx.x; i < 64 * 64 * 3; i += blockDim.x) {  // (unrolled: loads in flight)
+        const int cp = i / 192, r = i % 192;
+        m = fmaxf(m, fabsf(__ldg(theta + (int64_t)cp * ld_cin * 3 + r)));
+    }
+#pragma unroll 4
+    for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) m = fmaxf(m, fabsf(__ldg(theta_b + (int64_t)(i >> 6) * ld_cin + (i & 63))));
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
     __syncthreads();
@@ -106,7 +116,7 @@ __global__ void __launch_bounds__(1024) fwd_pack_b_kernel(const float *__restric
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < BN * 256; idx += gridDim.x * blockDim.x) {
         const int nn = idx >> 8, k = idx & 255;
         const int t = k >> 6, c = k & 63, cp = nn & 63;
-        const float v = ((t < 3) ? theta[(cp * 64 + c) * 3 + t] : theta_b[cp * 64 + c]) * sc;
+        const float v = ((t < 3) ? theta[((int64_t)cp * ld_cin + c) * 3 + t] : theta_b[(int64_t)cp * ld_cin + c]) * sc;
         uint16_t bits;
         if (SPLIT) {
             const __half hh = __float2half_rn(v);
@@ -167,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_fwd64_kernel(FwdArgs a) {
     {  // resident B image
         const uint4 *src = reinterpret_cast<const uint4 *>(a.bimg);
         uint4 *dst = reinterpret_cast<uint4 *>(smem + L::B_OFF);
-        for (int i = threadIdx.x; i < L::B_BYTES / 16; i += blockDim.x) dst[i] = src[i];
+        smem_fill16(dst, src, L::B_BYTES / 16);
     }
     fence_proxy_async_smem();
     tc_fence_before();
@@ -507,7 +517,7 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(a.bimg);
         uint4 *dst = reinterpret_cast<uint4 *>(smem + L::B_OFF);
-        for (int i = threadIdx.x; i < L::B_BYTES / 16; i += blockDim.x) dst[i] = src[i];
+        smem_fill16(dst, src, L::B_BYTES / 16);
     }
     fence_proxy_async_smem();
     tc_fence_before();
@@ -552,7 +562,7 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
             const float s0 = exp2i(rs[(b * 2 + 0) * kTile + t]) * binv;
             const float s1 = exp2i(rs[(b * 2 + 1) * kTile + t]) * binv;
             const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(b * 256);
-            float *orow = a.out + p * 64;
+            float *orow = a.out + p * a.ld_out;
 #pragma unroll 1
             for (int c0 = 0; c0 < 64; c0 += 16) {
                 float x0[16], x1[16], d[16];
@@ -570,6 +580,13 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
                     float o[16];
 #pragma unroll
                     for (int c = 0; c < 16; ++c) o[c] = fmaf(x1[c], s1, x0[c] * s0);
+                    if (a.acc) {  // block pass after the first: out += this block's product
+#pragma unroll
+                        for (int c = 0; c < 16; c += 4) {
+                            const float4 q = *reinterpret_cast<const float4 *>(orow + c0 + c);
+                            o[c] += q.x, o[c + 1] += q.y, o[c + 2] += q.z, o[c + 3] += q.w;
+                        }
+                    }
                     stg256(orow + c0, o);
                     stg256(orow + c0 + 8, o + 8);
                 }
@@ -651,10 +668,11 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
         auto load4 = [&](int i, int h, int b0) {
             const uint32_t es = E0 + (uint32_t)((i & 1) * L::E_STAGE + row * 16);
             const float *src = a.feat + 32 * h + 8 * cl;
+            const int64_t ldf = a.ld_feat;
 #pragma unroll
             for (int s2 = 0; s2 < 4; ++s2) {
                 const int32_t j = lds32(es + (uint32_t)((b0 + s2) * kTile * 16));
-                ldg_nc8(src + (int64_t)j * 64, v[s2]);
+                ldg_nc8(src + (int64_t)j * ldf, v[s2]);
             }
         };
         // x[t][c]: 4 components x 8 channels as float2 pairs
@@ -751,16 +769,29 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
 }  // namespace fast
 
 // forward for c_in = c_out = 64, k = 8, d = 3 (the bench / C3 / C4 shape)
+int tc_fast_forward_block(bool split, int64_t total, int64_t n, const float *feat, int64_t ld_feat, const float *loc,
+                          const int32_t *nbr, const float *theta, const float *theta_b, int ld_cin, float *out,
+                          int64_t ld_out, bool acc, cudaStream_t st, const int32_t *rows, int64_t nrows);
+
 int tc_fast_forward(bool split, int64_t total, int64_t n, const float *feat, const float *loc, const int32_t *nbr,
                     const float *theta, const float *theta_b, float *out, cudaStream_t st, const int32_t *rows,
                     int64_t nrows) {
+    return tc_fast_forward_block(split, total, n, feat, 64, loc, nbr, theta, theta_b, 64, out, 64, false, st, rows, nrows);
+}
+
+// one 64 x 64 channel block of a wider forward (feat / out row strides ld_feat / ld_out, theta
+// rows of ld_cin input channels; acc adds the block's product to out), or the whole 64 -> 64
+// conv (strides 64, no acc)
+int tc_fast_forward_block(bool split, int64_t total, int64_t n, const float *feat, int64_t ld_feat, const float *loc,
+                          const int32_t *nbr, const float *theta, const float *theta_b, int ld_cin, float *out,
+                          int64_t ld_out, bool acc, cudaStream_t st, const int32_t *rows, int64_t nrows) {
     using namespace fast;
     const size_t bbytes = split ? FwdL<true>::B_BYTES : FwdL<false>::B_BYTES;
     uint8_t *img = (uint8_t *)scratch_alloc(bbytes + 256, st);
     if (!img) return set_error(FC_ERR_CUDA, "scratch allocation failed (fast forward)");
     float *binv = reinterpret_cast<float *>(img + bbytes);
-    if (split) fwd_pack_b_kernel<true><<<FwdL<true>::BN * 256 / 1024, 1024, 0, st>>>(theta, theta_b, img, binv);
-    else fwd_pack_b_kernel<false><<<FwdL<false>::BN * 256 / 1024, 1024, 0, st>>>(theta, theta_b, img, binv);
+    if (split) fwd_pack_b_kernel<true><<<FwdL<true>::BN * 256 / 1024, 1024, 0, st>>>(theta, theta_b, img, binv, ld_cin);
+    else fwd_pack_b_kernel<false><<<FwdL<false>::BN * 256 / 1024, 1024, 0, st>>>(theta, theta_b, img, binv, ld_cin);
     count_launch();
     FwdArgs a{};
     a.total = total;
@@ -774,6 +805,9 @@ int tc_fast_forward(bool split, int64_t total, int64_t n, const float *feat, con
     a.bimg = img;
     a.binv = binv;
     a.out = out;
+    a.ld_feat = ld_feat;
+    a.ld_out = ld_out;
+    a.acc = acc ? 1 : 0;
     {
         const char *e = getenv("FC_DBG");
         a.dbg = e ? atoi(e) : 0;
@@ -792,6 +826,8 @@ int tc_fast_forward(bool split, int64_t total, int64_t n, const float *feat, con
         narrow = (e && e[0] == '1') ? 1 : 0;
     }
     if (rows && narrow) return set_error(FC_ERR_UNSUPPORTED, "row-list forward needs the wide kernel");
+    if ((ld_feat != 64 || ld_out != 64 || acc) && narrow)
+        return set_error(FC_ERR_UNSUPPORTED, "channel-block forward needs the wide kernel");
     if (a.num_tiles == 0) {
         prof_end(st);
         scratch_free(img, st);

@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(dThreads, 1) tc_dt64_kernel(DtArgs2 a) {
         for (int h = 0; h < 2; ++h) {
             const uint4 *src = reinterpret_cast<const uint4 *>(a.bimg + h * img_b);
             uint4 *dst = reinterpret_cast<uint4 *>(smem + L::BZ_OFF + h * 3 * L::BZ);
-            for (int i = threadIdx.x; i < 3 * L::BZ / 16; i += blockDim.x) dst[i] = src[i];
+            smem_fill16(dst, src, 3 * L::BZ / 16);
         }
     }
     fence_proxy_async_smem();

@@ -79,6 +79,8 @@ struct RevArgs {
     const float *binv;
     float *out;           // [total, 64]
     const float *feat;    // location gradient only: conv input features [total, 64]
+    int64_t ld_rows, ld_out;  // wide kernel: row strides of rows / out (a 64 x 64 channel block)
+    int acc;                  // wide kernel: out += this block's product
     const float *centre;  // centre-role term [total, 3]
     float *dloc;          // [total, 3] or null
     int dbg;              // timing probes (FC_DBG): 2 no MMA, 8 gather + index only, 16 first 8 slots only (wrong results)
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(rThreads, 1) tc_rev64_kernel(RevArgs a) {
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(a.bimg);
         uint4 *dst = reinterpret_cast<uint4 *>(smem + L::B_OFF);
-        for (int i = threadIdx.x; i < L::NS * L::B_BYTES / 16; i += blockDim.x) dst[i] = src[i];
+        smem_fill16(dst, src, L::NS * L::B_BYTES / 16);
     }
     if (threadIdx.x < rStages) {  // zero entries: row 0 of the zero row, zero offsets
         float4 *z = reinterpret_cast<float4 *>(smem + L::E_OFF + threadIdx.x * L::E_STAGE + rCap * 16);
@@ -624,7 +626,7 @@ __global__ void __launch_bounds__(wrThreads, 1) tc_rev64w_kernel(RevArgs a) {
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(a.bimg);
         uint4 *dst = reinterpret_cast<uint4 *>(smem + L::B_OFF);
-        for (int i = threadIdx.x; i < L::NS * L::B_BYTES / 16; i += blockDim.x) dst[i] = src[i];
+        smem_fill16(dst, src, L::NS * L::B_BYTES / 16);
     }
     if (threadIdx.x < rStages) {  // zero entries: row 0 of the zero row, zero offsets
         float4 *z = reinterpret_cast<float4 *>(smem + L::E_OFF + threadIdx.x * L::E_STAGE + rCap * 16);
@@ -694,7 +696,7 @@ __global__ void __launch_bounds__(wrThreads, 1) tc_rev64w_kernel(RevArgs a) {
             const float s1 = exp2i(rs[(b * 2 + 1) * kTile + tr]) * binv;
             const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16);
             const bool pv = p < a.total;
-            float *orow = a.out + p * 64;
+            float *orow = a.out + p * a.ld_out;
 #pragma unroll 1
             for (int c0 = 0; c0 < 64; c0 += 16) {
                 float x0[16], x1[16];
@@ -704,6 +706,13 @@ __global__ void __launch_bounds__(wrThreads, 1) tc_rev64w_kernel(RevArgs a) {
                     float o[16];
 #pragma unroll
                     for (int c = 0; c < 16; ++c) o[c] = fmaf(x1[c], s1, x0[c] * s0);
+                    if (a.acc) {  // block pass after the first: out += this block's product
+#pragma unroll
+                        for (int c = 0; c < 16; c += 4) {
+                            const float4 q = *reinterpret_cast<const float4 *>(orow + c0 + c);
+                            o[c] += q.x, o[c + 1] += q.y, o[c + 2] += q.z, o[c + 3] += q.w;
+                        }
+                    }
                     stg256(orow + c0, o);
                     stg256(orow + c0 + 8, o + 8);
                 }
@@ -900,7 +909,7 @@ __global__ void __launch_bounds__(wrThreads, 1) tc_rev64w_kernel(RevArgs a) {
                 const int sl = b0 + s2;
                 const bool ok = sl < it.cnt;
                 const int32_t j = lds32(ok ? it.eb + (uint32_t)(sl * 16) : it.ez);
-                ldg_nc8r_if(src + (int64_t)j * 64, v[s2], ok);
+                ldg_nc8r_if(src + (int64_t)j * a.ld_rows, v[s2], ok);
             }
         };
         auto fma4w = [&](const ItemW &it, int b0) {
@@ -945,7 +954,7 @@ __global__ void __launch_bounds__(wrThreads, 1) tc_rev64w_kernel(RevArgs a) {
                                         __ldg(a.loc + (int64_t)jr * 3 + 1) - lp1, __ldg(a.loc + (int64_t)jr * 3 + 2) - lp2);
                     }
                     float r[8];
-                    ldg_nc8r(src + (int64_t)__float_as_int(e.x) * 64, r);
+                    ldg_nc8r(src + (int64_t)__float_as_int(e.x) * a.ld_rows, r);
                     const float2 w0 = make_float2(e.y, e.y), w1 = make_float2(e.z, e.z), w2 = make_float2(e.w, e.w);
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
@@ -1041,14 +1050,35 @@ __global__ void __launch_bounds__(wrThreads, 1) tc_rev64w_kernel(RevArgs a) {
 
 }  // namespace fast
 
-void launch_pack_b(bool split, int cin, int cout, const float *theta, const float *theta_b, int reverse, int nout,
-                   int gc, uint8_t *img, float *binv, cudaStream_t st);
+void launch_pack_b_ld(bool split, int cin, int cout, int ld_cin, const float *theta, const float *theta_b, int reverse,
+                      int nout, int gc, uint8_t *img, float *binv, cudaStream_t st);
+
+static int fast_reverse_impl(bool split, int64_t total, int k, const float *rows, int64_t ld_rows, const float *loc,
+                             Csr csr, const float *theta, const float *theta_b, int ld_cin, float *out, int64_t ld_out,
+                             bool acc, const float *feat, const float *centre, float *dloc, cudaStream_t st);
 
 // reverse pass for c_in = c_out = 64, d = 3: out = A(theta)^T rows (d_features / flex_deconv),
 // plus the neighbour-role location gradient when dloc is non-null
 int tc_fast_reverse(bool split, int64_t total, int k, const float *rows, const float *loc, Csr csr, const float *theta,
                     const float *theta_b, float *out, const float *feat, const float *centre, float *dloc,
                     cudaStream_t st) {
+    return fast_reverse_impl(split, total, k, rows, 64, loc, csr, theta, theta_b, 64, out, 64, false, feat, centre, dloc,
+                             st);
+}
+
+// one 64 x 64 channel block of a wider reverse pass (no location gradient): gathered rows /
+// output rows with strides ld_rows / ld_out, theta rows of ld_cin input channels, the block's
+// product added to out when acc
+int tc_fast_reverse_block(bool split, int64_t total, int k, const float *rows, int64_t ld_rows, const float *loc,
+                          Csr csr, const float *theta, const float *theta_b, int ld_cin, float *out, int64_t ld_out,
+                          bool acc, cudaStream_t st) {
+    return fast_reverse_impl(split, total, k, rows, ld_rows, loc, csr, theta, theta_b, ld_cin, out, ld_out, acc, nullptr,
+                             nullptr, nullptr, st);
+}
+
+static int fast_reverse_impl(bool split, int64_t total, int k, const float *rows, int64_t ld_rows, const float *loc,
+                             Csr csr, const float *theta, const float *theta_b, int ld_cin, float *out, int64_t ld_out,
+                             bool acc, const float *feat, const float *centre, float *dloc, cudaStream_t st) {
     using namespace fast;
     const size_t bbytes = (size_t)RevL<true>::B_BYTES * (split ? 2 : 1);
     uint8_t *img = (uint8_t *)scratch_alloc(bbytes + 512, st);
@@ -1056,7 +1086,7 @@ int tc_fast_reverse(bool split, int64_t total, int k, const float *rows, const f
     float *binv = reinterpret_cast<float *>(img + bbytes);
     float *zero = reinterpret_cast<float *>(img + bbytes + 256);
     cudaMemsetAsync(zero, 0, 256, st);
-    launch_pack_b(split, 64, 64, theta, theta_b, 1, 64, 64, img, binv, st);
+    launch_pack_b_ld(split, 64, 64, ld_cin, theta, theta_b, 1, 64, 64, img, binv, st);
     RevArgs a{};
     a.total = total;
     a.num_tiles = ceil_div(total, kTile);
@@ -1071,6 +1101,9 @@ int tc_fast_reverse(bool split, int64_t total, int k, const float *rows, const f
     a.feat = feat;
     a.centre = centre;
     a.dloc = dloc;
+    a.ld_rows = ld_rows;
+    a.ld_out = ld_out;
+    a.acc = acc ? 1 : 0;
     {
         const char *e = getenv("FC_DBG");
         a.dbg = e ? atoi(e) : 0;
@@ -1081,6 +1114,11 @@ int tc_fast_reverse(bool split, int64_t total, int k, const float *rows, const f
     if (narrow < 0) {
         const char *e = getenv("FC_REV_NARROW");
         narrow = (e && e[0] == '1') ? 1 : 0;
+    }
+    if ((ld_rows != 64 || ld_out != 64 || acc) && (narrow || dloc)) {
+        prof_end(st);
+        scratch_free(img, st);
+        return set_error(FC_ERR_UNSUPPORTED, "channel-block reverse needs the wide kernel without d_locations");
     }
 #define FC_LAUNCH_REV(S, D)                                                                                     \
     do {                                                                                                        \

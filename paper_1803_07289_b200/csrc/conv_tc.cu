@@ -118,10 +118,13 @@ __device__ __forceinline__ void pack_b_body(int cin, int cout, int ld_cin, const
     __shared__ float red[32];
     float m = 0.f;
     const int ntb = cout * cin;
+    // unrolled: the loads of several iterations in flight (the loop-carried max would otherwise
+    // serialise one L2 round trip per iteration)
+#pragma unroll 4
     for (int i = threadIdx.x; i < ntb; i += blockDim.x) {
         const int64_t e = (int64_t)(i / cin) * ld_cin + i % cin;
-        m = fmaxf(m, fmaxf(fabsf(theta_b[e]), fmaxf(fabsf(theta[e * 3]), fmaxf(fabsf(theta[e * 3 + 1]),
-                                                                                  fabsf(theta[e * 3 + 2])))));
+        m = fmaxf(m, fmaxf(fabsf(__ldg(theta_b + e)), fmaxf(fabsf(__ldg(theta + e * 3)), fmaxf(fabsf(__ldg(theta + e * 3 + 1)),
+                                                                                          fabsf(__ldg(theta + e * 3 + 2))))));
     }
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
@@ -839,7 +842,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gmc_kernel(TcArgs a) {
         const uint4 *src = reinterpret_cast<const uint4 *>(a.bimg);
         uint4 *dst = reinterpret_cast<uint4 *>(B_hi);
         const int nvec = L::B_BYTES * L::NSPLIT / 16;
-        for (int i = threadIdx.x; i < nvec; i += blockDim.x) dst[i] = src[i];
+        smem_fill16(dst, src, nvec);
     }
     const float binv = a.binv[0];
     fence_proxy_async_smem();
@@ -1202,7 +1205,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
         for (int h = 0; h < 2; ++h) {
             const uint4 *src = reinterpret_cast<const uint4 *>(a.bimg + h * img_b);
             uint4 *dst = reinterpret_cast<uint4 *>(smem + L::B_OFF + h * 3 * L::BZ);
-            for (int i = threadIdx.x; i < 3 * L::BZ / 16; i += blockDim.x) dst[i] = src[i];
+            smem_fill16(dst, src, 3 * L::BZ / 16);
         }
     }
     const float binv = L::Z ? a.binv[0] : 1.f;
@@ -1557,12 +1560,16 @@ int tc_conv_forward_supported(int mode, int c_in, int d, int k, int c_out) {
     return tc_shape_ok(mode, c_in, d, c_out) ? 1 : 0;
 }
 
+void launch_pack_b_ld(bool split, int cin, int cout, int ld_cin, const float *theta, const float *theta_b, int reverse,
+                      int nout, int gc, uint8_t *img, float *binv, cudaStream_t st) {
+    const unsigned g = (unsigned)ceil_div((int64_t)nout * 4 * gc, 1024);
+    if (split) tc_pack_b_kernel<true><<<g, 1024, 0, st>>>(cin, cout, ld_cin, theta, theta_b, reverse, nout, gc, img, binv);
+    else tc_pack_b_kernel<false><<<g, 1024, 0, st>>>(cin, cout, ld_cin, theta, theta_b, reverse, nout, gc, img, binv);
+    count_launch();
+}
 void launch_pack_b(bool split, int cin, int cout, const float *theta, const float *theta_b, int reverse, int nout,
                    int gc, uint8_t *img, float *binv, cudaStream_t st) {
-    const unsigned g = (unsigned)ceil_div((int64_t)nout * 4 * gc, 1024);
-    if (split) tc_pack_b_kernel<true><<<g, 1024, 0, st>>>(cin, cout, cin, theta, theta_b, reverse, nout, gc, img, binv);
-    else tc_pack_b_kernel<false><<<g, 1024, 0, st>>>(cin, cout, cin, theta, theta_b, reverse, nout, gc, img, binv);
-    count_launch();
+    launch_pack_b_ld(split, cin, cout, cin, theta, theta_b, reverse, nout, gc, img, binv, st);
 }
 
 int tc_fast_forward(bool split, int64_t total, int64_t n, const float *feat, const float *loc, const int32_t *nbr,
@@ -1905,9 +1912,38 @@ int tc_blocked_supported(int mode, int c_in, int d, int c_out) {
     return (d == 3 && mode != FC_MODE_SIMT && c_in % 64 == 0 && c_out % 64 == 0 && (c_in > 64 || c_out > 64)) ? 1 : 0;
 }
 
+int tc_fast_forward_block(bool split, int64_t total, int64_t n, const float *feat, int64_t ld_feat, const float *loc,
+                          const int32_t *nbr, const float *theta, const float *theta_b, int ld_cin, float *out,
+                          int64_t ld_out, bool acc, cudaStream_t st, const int32_t *rows, int64_t nrows);
+
+// Channel blocks on the 64 -> 64 K = 8 headline kernels (warp-specialised gather, 8-channel
+// lanes): for clouds large enough to fill the GPU with one pass, each of the
+// (c_in / 64) x (c_out / 64) block pairs is one fast pass, the input blocks of an output
+// block accumulated in ascending order in the epilogue.  FC_BLOCK_FAST=0 keeps the generic
+// 32-channel-gather engine below for A/B.
+static bool block_fast(int64_t total, int k, int c_in, int c_out) {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("FC_BLOCK_FAST");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on && fast_enabled() && k == kSlots && c_in % 64 == 0 && c_out % 64 == 0 &&
+           ceil_div(total, kTcM) >= num_sms();
+}
+
 int tc_blocked_forward(int mode, int64_t total, int64_t n, int c_in, int k, int c_out, const float *feat,
                        const float *loc, const int32_t *nbr, const float *theta, const float *theta_b, float *out,
                        cudaStream_t st) {
+    if (block_fast(total, k, c_in, c_out)) {
+        for (int o0 = 0; o0 < c_out; o0 += 64)
+            for (int i0 = 0; i0 < c_in; i0 += 64) {
+                const int rc = tc_fast_forward_block(mode != FC_MODE_TC_BF16, total, n, feat + i0, c_in, loc, nbr,
+                                                     theta + ((int64_t)o0 * c_in + i0) * 3, theta_b + (int64_t)o0 * c_in + i0,
+                                                     c_in, out + o0, c_out, i0 > 0, st, nullptr, 0);
+                if (rc) return rc;
+            }
+        return FC_OK;
+    }
     // each 32-channel block of the input is gathered ONCE and contracted against all (up to
     // 256) output channels in one pass (N = 128 / 256 accumulators), the blocks' products
     // summed in the epilogue (acc): the gather -- the kernel's cost -- is not repeated per
@@ -1969,9 +2005,23 @@ int tc_blocked_forward(int mode, int64_t total, int64_t n, int c_in, int k, int 
 // Reverse pass over blocks: out [total, c_in] = sum over gathered c' blocks of the block
 // products (d_features of the backward, or flex_deconv); with dloc, the neighbour role of
 // the location gradient (dloc = centre - sum of the blocks' terms).
+int tc_fast_reverse_block(bool split, int64_t total, int k, const float *rows, int64_t ld_rows, const float *loc,
+                          Csr csr, const float *theta, const float *theta_b, int ld_cin, float *out, int64_t ld_out,
+                          bool acc, cudaStream_t st);
+
 static int tc_blocked_reverse(int mode, int64_t total, int64_t n, int c_in, int k, int c_out, const float *rows,
                               const float *loc, Csr csr, const float *theta, const float *theta_b, float *out,
                               const float *feat, const float *centre, float *dloc, cudaStream_t st) {
+    if (!dloc && block_fast(total, k, c_in, c_out)) {  // 64 x 64 blocks on the headline reverse kernel
+        for (int i0 = 0; i0 < c_in; i0 += 64)
+            for (int j0 = 0; j0 < c_out; j0 += 64) {
+                const int rc = tc_fast_reverse_block(mode != FC_MODE_TC_BF16, total, k, rows + j0, c_out, loc, csr,
+                                                     theta + ((int64_t)j0 * c_in + i0) * 3, theta_b + (int64_t)j0 * c_in + i0,
+                                                     c_in, out + i0, c_in, j0 > 0, st);
+                if (rc) return rc;
+            }
+        return FC_OK;
+    }
     // gathered (c') blocks of 32 channels, each gathered once per output block of up to 256
     // channels (64-channel gathers for a 64-wide output block, e.g. with the location-gradient
     // epilogue, whose U accumulators need 4x the columns)

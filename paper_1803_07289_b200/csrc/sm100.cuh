@@ -14,6 +14,19 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Copy nvec 16-byte vectors global -> shared with the whole CTA: every thread issues all of its
+// cp.async copies before waiting once (a plain load/store loop waits out one L2 round trip per
+// iteration: ~6 us for a 64 KB operand image at kernel start).  The caller's __syncthreads
+// (and proxy fence, for tcgen05 operands) publishes the data.
+__device__ __forceinline__ void smem_fill16(void *dst, const void *src, int nvec) {
+    const uint32_t d = smem_u32(dst);
+    const char *s = static_cast<const char *>(src);
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16u * (uint32_t)i), "l"(s + 16 * (size_t)i)
+                     : "memory");
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");

@@ -192,3 +192,41 @@ def test_side_stream_dtheta_bitwise_equal_sequential(tmp_path):
     """Without d_locations, fc_conv_backward runs d_theta on a side stream beside the reverse
     pass: bitwise the in-order result (C2 blocked, 64->64 fast kernels, 128->128 blocked)."""
     _run_check_twice(tmp_path, "FC_NO_SIDE_BWD")
+
+
+@pytest.mark.parametrize("cin,cout", [(128, 128), (256, 128), (64, 192)])
+def test_wide_fast_channel_blocks_vs_oracle(fc, oracle_mod, cin, cout):
+    """Clouds that fill the GPU with one pass run the channel blocks on the 64 -> 64 K = 8
+    headline kernels (strided rows, ascending-block accumulation in the epilogue): 40 K
+    points, sampled rows of the forward / d_features and the full parameter gradients against
+    the oracle (fp32 tolerances of the module docstring)."""
+    import torch
+
+    n, k, d = 40_000, 8, 3
+    g = np.random.default_rng(cin + cout)
+    loc = np.floor(g.random((n, d)) * 2 ** 24) / 2 ** 24
+    order = np.lexsort((loc[:, 2], loc[:, 1], np.floor(loc[:, 0] * 64)))  # roughly local rows
+    loc = loc[order]
+    feat = g.standard_normal((n, cin)).astype(np.float32).astype(np.float64)
+    up = g.standard_normal((n, cout)).astype(np.float32).astype(np.float64)
+    th = (0.1 * g.standard_normal((cout, cin, d))).astype(np.float32).astype(np.float64)
+    tb = (0.1 * g.standard_normal((cout, cin))).astype(np.float32).astype(np.float64)
+    f32 = torch.float32
+    pos = _t(loc.astype(np.float32), f32)
+    from paper_1803_07289_b200 import _ops
+
+    nbr_t = _ops.knn(pos, 1, n, k)
+    nbr = nbr_t.cpu().numpy().astype(np.int64)
+    rows = np.unique(np.concatenate([np.arange(64), np.arange(n - 64, n), g.integers(0, n, 2000)]))
+    nb = fc.NeighborIndex(_t(nbr, torch.int64))
+    params = fc.FlexConvParams(_t(th, f32), _t(tb, f32))
+    locf = loc.astype(np.float32).astype(np.float64)
+    out = _np(fc.flex_conv_forward(_t(feat, f32), pos, nb, params))
+    ref = oracle_mod.conv_forward_rows(feat, locf, nbr, th, tb, rows)
+    np.testing.assert_allclose(out[rows], ref, rtol=1e-4, atol=1e-5)
+    gb = fc.flex_conv_backward(_t(up, f32), _t(feat, f32), pos, nb, params, with_locations=False)
+    df_ref, _ = oracle_mod.conv_backward_rows(up, feat, locf, nbr, th, tb, rows, with_locations=False)
+    np.testing.assert_allclose(_np(gb.d_features)[rows], df_ref, rtol=1e-4, atol=1e-5)
+    dth, dtb = oracle_mod.conv_param_grads(up, feat, locf, nbr)
+    _red_close(_np(gb.d_theta), dth, "d_theta")
+    _red_close(_np(gb.d_theta_b), dtb, "d_theta_b")
