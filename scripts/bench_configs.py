@@ -252,6 +252,8 @@ def c5(reps):
     x = torch.from_numpy(feats).cuda().float()
     lab = torch.from_numpy(labels).cuda()
     ms = timed(lambda: network.train_step(g, adam, h, x, lab), max(3, reps // 2), warmup=2)
+    graphed = network.GraphedTrainStep(g, adam, h, x, lab)  # the same step captured as one CUDA graph
+    ms_graph = timed(lambda: graphed(), max(3, reps // 2), warmup=2)
     # a GPU's batch-sharded share of B = 32 over 8 GPUs: 4 scenes, one fused pass
     # (train_step_batch(fused=True) over sampling.concat_hierarchies)
     scenes = [(h, x, lab)]
@@ -268,6 +270,7 @@ def c5(reps):
                      "(sampling.spatially_ordered)",
             "params": g.param_count(), "sizes": h.sizes(), "hierarchy_build_ms": round(hier_ms, 2),
             "train_step": row(ms, n),
+            "train_step_cuda_graph": row(ms_graph, n),
             "per_gpu_step_4_scenes_fused": row(ms4, 4 * n),
             "per_gpu_step_4_scenes_scene_loop": row(ms4_loop, 4 * n)}
 
