@@ -85,10 +85,11 @@ struct FwdArgs {
 // B image for the forward: B[n][k], k = t*64 + c (theta[n', c, t], t < 3 | theta_b[n', c]),
 // rows n < 64: hi (or bf16) of c' = n; rows 64..127 (split only): lo of c' = n - 64.
 template <bool SPLIT>
-__global__ void __launch_bounds__(1024) fwd_pack_b_kernel(const float *__restrict__ theta,
-                                                          const float *__restrict__ theta_b, uint8_t *__restrict__ img,
-                                                          float *__restrict__ binv, int ld_cin) {
-    // theta / theta_b: the 64 x 64 block's first (c', c) of a theta with ld_cin input channels
+__device__ __forceinline__ void fwd_pack_b_body(const float *__restrict__ theta, const float *__restrict__ theta_b,
+                                                uint8_t *__restrict__ img, float *__restrict__ binv, int ld_cin, int bx,
+                                                int gx) {
+    // theta / theta_b: the 64 x 64 block's first (c', c) of a theta with ld_cin input channels;
+    // (bx, gx): this CTA's slice of the image
     __shared__ float red[32];
     float m = 0.f;
 #pragma unroll 4
@@ -109,11 +110,11 @@ __global__ void __launch_bounds__(1024) fwd_pack_b_kernel(const float *__restric
     __syncthreads();
     int e = 0;
     if (SPLIT) e = scale_exp(red[0]);
-    if (blockIdx.x == 0 && threadIdx.x == 0) binv[0] = exp2i(e);
+    if (bx == 0 && threadIdx.x == 0) binv[0] = exp2i(e);
     const float sc = exp2i(-e);
     constexpr int BN = FwdL<SPLIT>::BN;
     // every block reduces the (L2-resident) max itself and packs its slice of the image
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < BN * 256; idx += gridDim.x * blockDim.x) {
+    for (int idx = bx * blockDim.x + threadIdx.x; idx < BN * 256; idx += gx * blockDim.x) {
         const int nn = idx >> 8, k = idx & 255;
         const int t = k >> 6, c = k & 63, cp = nn & 63;
         const float v = ((t < 3) ? theta[((int64_t)cp * ld_cin + c) * 3 + t] : theta_b[(int64_t)cp * ld_cin + c]) * sc;
@@ -126,6 +127,26 @@ __global__ void __launch_bounds__(1024) fwd_pack_b_kernel(const float *__restric
         }
         *reinterpret_cast<uint16_t *>(img + sw128_offset(nn, k, BN)) = bits;
     }
+}
+template <bool SPLIT>
+__global__ void __launch_bounds__(1024) fwd_pack_b_kernel(const float *__restrict__ theta,
+                                                          const float *__restrict__ theta_b, uint8_t *__restrict__ img,
+                                                          float *__restrict__ binv, int ld_cin) {
+    fwd_pack_b_body<SPLIT>(theta, theta_b, img, binv, ld_cin, blockIdx.x, gridDim.x);
+}
+// the images of a channel-blocked forward's passes in one launch (blockIdx.y = pass): image j
+// at img0 + j * stride, its 1 / scale right after the image bytes
+constexpr int kFwdPackBatch = 32;
+struct FwdPackJobs {
+    const float *theta[kFwdPackBatch];
+    const float *theta_b[kFwdPackBatch];
+};
+template <bool SPLIT>
+__global__ void __launch_bounds__(1024) fwd_pack_b_batch_kernel(const __grid_constant__ FwdPackJobs jobs, int ld_cin,
+                                                                uint8_t *__restrict__ img0, int64_t stride) {
+    uint8_t *img = img0 + (int64_t)blockIdx.y * stride;
+    fwd_pack_b_body<SPLIT>(jobs.theta[blockIdx.y], jobs.theta_b[blockIdx.y], img,
+                           reinterpret_cast<float *>(img + FwdL<SPLIT>::B_BYTES), ld_cin, blockIdx.x, gridDim.x);
 }
 
 constexpr int kTraceN = 2048;
@@ -771,7 +792,32 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
 // forward for c_in = c_out = 64, k = 8, d = 3 (the bench / C3 / C4 shape)
 int tc_fast_forward_block(bool split, int64_t total, int64_t n, const float *feat, int64_t ld_feat, const float *loc,
                           const int32_t *nbr, const float *theta, const float *theta_b, int ld_cin, float *out,
-                          int64_t ld_out, bool acc, cudaStream_t st, const int32_t *rows, int64_t nrows);
+                          int64_t ld_out, bool acc, cudaStream_t st, const int32_t *rows, int64_t nrows,
+                          const uint8_t *pre_img = nullptr);
+
+// bytes per pass image of pack_forward_blocks (image, 1 / scale, alignment)
+int64_t fast_forward_image_stride(bool split) {
+    using namespace fast;
+    const int64_t b = split ? FwdL<true>::B_BYTES : FwdL<false>::B_BYTES;
+    return (b + 256 + 1023) / 1024 * 1024;
+}
+
+// all passes' forward images of a channel-blocked forward in one launch (img0: njobs strides)
+int pack_forward_blocks(bool split, int njobs, const float *const *th, const float *const *tb, int ld_cin,
+                        uint8_t *img0, cudaStream_t st) {
+    using namespace fast;
+    const int64_t stride = fast_forward_image_stride(split);
+    for (int j0 = 0; j0 < njobs; j0 += kFwdPackBatch) {
+        const int nj = std::min(kFwdPackBatch, njobs - j0);
+        FwdPackJobs jobs{};
+        for (int j = 0; j < nj; ++j) jobs.theta[j] = th[j0 + j], jobs.theta_b[j] = tb[j0 + j];
+        uint8_t *img = img0 + (int64_t)j0 * stride;
+        if (split) fwd_pack_b_batch_kernel<true><<<dim3(FwdL<true>::BN * 256 / 1024, nj), 1024, 0, st>>>(jobs, ld_cin, img, stride);
+        else fwd_pack_b_batch_kernel<false><<<dim3(FwdL<false>::BN * 256 / 1024, nj), 1024, 0, st>>>(jobs, ld_cin, img, stride);
+        count_launch();
+    }
+    return check_launch("pack forward blocks");
+}
 
 int tc_fast_forward(bool split, int64_t total, int64_t n, const float *feat, const float *loc, const int32_t *nbr,
                     const float *theta, const float *theta_b, float *out, cudaStream_t st, const int32_t *rows,
@@ -784,15 +830,18 @@ int tc_fast_forward(bool split, int64_t total, int64_t n, const float *feat, con
 // conv (strides 64, no acc)
 int tc_fast_forward_block(bool split, int64_t total, int64_t n, const float *feat, int64_t ld_feat, const float *loc,
                           const int32_t *nbr, const float *theta, const float *theta_b, int ld_cin, float *out,
-                          int64_t ld_out, bool acc, cudaStream_t st, const int32_t *rows, int64_t nrows) {
+                          int64_t ld_out, bool acc, cudaStream_t st, const int32_t *rows, int64_t nrows,
+                          const uint8_t *pre_img) {
     using namespace fast;
     const size_t bbytes = split ? FwdL<true>::B_BYTES : FwdL<false>::B_BYTES;
-    uint8_t *img = (uint8_t *)scratch_alloc(bbytes + 256, st);
+    uint8_t *img = pre_img ? const_cast<uint8_t *>(pre_img) : (uint8_t *)scratch_alloc(bbytes + 256, st);
     if (!img) return set_error(FC_ERR_CUDA, "scratch allocation failed (fast forward)");
     float *binv = reinterpret_cast<float *>(img + bbytes);
-    if (split) fwd_pack_b_kernel<true><<<FwdL<true>::BN * 256 / 1024, 1024, 0, st>>>(theta, theta_b, img, binv, ld_cin);
-    else fwd_pack_b_kernel<false><<<FwdL<false>::BN * 256 / 1024, 1024, 0, st>>>(theta, theta_b, img, binv, ld_cin);
-    count_launch();
+    if (!pre_img) {
+        if (split) fwd_pack_b_kernel<true><<<FwdL<true>::BN * 256 / 1024, 1024, 0, st>>>(theta, theta_b, img, binv, ld_cin);
+        else fwd_pack_b_kernel<false><<<FwdL<false>::BN * 256 / 1024, 1024, 0, st>>>(theta, theta_b, img, binv, ld_cin);
+        count_launch();
+    }
     FwdArgs a{};
     a.total = total;
     a.n = n;
@@ -825,12 +874,14 @@ int tc_fast_forward_block(bool split, int64_t total, int64_t n, const float *fea
         const char *e = getenv("FC_FWD_NARROW");
         narrow = (e && e[0] == '1') ? 1 : 0;
     }
-    if (rows && narrow) return set_error(FC_ERR_UNSUPPORTED, "row-list forward needs the wide kernel");
-    if ((ld_feat != 64 || ld_out != 64 || acc) && narrow)
-        return set_error(FC_ERR_UNSUPPORTED, "channel-block forward needs the wide kernel");
+    if (narrow && (rows || ld_feat != 64 || ld_out != 64 || acc)) {
+        prof_end(st);
+        if (!pre_img) scratch_free(img, st);
+        return set_error(FC_ERR_UNSUPPORTED, "row-list / channel-block forward needs the wide kernel");
+    }
     if (a.num_tiles == 0) {
         prof_end(st);
-        scratch_free(img, st);
+        if (!pre_img) scratch_free(img, st);
         return FC_OK;
     }
     if (!narrow) {
@@ -862,7 +913,7 @@ int tc_fast_forward_block(bool split, int64_t total, int64_t n, const float *fea
     }
     prof_end(st);
     count_launch();
-    scratch_free(img, st);
+    if (!pre_img) scratch_free(img, st);
     if (a.dbg & 32) {
         static unsigned long long h[kWarps * kTraceN];
         cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, st);

@@ -1055,7 +1055,8 @@ void launch_pack_b_ld(bool split, int cin, int cout, int ld_cin, const float *th
 
 static int fast_reverse_impl(bool split, int64_t total, int k, const float *rows, int64_t ld_rows, const float *loc,
                              Csr csr, const float *theta, const float *theta_b, int ld_cin, float *out, int64_t ld_out,
-                             bool acc, const float *feat, const float *centre, float *dloc, cudaStream_t st);
+                             bool acc, const float *feat, const float *centre, float *dloc, cudaStream_t st,
+                             const uint8_t *pre_img = nullptr, const float *pre_zero = nullptr);
 
 // reverse pass for c_in = c_out = 64, d = 3: out = A(theta)^T rows (d_features / flex_deconv),
 // plus the neighbour-role location gradient when dloc is non-null
@@ -1069,24 +1070,30 @@ int tc_fast_reverse(bool split, int64_t total, int k, const float *rows, const f
 // one 64 x 64 channel block of a wider reverse pass (no location gradient): gathered rows /
 // output rows with strides ld_rows / ld_out, theta rows of ld_cin input channels, the block's
 // product added to out when acc
+// (pre_img: this block's reverse image already packed -- tc_pack_b layout, 1 / scale after it --
+// and pre_zero: 64 zero floats, both from the caller; null = packed / zeroed here)
 int tc_fast_reverse_block(bool split, int64_t total, int k, const float *rows, int64_t ld_rows, const float *loc,
                           Csr csr, const float *theta, const float *theta_b, int ld_cin, float *out, int64_t ld_out,
-                          bool acc, cudaStream_t st) {
+                          bool acc, cudaStream_t st, const uint8_t *pre_img, const float *pre_zero) {
     return fast_reverse_impl(split, total, k, rows, ld_rows, loc, csr, theta, theta_b, ld_cin, out, ld_out, acc, nullptr,
-                             nullptr, nullptr, st);
+                             nullptr, nullptr, st, pre_img, pre_zero);
 }
 
 static int fast_reverse_impl(bool split, int64_t total, int k, const float *rows, int64_t ld_rows, const float *loc,
                              Csr csr, const float *theta, const float *theta_b, int ld_cin, float *out, int64_t ld_out,
-                             bool acc, const float *feat, const float *centre, float *dloc, cudaStream_t st) {
+                             bool acc, const float *feat, const float *centre, float *dloc, cudaStream_t st,
+                             const uint8_t *pre_img, const float *pre_zero) {
     using namespace fast;
     const size_t bbytes = (size_t)RevL<true>::B_BYTES * (split ? 2 : 1);
-    uint8_t *img = (uint8_t *)scratch_alloc(bbytes + 512, st);
+    const bool own = !(pre_img && pre_zero);
+    uint8_t *img = own ? (uint8_t *)scratch_alloc(bbytes + 512, st) : const_cast<uint8_t *>(pre_img);
     if (!img) return set_error(FC_ERR_CUDA, "scratch allocation failed (fast reverse)");
     float *binv = reinterpret_cast<float *>(img + bbytes);
-    float *zero = reinterpret_cast<float *>(img + bbytes + 256);
-    cudaMemsetAsync(zero, 0, 256, st);
-    launch_pack_b_ld(split, 64, 64, ld_cin, theta, theta_b, 1, 64, 64, img, binv, st);
+    float *zero = own ? reinterpret_cast<float *>(img + bbytes + 256) : const_cast<float *>(pre_zero);
+    if (own) {
+        cudaMemsetAsync(zero, 0, 256, st);
+        launch_pack_b_ld(split, 64, 64, ld_cin, theta, theta_b, 1, 64, 64, img, binv, st);
+    }
     RevArgs a{};
     a.total = total;
     a.num_tiles = ceil_div(total, kTile);
@@ -1117,7 +1124,7 @@ static int fast_reverse_impl(bool split, int64_t total, int k, const float *rows
     }
     if ((ld_rows != 64 || ld_out != 64 || acc) && (narrow || dloc)) {
         prof_end(st);
-        scratch_free(img, st);
+        if (own) scratch_free(img, st);
         return set_error(FC_ERR_UNSUPPORTED, "channel-block reverse needs the wide kernel without d_locations");
     }
 #define FC_LAUNCH_REV(S, D)                                                                                     \
@@ -1146,7 +1153,7 @@ static int fast_reverse_impl(bool split, int64_t total, int k, const float *rows
 #undef FC_LAUNCH_REV
     prof_end(st);
     count_launch();
-    scratch_free(img, st);
+    if (own) scratch_free(img, st);
     return check_launch("tc_rev64_kernel");
 }
 

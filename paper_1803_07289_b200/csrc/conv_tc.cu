@@ -1914,7 +1914,11 @@ int tc_blocked_supported(int mode, int c_in, int d, int c_out) {
 
 int tc_fast_forward_block(bool split, int64_t total, int64_t n, const float *feat, int64_t ld_feat, const float *loc,
                           const int32_t *nbr, const float *theta, const float *theta_b, int ld_cin, float *out,
-                          int64_t ld_out, bool acc, cudaStream_t st, const int32_t *rows, int64_t nrows);
+                          int64_t ld_out, bool acc, cudaStream_t st, const int32_t *rows, int64_t nrows,
+                          const uint8_t *pre_img);
+int64_t fast_forward_image_stride(bool split);
+int pack_forward_blocks(bool split, int njobs, const float *const *th, const float *const *tb, int ld_cin,
+                        uint8_t *img0, cudaStream_t st);
 
 // Channel blocks on the 64 -> 64 K = 8 headline kernels (warp-specialised gather, 8-channel
 // lanes): for clouds large enough to fill the GPU with one pass, each of the
@@ -1935,14 +1939,23 @@ int tc_blocked_forward(int mode, int64_t total, int64_t n, int c_in, int k, int 
                        const float *loc, const int32_t *nbr, const float *theta, const float *theta_b, float *out,
                        cudaStream_t st) {
     if (block_fast(total, k, c_in, c_out)) {
+        const bool split = mode != FC_MODE_TC_BF16;
+        std::vector<const float *> th, tb;  // all passes' images packed up front, one launch
         for (int o0 = 0; o0 < c_out; o0 += 64)
             for (int i0 = 0; i0 < c_in; i0 += 64) {
-                const int rc = tc_fast_forward_block(mode != FC_MODE_TC_BF16, total, n, feat + i0, c_in, loc, nbr,
-                                                     theta + ((int64_t)o0 * c_in + i0) * 3, theta_b + (int64_t)o0 * c_in + i0,
-                                                     c_in, out + o0, c_out, i0 > 0, st, nullptr, 0);
-                if (rc) return rc;
+                th.push_back(theta + ((int64_t)o0 * c_in + i0) * 3);
+                tb.push_back(theta_b + (int64_t)o0 * c_in + i0);
             }
-        return FC_OK;
+        const int64_t stride = fast_forward_image_stride(split);
+        Scratch imgs((size_t)stride * th.size(), st);
+        if (!imgs.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (block images)");
+        int rc = pack_forward_blocks(split, (int)th.size(), th.data(), tb.data(), c_in, imgs.as<uint8_t>(), st);
+        int pass = 0;
+        for (int o0 = 0; o0 < c_out && rc == FC_OK; o0 += 64)
+            for (int i0 = 0; i0 < c_in && rc == FC_OK; i0 += 64, ++pass)
+                rc = tc_fast_forward_block(split, total, n, feat + i0, c_in, loc, nbr, th[pass], tb[pass], c_in, out + o0,
+                                           c_out, i0 > 0, st, nullptr, 0, imgs.as<uint8_t>() + pass * stride);
+        return rc;
     }
     // each 32-channel block of the input is gathered ONCE and contracted against all (up to
     // 256) output channels in one pass (N = 128 / 256 accumulators), the blocks' products
@@ -2007,20 +2020,30 @@ int tc_blocked_forward(int mode, int64_t total, int64_t n, int c_in, int k, int 
 // the location gradient (dloc = centre - sum of the blocks' terms).
 int tc_fast_reverse_block(bool split, int64_t total, int k, const float *rows, int64_t ld_rows, const float *loc,
                           Csr csr, const float *theta, const float *theta_b, int ld_cin, float *out, int64_t ld_out,
-                          bool acc, cudaStream_t st);
+                          bool acc, cudaStream_t st, const uint8_t *pre_img, const float *pre_zero);
 
 static int tc_blocked_reverse(int mode, int64_t total, int64_t n, int c_in, int k, int c_out, const float *rows,
                               const float *loc, Csr csr, const float *theta, const float *theta_b, float *out,
                               const float *feat, const float *centre, float *dloc, cudaStream_t st) {
     if (!dloc && block_fast(total, k, c_in, c_out)) {  // 64 x 64 blocks on the headline reverse kernel
+        const bool split = mode != FC_MODE_TC_BF16;
+        std::vector<const float *> th, tb;  // all passes' images packed up front, one launch
         for (int i0 = 0; i0 < c_in; i0 += 64)
             for (int j0 = 0; j0 < c_out; j0 += 64) {
-                const int rc = tc_fast_reverse_block(mode != FC_MODE_TC_BF16, total, k, rows + j0, c_out, loc, csr,
-                                                     theta + ((int64_t)j0 * c_in + i0) * 3, theta_b + (int64_t)j0 * c_in + i0,
-                                                     c_in, out + i0, c_in, j0 > 0, st);
-                if (rc) return rc;
+                th.push_back(theta + ((int64_t)j0 * c_in + i0) * 3);
+                tb.push_back(theta_b + (int64_t)j0 * c_in + i0);
             }
-        return FC_OK;
+        Scratch imgs, zero(256, st);
+        int64_t stride = 0;
+        int rc = zero.ok() ? pack_passes(split, 64, 64, c_in, 1, 64, 64, (int)th.size(), th.data(), tb.data(), imgs, stride, st)
+                           : set_error(FC_ERR_CUDA, "scratch allocation failed (block images)");
+        if (rc == FC_OK) cudaMemsetAsync(zero.p, 0, 256, st);
+        int pass = 0;
+        for (int i0 = 0; i0 < c_in && rc == FC_OK; i0 += 64)
+            for (int j0 = 0; j0 < c_out && rc == FC_OK; j0 += 64, ++pass)
+                rc = tc_fast_reverse_block(split, total, k, rows + j0, c_out, loc, csr, th[pass], tb[pass], c_in, out + i0,
+                                           c_in, j0 > 0, st, imgs.as<uint8_t>() + pass * stride, zero.as<float>());
+        return rc;
     }
     // gathered (c') blocks of 32 channels, each gathered once per output block of up to 256
     // channels (64-channel gathers for a 64-wide output block, e.g. with the location-gradient
