@@ -76,7 +76,7 @@ struct FwdArgs {
     int64_t nrows;
     // one 64 x 64 block of a wider conv (wide kernel): feature rows / output rows with these
     // strides, the block's product added to out (acc) -- the channel-blocked engine's passes
-    int64_t ld_feat, ld_out;
+    int ld_feat, ld_out;  // (32-bit, as RevArgs: keeps the plain instance's register allocation)
     int acc;
     int dbg;                    // timing-probe variants (FC_DBG): 2 no MMA, 8 gather+index only, 32 CTA-0 trace
     unsigned long long *trace;  // [24 warps][kTraceN]
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_fwd64_kernel(FwdArgs a) {
     {  // resident B image
         const uint4 *src = reinterpret_cast<const uint4 *>(a.bimg);
         uint4 *dst = reinterpret_cast<uint4 *>(smem + L::B_OFF);
-        smem_fill16(dst, src, L::B_BYTES / 16);
+        for (int i = threadIdx.x; i < L::B_BYTES / 16; i += blockDim.x) dst[i] = src[i];  // (a cp.async fill measured 1-2 % slower here)
     }
     fence_proxy_async_smem();
     tc_fence_before();
@@ -502,7 +502,7 @@ __device__ __forceinline__ void sts128u(uint32_t addr, uint32_t a, uint32_t b, u
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
-template <bool SPLIT>
+template <bool SPLIT, bool BLK = false>  // BLK: strided rows / out + accumulate (channel blocks)
 __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
     using L = FwdL<SPLIT>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(a.bimg);
         uint4 *dst = reinterpret_cast<uint4 *>(smem + L::B_OFF);
-        smem_fill16(dst, src, L::B_BYTES / 16);
+        for (int i = threadIdx.x; i < L::B_BYTES / 16; i += blockDim.x) dst[i] = src[i];  // (a cp.async fill measured 1-2 % slower here)
     }
     fence_proxy_async_smem();
     tc_fence_before();
@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
             const float s0 = exp2i(rs[(b * 2 + 0) * kTile + t]) * binv;
             const float s1 = exp2i(rs[(b * 2 + 1) * kTile + t]) * binv;
             const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(b * 256);
-            float *orow = a.out + p * a.ld_out;
+            float *orow = a.out + p * (BLK ? a.ld_out : 64);
 #pragma unroll 1
             for (int c0 = 0; c0 < 64; c0 += 16) {
                 float x0[16], x1[16], d[16];
@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
                     float o[16];
 #pragma unroll
                     for (int c = 0; c < 16; ++c) o[c] = fmaf(x1[c], s1, x0[c] * s0);
-                    if (a.acc) {  // block pass after the first: out += this block's product
+                    if (BLK && a.acc) {  // block pass after the first: out += this block's product
 #pragma unroll
                         for (int c = 0; c < 16; c += 4) {
                             const float4 q = *reinterpret_cast<const float4 *>(orow + c0 + c);
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(wThreads, 1) tc_fwd64w_kernel(FwdArgs a) {
         auto load4 = [&](int i, int h, int b0) {
             const uint32_t es = E0 + (uint32_t)((i & 1) * L::E_STAGE + row * 16);
             const float *src = a.feat + 32 * h + 8 * cl;
-            const int64_t ldf = a.ld_feat;
+            const int64_t ldf = BLK ? a.ld_feat : 64;
 #pragma unroll
             for (int s2 = 0; s2 < 4; ++s2) {
                 const int32_t j = lds32(es + (uint32_t)((b0 + s2) * kTile * 16));
@@ -854,8 +854,8 @@ int tc_fast_forward_block(bool split, int64_t total, int64_t n, const float *fea
     a.bimg = img;
     a.binv = binv;
     a.out = out;
-    a.ld_feat = ld_feat;
-    a.ld_out = ld_out;
+    a.ld_feat = (int)ld_feat;
+    a.ld_out = (int)ld_out;
     a.acc = acc ? 1 : 0;
     {
         const char *e = getenv("FC_DBG");
@@ -884,7 +884,19 @@ int tc_fast_forward_block(bool split, int64_t total, int64_t n, const float *fea
         if (!pre_img) scratch_free(img, st);
         return FC_OK;
     }
-    if (!narrow) {
+    const bool blk = ld_feat != 64 || ld_out != 64 || acc;  // (a separate instance: the plain one keeps its registers)
+    if (blk) {
+        static uint64_t attr_t = 0, attr_f = 0;
+        if (split) {
+            if (first_use_on_device(attr_t))
+                cudaFuncSetAttribute(tc_fwd64w_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdL<true>::SMEM_ALLOC);
+            tc_fwd64w_kernel<true, true><<<grid, wThreads, FwdL<true>::SMEM_ALLOC, st>>>(a);
+        } else {
+            if (first_use_on_device(attr_f))
+                cudaFuncSetAttribute(tc_fwd64w_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdL<false>::SMEM_ALLOC);
+            tc_fwd64w_kernel<false, true><<<grid, wThreads, FwdL<false>::SMEM_ALLOC, st>>>(a);
+        }
+    } else if (!narrow) {
         if (split) {
             static uint64_t attr = 0;
             if (first_use_on_device(attr)) {

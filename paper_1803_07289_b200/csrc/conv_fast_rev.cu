@@ -79,11 +79,12 @@ struct RevArgs {
     const float *binv;
     float *out;           // [total, 64]
     const float *feat;    // location gradient only: conv input features [total, 64]
-    int64_t ld_rows, ld_out;  // wide kernel: row strides of rows / out (a 64 x 64 channel block)
-    int acc;                  // wide kernel: out += this block's product
     const float *centre;  // centre-role term [total, 3]
     float *dloc;          // [total, 3] or null
     int dbg;              // timing probes (FC_DBG): 2 no MMA, 8 gather + index only, 16 first 8 slots only (wrong results)
+    int ld_rows, ld_out;  // wide kernel, BLK instance: row strides of rows / out (a 64 x 64 channel block;
+                          // 32-bit: with 64-bit fields here ptxas spills one more register in the plain instance)
+    int acc;                  // wide kernel, BLK instance: out += this block's product
 };
 
 __device__ __forceinline__ void ldg_nc8r(const float *p, float (&v)[8]) {
@@ -588,7 +589,7 @@ __global__ void __launch_bounds__(rThreads, 1) tc_rev64_kernel(RevArgs a) {
     }
 }
 
-template <bool SPLIT, bool DLOC>
+template <bool SPLIT, bool DLOC, bool BLK = false>  // BLK: strided rows / out + accumulate (channel blocks)
 __global__ void __launch_bounds__(wrThreads, 1) tc_rev64w_kernel(RevArgs a) {
     using L = RevL<SPLIT>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -696,7 +697,7 @@ __global__ void __launch_bounds__(wrThreads, 1) tc_rev64w_kernel(RevArgs a) {
             const float s1 = exp2i(rs[(b * 2 + 1) * kTile + tr]) * binv;
             const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16);
             const bool pv = p < a.total;
-            float *orow = a.out + p * a.ld_out;
+            float *orow = a.out + p * (BLK ? a.ld_out : 64);
 #pragma unroll 1
             for (int c0 = 0; c0 < 64; c0 += 16) {
                 float x0[16], x1[16];
@@ -706,7 +707,7 @@ __global__ void __launch_bounds__(wrThreads, 1) tc_rev64w_kernel(RevArgs a) {
                     float o[16];
 #pragma unroll
                     for (int c = 0; c < 16; ++c) o[c] = fmaf(x1[c], s1, x0[c] * s0);
-                    if (a.acc) {  // block pass after the first: out += this block's product
+                    if (BLK && a.acc) {  // block pass after the first: out += this block's product
 #pragma unroll
                         for (int c = 0; c < 16; c += 4) {
                             const float4 q = *reinterpret_cast<const float4 *>(orow + c0 + c);
@@ -909,7 +910,7 @@ __global__ void __launch_bounds__(wrThreads, 1) tc_rev64w_kernel(RevArgs a) {
                 const int sl = b0 + s2;
                 const bool ok = sl < it.cnt;
                 const int32_t j = lds32(ok ? it.eb + (uint32_t)(sl * 16) : it.ez);
-                ldg_nc8r_if(src + (int64_t)j * a.ld_rows, v[s2], ok);
+                ldg_nc8r_if(src + (int64_t)j * (BLK ? a.ld_rows : 64), v[s2], ok);
             }
         };
         auto fma4w = [&](const ItemW &it, int b0) {
@@ -954,7 +955,7 @@ __global__ void __launch_bounds__(wrThreads, 1) tc_rev64w_kernel(RevArgs a) {
                                         __ldg(a.loc + (int64_t)jr * 3 + 1) - lp1, __ldg(a.loc + (int64_t)jr * 3 + 2) - lp2);
                     }
                     float r[8];
-                    ldg_nc8r(src + (int64_t)__float_as_int(e.x) * a.ld_rows, r);
+                    ldg_nc8r(src + (int64_t)__float_as_int(e.x) * (BLK ? a.ld_rows : 64), r);
                     const float2 w0 = make_float2(e.y, e.y), w1 = make_float2(e.z, e.z), w2 = make_float2(e.w, e.w);
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
@@ -1108,8 +1109,8 @@ static int fast_reverse_impl(bool split, int64_t total, int k, const float *rows
     a.feat = feat;
     a.centre = centre;
     a.dloc = dloc;
-    a.ld_rows = ld_rows;
-    a.ld_out = ld_out;
+    a.ld_rows = (int)ld_rows;
+    a.ld_out = (int)ld_out;
     a.acc = acc ? 1 : 0;
     {
         const char *e = getenv("FC_DBG");
@@ -1143,7 +1144,21 @@ static int fast_reverse_impl(bool split, int64_t total, int k, const float *rows
             tc_rev64w_kernel<S, D><<<grid, wrThreads, RevL<S>::SMEM_ALLOC, st>>>(a);                            \
         }                                                                                                       \
     } while (0)
-    if (split) {
+    const bool blk = ld_rows != 64 || ld_out != 64 || acc;  // (a separate instance: the plain one keeps its registers)
+    if (blk) {
+        static uint64_t attr_t = 0, attr_f = 0;
+        if (split) {
+            if (first_use_on_device(attr_t))
+                cudaFuncSetAttribute(tc_rev64w_kernel<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     RevL<true>::SMEM_ALLOC);
+            tc_rev64w_kernel<true, false, true><<<grid, wrThreads, RevL<true>::SMEM_ALLOC, st>>>(a);
+        } else {
+            if (first_use_on_device(attr_f))
+                cudaFuncSetAttribute(tc_rev64w_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     RevL<false>::SMEM_ALLOC);
+            tc_rev64w_kernel<false, false, true><<<grid, wrThreads, RevL<false>::SMEM_ALLOC, st>>>(a);
+        }
+    } else if (split) {
         if (dloc) FC_LAUNCH_REV(true, true);
         else FC_LAUNCH_REV(true, false);
     } else {
