@@ -1217,7 +1217,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_dtheta_kernel(DtArgs a) {
     const int64_t tiles_mine = a.num_tiles > blockIdx.x ? ceil_div(a.num_tiles - blockIdx.x, gridDim.x) : 0;
 
     // ---------------------------------------------------------------- MMA issue (warp 15, lane 0)
-    int mma_chunk = 0;  // next chunk (in this CTA's order) whose MMAs are to be issued
     auto issue_chunk = [&](int64_t u_global) {
         // u_global = tile_local * 8 + c.  D[(c' | c'+64), k] += [G_hi; G_lo]^T . X_hi + [G_hi; G_lo]^T . X_lo:
         // M = 128 (upstream channel hi / lo parts), N = 256 (all moment columns), K = 8 points

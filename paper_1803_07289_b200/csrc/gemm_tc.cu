@@ -401,7 +401,6 @@ __global__ void __launch_bounds__(64) wgrad_kernel(WArgs a) {
     int64_t tld = 0;
     const float *tp = tload ? col_src(tcol, tld) : nullptr;
     const bool tones = tload && tcol == a.ci;
-    constexpr bool masked = MASKED;
     auto issue = [&](int64_t pb, int buf) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {

@@ -412,7 +412,6 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 if (src[u] >= 0) {
-#pragma unroll
                     if constexpr (V == 8) {
                         asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                                      : "=r"(am[u][0]), "=r"(am[u][1]), "=r"(am[u][2]), "=r"(am[u][3]), "=r"(am[u][4]),
