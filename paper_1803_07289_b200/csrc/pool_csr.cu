@@ -326,7 +326,9 @@ __device__ __forceinline__ void ldvec(const T *p, T (&v)[V]) {
 
 // out row r pools fine row p = rows ? rows[r] : r; neighbour j's value is
 // owner ? (owner[j] >= 0 ? feat[owner[j]] : 0) : feat[j]; winners hold the fine index j.
-template <typename T, int V>
+// B slots in flight per batch (fp32 x 8 channels: 4, so that the loaded rows stay within
+// ~128 registers and two or more 256-thread blocks fit an SM: these are latency-bound)
+template <typename T, int V, int B = (V == 8 ? 4 : 8)>
 __global__ void __launch_bounds__(256)
     pool_select_fwd_kernel(int64_t m, int c, int k, const T *__restrict__ feat, const int32_t *__restrict__ nbr,
                            const int32_t *__restrict__ rows, const int32_t *__restrict__ owner, T *__restrict__ out,
@@ -341,13 +343,13 @@ __global__ void __launch_bounds__(256)
         const int32_t *row = nbr + p * k;
         T bv[V];
         int32_t bj[V];
-        for (int s0 = 0; s0 < k; s0 += 8) {
-            int32_t jj[8];
-            T vv[8][V];
+        for (int s0 = 0; s0 < k; s0 += B) {
+            int32_t jj[B];
+            T vv[B][V];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) jj[u] = __ldg(row + min(s0 + u, k - 1));
+            for (int u = 0; u < B; ++u) jj[u] = __ldg(row + min(s0 + u, k - 1));
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < B; ++u) {
                 const int64_t src = owner ? (int64_t)__ldg(owner + jj[u]) : (int64_t)jj[u];
                 if (src >= 0) {
                     ldvec<T, V>(feat + src * c + ch, vv[u]);
@@ -357,7 +359,7 @@ __global__ void __launch_bounds__(256)
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < B; ++u) {
                 const int sl = s0 + u;
                 if (sl < k) {
 #pragma unroll
@@ -383,7 +385,7 @@ __global__ void __launch_bounds__(256)
 // (i, s) ascending, each i once, with q = owner ? owner[i] : i (skipped when < 0) and
 // winners[q, ch] == j -- the additions of _native.pyx:165-168 restricted to the rows that can
 // be non-zero (dropping additions of +0.0 cannot change an accumulator that starts at +0.0).
-template <typename T, int V>
+template <typename T, int V, int B = (V == 8 ? 4 : 8)>
 __global__ void __launch_bounds__(256)
     pool_select_bwd_kernel(int64_t m, int c, int k, const T *__restrict__ g, const int32_t *__restrict__ winners,
                            Csr csr, const int32_t *__restrict__ rows, const int32_t *__restrict__ owner,
@@ -400,32 +402,32 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int e = 0; e < V; ++e) acc[e] = T(0);
         int64_t prev = -1;
-        for (int32_t qb = q0; qb < q1; qb += 8) {
-            int64_t ii[8], src[8];
+        for (int32_t qb = q0; qb < q1; qb += B) {
+            int32_t ii[B], src[B];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                ii[u] = (int64_t)__ldg(csr.ent + min(qb + u, q1 - 1)) / k;
-                src[u] = owner ? (int64_t)__ldg(owner + ii[u]) : ii[u];
+            for (int u = 0; u < B; ++u) {
+                ii[u] = __ldg(csr.ent + min(qb + u, q1 - 1)) / k;
+                src[u] = owner ? __ldg(owner + ii[u]) : ii[u];
             }
-            int32_t am[8][V];
-            T gv[8][V];
+            int32_t am[B][V];
+            T gv[B][V];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < B; ++u) {
                 if (src[u] >= 0) {
                     if constexpr (V == 8) {
                         asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                                      : "=r"(am[u][0]), "=r"(am[u][1]), "=r"(am[u][2]), "=r"(am[u][3]), "=r"(am[u][4]),
                                        "=r"(am[u][5]), "=r"(am[u][6]), "=r"(am[u][7])
-                                     : "l"(winners + src[u] * c + ch));
+                                     : "l"(winners + (int64_t)src[u] * c + ch));
                     } else {
 #pragma unroll
-                        for (int e = 0; e < V; ++e) am[u][e] = __ldg(winners + src[u] * c + ch + e);
+                        for (int e = 0; e < V; ++e) am[u][e] = __ldg(winners + (int64_t)src[u] * c + ch + e);
                     }
-                    ldvec<T, V>(g + src[u] * c + ch, gv[u]);
+                    ldvec<T, V>(g + (int64_t)src[u] * c + ch, gv[u]);
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < B; ++u) {
                 if (qb + u < q1 && ii[u] != prev) {
                     prev = ii[u];
                     if (src[u] >= 0) {
