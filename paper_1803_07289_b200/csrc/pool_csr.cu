@@ -271,15 +271,15 @@ __global__ void __launch_bounds__(256)
         for (int e = 0; e < 8; ++e) acc[e] = 0.f;
         int64_t prev = -1;
         for (int32_t qb = q0; qb < q1; qb += 4) {
-            int64_t ii[4];
+            int32_t ii[4];
             int32_t am[4][8];
             float gv[4][8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) ii[u] = (int64_t)__ldg(csr.ent + min(qb + u, q1 - 1)) / k;
+            for (int u = 0; u < 4; ++u) ii[u] = __ldg(csr.ent + min(qb + u, q1 - 1)) / k;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                ldg8i(argmax + ii[u] * c + ch, am[u]);
-                ldg8f(g + ii[u] * c + ch, gv[u]);
+                ldg8i(argmax + (int64_t)ii[u] * c + ch, am[u]);
+                ldg8f(g + (int64_t)ii[u] * c + ch, gv[u]);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -798,7 +798,13 @@ int launch_pool_bwd(int64_t total, int64_t n, int c, int k, const T *g, const in
         }();
         if (!v4 && c % 8 == 0 && reinterpret_cast<uintptr_t>(g) % 32 == 0 &&
             reinterpret_cast<uintptr_t>(argmax) % 32 == 0 && reinterpret_cast<uintptr_t>(df) % 16 == 0) {
-            pool_bwd_w8_kernel<<<grid_1d(total * (c / 8)), 256, 0, st>>>(total, n, c, k, (const float *)g, argmax, csr,
+            // 128-thread blocks: at 92 registers five fit an SM (20 warps) against two of 256
+            // (16 warps); latency-bound, 7 M x 64 ch: 2.97 -> 2.76 ms (FC_POOL_BWD_BLOCK for A/B)
+            static const int bs = [] {
+                const char *e = getenv("FC_POOL_BWD_BLOCK");
+                return e ? atoi(e) : 128;
+            }();
+            pool_bwd_w8_kernel<<<grid_1d(total * (c / 8), bs), bs, 0, st>>>(total, n, c, k, (const float *)g, argmax, csr,
                                                                           (float *)df);
             count_launch();
             return check_launch("pool_bwd_w8_kernel");
