@@ -230,3 +230,41 @@ def test_wide_fast_channel_blocks_vs_oracle(fc, oracle_mod, cin, cout):
     dth, dtb = oracle_mod.conv_param_grads(up, feat, locf, nbr)
     _red_close(_np(gb.d_theta), dth, "d_theta")
     _red_close(_np(gb.d_theta_b), dtb, "d_theta_b")
+
+
+def test_wide_fast_channel_blocks_bf16_mode(oracle_mod):
+    """The bf16 tensor-core mode through the fast channel blocks (128 -> 128 at 40 K points):
+    forward, flex_deconv and d_features within the bf16 bounds (norm-wise 1e-2 and max-abs
+    1e-2 x max|ref|) on sampled rows."""
+    import torch
+
+    from paper_1803_07289_b200 import _ops
+
+    n, k, c = 40_000, 8, 128
+    g = np.random.default_rng(77)
+    loc = (np.floor(g.random((n, 3)) * 2 ** 24) / 2 ** 24).astype(np.float32)
+    pos = torch.from_numpy(loc).cuda()
+    pos = pos[_ops.spatial_order(pos).long()].contiguous()
+    locf = pos.cpu().numpy().astype(np.float64)
+    feat = g.standard_normal((n, c)).astype(np.float32)
+    up = g.standard_normal((n, c)).astype(np.float32)
+    th = (0.1 * g.standard_normal((c, c, 3))).astype(np.float32)
+    tb = (0.1 * g.standard_normal((c, c))).astype(np.float32)
+    t = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+    nbr = _ops.knn(pos, 1, n, k)
+    csr = _ops.csr_build(nbr, 1, n)
+    nb = nbr.cpu().numpy().astype(np.int64)
+    rows = np.unique(g.integers(0, n, 1500))
+
+    def close(got, ref):
+        assert np.linalg.norm(got - ref) <= 1e-2 * np.linalg.norm(ref)
+        assert np.abs(got - ref).max() <= 1e-2 * np.abs(ref).max()
+
+    out = _ops.conv_forward(t(feat), pos, nbr, t(th), t(tb), 1, n, mode="bf16").cpu().numpy()
+    close(out[rows], oracle_mod.conv_forward_rows(feat, locf, nb, th, tb, rows))
+    df = _ops.conv_backward(t(up), t(feat), pos, nbr, csr, t(th), t(tb), 1, n, need=(True, False, False, False),
+                            mode="bf16")[0].cpu().numpy()
+    df_ref, _ = oracle_mod.conv_backward_rows(up, feat, locf, nb, th, tb, rows, with_locations=False)
+    close(df[rows], df_ref)
+    y = _ops.deconv_forward(t(up), pos, csr, t(th), t(tb), 1, n, k, mode="bf16").cpu().numpy()
+    close(y[rows], df_ref)  # flex_deconv = A(theta)^T x = d_features of the conv with upstream x
