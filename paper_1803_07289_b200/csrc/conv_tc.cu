@@ -1822,23 +1822,29 @@ struct ForkJoin {
     bool on = false;
     cudaStream_t s[4];
     cudaEvent_t fork_ev, join_ev[4];
-    ForkJoin(cudaStream_t m, int jobs, bool enable) : main(m), n(jobs), on(enable && jobs > 1 && jobs <= 4) {
+    // pool: which set of side streams (two fork / joins in flight at once -- d_theta's passes
+    // beside the reverse pass's -- must not share streams, or they would serialise)
+    ForkJoin(cudaStream_t m, int jobs, bool enable, int pool = 0)
+        : main(m), n(jobs), on(enable && jobs > 1 && jobs <= 4) {
         for (int j = 0; j < 4; ++j) s[j] = m;
         if (!on) return;
         // per host thread and device: two threads forking on one device must not share events
-        static thread_local cudaStream_t aux[64][4];
-        static thread_local cudaEvent_t evs[64][5];
+        static thread_local cudaStream_t aux[64][2][4];
+        static thread_local cudaEvent_t evs[64][2][5];
         static thread_local uint64_t made = 0;
         const int dev = current_device() & 63;
         if (first_use_on_device(made)) {
-            for (int j = 0; j < 4; ++j) cudaStreamCreateWithFlags(&aux[dev][j], cudaStreamNonBlocking);
-            for (int j = 0; j < 5; ++j) cudaEventCreateWithFlags(&evs[dev][j], cudaEventDisableTiming);
+            for (int q = 0; q < 2; ++q) {
+                for (int j = 0; j < 4; ++j) cudaStreamCreateWithFlags(&aux[dev][q][j], cudaStreamNonBlocking);
+                for (int j = 0; j < 5; ++j) cudaEventCreateWithFlags(&evs[dev][q][j], cudaEventDisableTiming);
+            }
         }
-        fork_ev = evs[dev][4];
+        pool &= 1;
+        fork_ev = evs[dev][pool][4];
         cudaEventRecord(fork_ev, m);
         for (int j = 0; j < n; ++j) {
-            s[j] = aux[dev][j];
-            join_ev[j] = evs[dev][j];
+            s[j] = aux[dev][pool][j];
+            join_ev[j] = evs[dev][pool][j];
             cudaStreamWaitEvent(s[j], fork_ev, 0);
         }
     }
@@ -2021,9 +2027,15 @@ int tc_fast_reverse_block(bool split, int64_t total, int k, const float *rows, i
                           Csr csr, const float *theta, const float *theta_b, int ld_cin, float *out, int64_t ld_out,
                           bool acc, cudaStream_t st, const uint8_t *pre_img, const float *pre_zero);
 
+// late_centre (with dloc): the centre term is still being computed on late_join's side
+// stream; every pass runs against a zero centre and the centre is added after the join,
+// right after pass 0's term and before the later passes' (so the additions are the sequential
+// order's: (c - t0) - t1 ... = ((0 - t0) + c) + (0 - t1) ...).  Needs the concurrent-pass form
+// (or one pass); the caller checks blocked_reverse_late_ok.
 static int tc_blocked_reverse(int mode, int64_t total, int64_t n, int c_in, int k, int c_out, const float *rows,
                               const float *loc, Csr csr, const float *theta, const float *theta_b, float *out,
-                              const float *feat, const float *centre, float *dloc, cudaStream_t st) {
+                              const float *feat, const float *centre, float *dloc, cudaStream_t st,
+                              const float *late_centre = nullptr, SideFork *late_join = nullptr) {
     if (!dloc && block_fast(total, k, c_in, c_out)) {  // 64 x 64 blocks on the headline reverse kernel
         const bool split = mode != FC_MODE_TC_BF16;
         std::vector<const float *> th, tb;  // all passes' images packed up front, one launch
@@ -2051,16 +2063,18 @@ static int tc_blocked_reverse(int mode, int64_t total, int64_t n, int c_in, int 
     const int gb = ob > 64 ? 32 : 64;
     const int nj = (int)ceil_div(c_out, gb), ni = (int)ceil_div(c_in, ob);
     const bool conc = ni == 1 && concurrent_passes(total, nj);
+    const bool late = dloc && late_centre;
+    if (late && !(conc || (ni == 1 && nj == 1))) return set_error(FC_ERR_CONFIG, "late centre needs one block row");
     Scratch tmp, tdl, zero3;
     if (conc) {  // passes 1.. write their d_features part and (-) location term to side buffers
         tmp.alloc(sizeof(float) * (size_t)(nj - 1) * total * ob, st);
-        if (dloc) {
-            tdl.alloc(sizeof(float) * (size_t)(nj - 1) * total * 3, st);
-            zero3.alloc(sizeof(float) * (size_t)total * 3, st);
-        }
-        if (!tmp.ok() || (dloc && (!tdl.ok() || !zero3.ok())))
-            return set_error(FC_ERR_CUDA, "scratch allocation failed (blocked reverse)");
-        if (dloc) cudaMemsetAsync(zero3.p, 0, sizeof(float) * total * 3, st);
+        if (dloc) tdl.alloc(sizeof(float) * (size_t)(nj - 1) * total * 3, st);
+        if (!tmp.ok() || (dloc && !tdl.ok())) return set_error(FC_ERR_CUDA, "scratch allocation failed (blocked reverse)");
+    }
+    if (dloc && (conc || late)) {
+        zero3.alloc(sizeof(float) * (size_t)total * 3, st);
+        if (!zero3.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (blocked reverse)");
+        cudaMemsetAsync(zero3.p, 0, sizeof(float) * total * 3, st);
     }
     Scratch imgs;
     int64_t istride = 0;
@@ -2096,7 +2110,7 @@ static int tc_blocked_reverse(int mode, int64_t total, int64_t n, int c_in, int 
                 a.feat = feat + i0;
                 a.ld_feat = c_in;
                 // side passes: dloc_b = 0 - term_b (exact negation), added below: (c - t0) - t1
-                a.centre = side ? zero3.as<float>() : centre;
+                a.centre = (side || late) ? zero3.as<float>() : centre;
                 a.dloc = side ? tdl.as<float>() + (size_t)(b - 1) * total * 3 : dloc;
                 a.acc_dloc = !conc && (i0 > 0 || j0 > 0);
             }
@@ -2111,6 +2125,10 @@ static int tc_blocked_reverse(int mode, int64_t total, int64_t n, int c_in, int 
         }
     }
     fj.join();
+    if (late) {  // the centre term: pass 0's (0 - t0) + c
+        late_join->join();
+        if (rc == FC_OK) add_rows(total, 3, dloc, 3, late_centre, 3, st);
+    }
     if (rc) return rc;
     for (int b = 1; conc && b < nj; ++b) {
         add_rows(total, ob, out, c_in, tmp.as<float>() + (size_t)(b - 1) * total * ob, ob, st);
@@ -2129,19 +2147,23 @@ int tc_blocked_backward(int mode, int64_t total, int64_t n, int c_in, int k, int
                         const float *feat, const float *loc, const int32_t *nbr, Csr csr, const float *theta,
                         const float *theta_b, float *d_features, float *d_locations, float *d_theta,
                         float *d_theta_b, cudaStream_t st0) {
-    Scratch centre_buf;
-    SideFork sf(st0, !d_locations && d_features && (d_theta || d_theta_b));
+    // without the location gradient, c' tiles of 128 (each 64-channel feature block is
+    // gathered once per 128 upstream channels)
+    const int jb = (!d_locations && c_out % 128 == 0) ? 128 : 64;
+    const int npass = (int)(ceil_div(c_out, jb) * ceil_div(c_in, 64));
+    const bool conc = concurrent_passes(total, npass);
+    // small clouds with the location gradient: the reverse pass need not wait for the centre
+    // term (tc_blocked_reverse's late centre), so d_theta runs beside it there too
+    const int rni = (int)ceil_div(c_in, 64), rnj = (int)ceil_div(c_out, 64);
+    const bool late = d_locations && d_features && conc && rni == 1 && (rnj == 1 || concurrent_passes(total, rnj));
+    Scratch centre_buf;  // (allocated before the fork: the side stream writes it)
+    if (d_locations) {
+        centre_buf.alloc(sizeof(float) * total * 3, st0);
+        if (!centre_buf.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (blocked backward)");
+    }
+    SideFork sf(st0, (!d_locations && d_features && (d_theta || d_theta_b)) || late);
     const cudaStream_t st = sf.side;  // d_theta section (the caller's stream unless forked)
     if (d_theta || d_theta_b || d_locations) {
-        if (d_locations) {
-            centre_buf.alloc(sizeof(float) * total * 3, st);
-            if (!centre_buf.ok()) return set_error(FC_ERR_CUDA, "scratch allocation failed (blocked backward)");
-        }
-        // without the location gradient, c' tiles of 128 (each 64-channel feature block is
-        // gathered once per 128 upstream channels)
-        const int jb = (!d_locations && c_out % 128 == 0) ? 128 : 64;
-        const int npass = (int)(ceil_div(c_out, jb) * ceil_div(c_in, 64));
-        const bool conc = concurrent_passes(total, npass);
         Scratch cside;  // concurrent passes 1..: their own centre terms, added in pass order below
         if (conc && d_locations) {
             cside.alloc(sizeof(float) * (size_t)(npass - 1) * total * 3, st);
@@ -2159,7 +2181,7 @@ int tc_blocked_backward(int mode, int64_t total, int64_t n, int c_in, int k, int
             const int rc0 = pack_passes(true, 64, 64, c_in, 0, 64, 64, (int)th.size(), th.data(), tb.data(), imgs, istride, st);
             if (rc0) return rc0;
         }
-        ForkJoin fj(st, npass, conc);
+        ForkJoin fj(st, npass, conc, sf.on ? 1 : 0);  // (its own side streams beside the reverse pass's)
         int rc = FC_OK;
         int b = 0;
         for (int j0 = 0; j0 < c_out && rc == FC_OK; j0 += jb) {
@@ -2193,7 +2215,8 @@ int tc_blocked_backward(int mode, int64_t total, int64_t n, int c_in, int k, int
             df = df_buf.as<float>();
         }
         const int rc = tc_blocked_reverse(mode, total, n, c_in, k, c_out, g, loc, csr, theta, theta_b, df, feat,
-                                          centre_buf.as<float>(), d_locations, st0);
+                                          centre_buf.as<float>(), d_locations, st0, late ? centre_buf.as<float>() : nullptr,
+                                          late ? &sf : nullptr);
         sf.join();
         return rc;
     }
