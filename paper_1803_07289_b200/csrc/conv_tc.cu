@@ -63,6 +63,10 @@ struct TcArgs {
     int64_t ld_rows, ld_out, ld_feat;
     int acc;       // out += block result
     int acc_dloc;  // dloc -= this block's neighbour term (else dloc = centre - term)
+    // bimg == null: every CTA packs the B image itself from this block of theta (no separate
+    // pack launch on the critical path of a small call)
+    const float *pk_theta, *pk_theta_b;
+    int pk_cin, pk_cout, pk_ld;
 };
 
 template <bool SPLIT>
@@ -838,17 +842,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gmc_kernel(TcArgs a) {
         fence_mbar_init();
     }
     if (warp == kMmaWarp) tmem_alloc(tmem_holder, L::TMEM_COLS);
-    {  // resident B operand image(s)
-        const uint4 *src = reinterpret_cast<const uint4 *>(a.bimg);
-        uint4 *dst = reinterpret_cast<uint4 *>(B_hi);
-        const int nvec = L::B_BYTES * L::NSPLIT / 16;
-        smem_fill16(dst, src, nvec);
+    __shared__ float binv_s;
+    {  // resident B operand image(s): the caller's packed image, or packed here from theta
+        if (a.bimg) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(a.bimg);
+            uint4 *dst = reinterpret_cast<uint4 *>(B_hi);
+            const int nvec = L::B_BYTES * L::NSPLIT / 16;
+            smem_fill16(dst, src, nvec);
+        } else {
+            pack_b_body<SPLIT>(a.pk_cin, a.pk_cout, a.pk_ld, a.pk_theta, a.pk_theta_b, REVERSE ? 1 : 0, NOUT, GC, B_hi,
+                               &binv_s, 0, 1);
+        }
     }
-    const float binv = a.binv[0];
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    const float binv = a.bimg ? a.binv[0] : binv_s;
     const uint32_t tmem_base = *tmem_holder;
 
     // ---------------------------------------------------------------- MMA issue (warp kMmaWarp, lane 0)
@@ -1470,7 +1480,18 @@ static int launch_tc(const TcArgs &a0, int cin, int cout, const float *theta, co
     using L = TcLayout<GC, NOUT, SPLIT, DLOC>;
     TcArgs a = a0;
     uint8_t *img = nullptr;  // a0.bimg set: the caller packed this pass's image (pack_passes)
-    if (!a.bimg) {
+    static int pack_launch = -1;  // FC_PACK_KERNEL=1: a separate pack launch (A/B)
+    if (pack_launch < 0) {
+        const char *e = getenv("FC_PACK_KERNEL");
+        pack_launch = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (!a.bimg && !pack_launch) {  // each CTA packs the image in its prologue
+        a.pk_theta = theta;
+        a.pk_theta_b = theta_b;
+        a.pk_cin = cin;
+        a.pk_cout = cout;
+        a.pk_ld = ld_cin > 0 ? ld_cin : cin;
+    } else if (!a.bimg) {
         img = (uint8_t *)scratch_alloc((size_t)L::B_BYTES * L::NSPLIT + 256, st);
         if (!img) return set_error(FC_ERR_CUDA, "scratch allocation failed (tc)");
         float *binv = reinterpret_cast<float *>(img + (size_t)L::B_BYTES * L::NSPLIT);
