@@ -184,14 +184,22 @@ using namespace fc;
 // between).  FC_GEMM_ROUTE=1 selects moments rows + the hand-written tcgen05 GEMM instead (A/B
 // timing; measured on C2's 8192 points: forward 0.056 vs 0.070 ms, backward 0.297 vs 0.226 ms --
 // both routes are one latency-bound wave at that size).
+// Wide fp32 shapes: the channel-blocked gather -> tcgen05 engines, except (mode "auto") for
+// clouds of less than one wave of tiles with >= 256 channels on both sides (the U-Net's
+// 16 K-point level): there each blocked pass is a single latency-bound tile per CTA repeated
+// 8 times, and the moments rows + one tcgen05 GEMM route measures ~20 % faster (16 K x 256:
+// fwd 0.33 -> 0.26, deconv 0.35 -> 0.28, bwd 0.77 -> 0.66 ms).  FC_GEMM_ROUTE=1 / 0 forces
+// the GEMM / blocked route for every wide shape.
 static bool blocked_route(int mode, int64_t total, int c_in, int d, int c_out) {
-    (void)total;
-    static int gemm = -1;
-    if (gemm < 0) {
+    static int gemm = -2;
+    if (gemm == -2) {
         const char *e = getenv("FC_GEMM_ROUTE");
-        gemm = (e && e[0] == '1') ? 1 : 0;
+        gemm = e ? (e[0] == '1' ? 1 : 0) : -1;
     }
-    return !gemm && tc_blocked_supported(mode, c_in, d, c_out);
+    if (gemm == 1 || !tc_blocked_supported(mode, c_in, d, c_out)) return false;
+    if (gemm == -1 && mode == FC_MODE_AUTO && ceil_div(total, (int64_t)128) < num_sms() && c_in >= 256 && c_out >= 256)
+        return false;
+    return true;
 }
 
 static int check_dtype(int dtype) {
