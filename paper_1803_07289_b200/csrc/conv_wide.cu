@@ -562,13 +562,16 @@ int launch_dtheta_slice_dp(int64_t total, int64_t n, int cin, int k, int cout, c
 // mode), which runs it at several times the CTA-tiled FFMA rate.  The gather stays here.
 namespace {
 
-// X[p, c*(DP+1) + t] for points [p0, p0 + m): one warp per point, lanes over 4 channels,
-// 8 neighbour rows in flight, slot order per (c, t) (_native.pyx:52-59).
-template <int DP, bool REVERSE, bool TMAJOR = false>
+// X[p, c*(DP+1) + t] for points [p0, p0 + m): one warp per point, lanes over 4 channels
+// (H = 2: two 4-channel groups 128 channels apart, so a 256-channel row is one pass with the
+// neighbour indices and offsets loaded once), 8 (H = 2: 4) neighbour rows in flight, slot
+// order per (c, t) (_native.pyx:52-59).
+template <int DP, bool REVERSE, bool TMAJOR = false, int H = 1>
 __global__ void __launch_bounds__(256)
     moments_rows_kernel(int64_t p0, int64_t m, int64_t n, int gc, int k, const float *__restrict__ rows,
                         const float *__restrict__ loc, const int32_t *__restrict__ nbr, Csr csr,
                         float *__restrict__ X) {
+    constexpr int SB = H == 1 ? 8 : 4;  // slots per batch
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int ktot = gc * (DP + 1);
@@ -584,53 +587,70 @@ __global__ void __launch_bounds__(256)
             q1 = csr.off[p + 1];
         }
         float *xr = X + r * ktot;
-        for (int c0 = 0; c0 < gc; c0 += 128) {
-            const int c = c0 + lane * 4;
-            const bool ok = c < gc;
-            float acc[4][DP + 1];
+        for (int c0 = 0; c0 < gc; c0 += 128 * H) {
+            int cg[H];
+            bool ok[H];
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
+            for (int h = 0; h < H; ++h) {
+                cg[h] = c0 + h * 128 + lane * 4;
+                ok[h] = cg[h] < gc;
+            }
+            float acc[H][4][DP + 1];
 #pragma unroll
-                for (int t = 0; t <= DP; ++t) acc[e][t] = 0.f;
-            for (int64_t qb = q0; qb < q1; qb += 8) {
-                int64_t jj[8];
+            for (int h = 0; h < H; ++h)
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int e = 0; e < 4; ++e)
+#pragma unroll
+                    for (int t = 0; t <= DP; ++t) acc[h][e][t] = 0.f;
+            for (int64_t qb = q0; qb < q1; qb += SB) {
+                int64_t jj[SB];
+#pragma unroll
+                for (int u = 0; u < SB; ++u) {
                     const int64_t q = qb + u < q1 ? qb + u : q1 - 1;
                     jj[u] = REVERSE ? (int64_t)csr.ent[q] / k : base + nbr[p * k + q];
                 }
-                float4 v[8];
-                float o[8][DP];
+                float4 v[SB][H];
+                float o[SB][DP];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    v[u] = ok ? __ldg(reinterpret_cast<const float4 *>(rows + jj[u] * gc + c)) : make_float4(0, 0, 0, 0);
+                for (int u = 0; u < SB; ++u) {
+#pragma unroll
+                    for (int h = 0; h < H; ++h)
+                        v[u][h] = ok[h] ? __ldg(reinterpret_cast<const float4 *>(rows + jj[u] * gc + cg[h]))
+                                        : make_float4(0, 0, 0, 0);
 #pragma unroll
                     for (int t = 0; t < DP; ++t)
                         o[u][t] = REVERSE ? loc[jj[u] * DP + t] - lp[t] : lp[t] - loc[jj[u] * DP + t];
                 }
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < SB; ++u) {
                     if (qb + u < q1) {
-                        const float ve[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
+                        for (int h = 0; h < H; ++h) {
+                            const float ve[4] = {v[u][h].x, v[u][h].y, v[u][h].z, v[u][h].w};
 #pragma unroll
-                            for (int t = 0; t < DP; ++t) acc[e][t] = fmaf(ve[e], o[u][t], acc[e][t]);
-                            acc[e][DP] += ve[e];
+                            for (int e = 0; e < 4; ++e) {
+#pragma unroll
+                                for (int t = 0; t < DP; ++t) acc[h][e][t] = fmaf(ve[e], o[u][t], acc[h][e][t]);
+                                acc[h][e][DP] += ve[e];
+                            }
                         }
                     }
                 }
             }
-            if (ok) {
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                if (!ok[h]) continue;
+                const int c = cg[h];
                 if constexpr (TMAJOR) {  // X[p, t*gc + c]: one float4 per t
 #pragma unroll
                     for (int t = 0; t <= DP; ++t)
-                        *reinterpret_cast<float4 *>(xr + t * gc + c) = make_float4(acc[0][t], acc[1][t], acc[2][t], acc[3][t]);
+                        *reinterpret_cast<float4 *>(xr + t * gc + c) =
+                            make_float4(acc[h][0][t], acc[h][1][t], acc[h][2][t], acc[h][3][t]);
                 } else {  // X[p, c*(DP+1) + t]: 4 channels x (DP+1) consecutive floats
 #pragma unroll
                     for (int e = 0; e < 4; ++e)
 #pragma unroll
-                        for (int t = 0; t <= DP; ++t) xr[(c + e) * (DP + 1) + t] = acc[e][t];
+                        for (int t = 0; t <= DP; ++t) xr[(c + e) * (DP + 1) + t] = acc[h][e][t];
                 }
             }
         }
@@ -694,7 +714,8 @@ int launch_gemm_gmc_dp(int64_t total, int64_t n, int gc, int k, int cout, const 
     for (int64_t p0 = 0; p0 < total && rc == FC_OK; p0 += chunk) {
         const int64_t m = std::min(chunk, total - p0);
         const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)num_sms() * 8);
-        moments_rows_kernel<DP, REV><<<grid, 256, 0, st>>>(p0, m, n, gc, k, rows, loc, nbr, csr, X);
+        if (gc % 256 == 0) moments_rows_kernel<DP, REV, false, 2><<<grid, 256, 0, st>>>(p0, m, n, gc, k, rows, loc, nbr, csr, X);
+        else moments_rows_kernel<DP, REV><<<grid, 256, 0, st>>>(p0, m, n, gc, k, rows, loc, nbr, csr, X);
         count_launch();
         rc = tc_gemm(X, ktot, ktot, m, img, cout, out + p0 * cout, cout, st);
     }
@@ -718,7 +739,9 @@ int launch_gemm_dtheta_dp(int64_t total, int64_t n, int cin, int k, int cout, co
     for (int64_t p0 = 0; p0 < total && rc == FC_OK; p0 += chunk) {
         const int64_t m = std::min(chunk, total - p0);
         const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)num_sms() * 8);
-        moments_rows_kernel<DP, false><<<grid, 256, 0, st>>>(p0, m, n, cin, k, feat, loc, nbr, Csr{nullptr, nullptr}, X);
+        if (cin % 256 == 0)
+            moments_rows_kernel<DP, false, false, 2><<<grid, 256, 0, st>>>(p0, m, n, cin, k, feat, loc, nbr, Csr{nullptr, nullptr}, X);
+        else moments_rows_kernel<DP, false><<<grid, 256, 0, st>>>(p0, m, n, cin, k, feat, loc, nbr, Csr{nullptr, nullptr}, X);
         count_launch();
         // P [cout, ktot] = G^T X (fc_gemm_wgrad: fixed-order partial sums); chunks added in order
         const float *xo = X;
@@ -814,7 +837,8 @@ int launch_gemm_rev_dloc_dp(int64_t total, int64_t n, int gc, int k, int cout, c
     for (int64_t p0 = 0; p0 < total && rc == FC_OK; p0 += chunk) {
         const int64_t m = std::min(chunk, total - p0);
         const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 8), (int64_t)num_sms() * 8);
-        moments_rows_kernel<DP, true, true><<<grid, 256, 0, st>>>(p0, m, n, gc, k, rows, loc, nullptr, csr, X);
+        if (gc % 256 == 0) moments_rows_kernel<DP, true, true, 2><<<grid, 256, 0, st>>>(p0, m, n, gc, k, rows, loc, nullptr, csr, X);
+        else moments_rows_kernel<DP, true, true><<<grid, 256, 0, st>>>(p0, m, n, gc, k, rows, loc, nullptr, csr, X);
         count_launch();
         rc = tc_gemm(X, ktot, ktot, m, img_w, cout, out + p0 * cout, cout, st);
         // U = Yb . [theta_0 .. theta_{d-1}]: the bias-moment columns of X as the operand
