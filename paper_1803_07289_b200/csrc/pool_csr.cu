@@ -863,8 +863,12 @@ int launch_pool_select_fwd(int64_t m, int c, int k, const T *feat, const int32_t
     if constexpr (sizeof(T) == 4) {  // fp32: 8 channels per thread, 32-byte loads
         if (c % 8 == 0 && reinterpret_cast<uintptr_t>(feat) % 32 == 0 && reinterpret_cast<uintptr_t>(out) % 32 == 0 &&
             reinterpret_cast<uintptr_t>(winners) % 32 == 0) {
-            pool_select_fwd_kernel<T, 8><<<grid_1d(m * (c / 8)), 256, 0, st>>>(m, c, k, feat, nbr, rows, owner, out,
-                                                                                winners);
+            static const int bs = [] {  // 128-thread blocks: 5 resident per SM at 89 registers (FC_POOL_SEL_BLOCK: A/B)
+                const char *e = getenv("FC_POOL_SEL_BLOCK");
+                return e ? atoi(e) : 128;
+            }();
+            pool_select_fwd_kernel<T, 8><<<grid_1d(m * (c / 8), bs), bs, 0, st>>>(m, c, k, feat, nbr, rows, owner, out,
+                                                                                  winners);
             count_launch();
             return check_launch("pool_select_fwd_kernel");
         }
