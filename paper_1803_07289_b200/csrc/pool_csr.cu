@@ -165,8 +165,9 @@ __global__ void __launch_bounds__(256)
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t p = idx / cv;
         const int ch = (int)(idx - p * cv) * 8;
-        const int64_t base = (p / n) * n;
+        const int32_t base = (int32_t)((p / n) * n);  // (point indices fit int32: B*N*k < 2^31)
         const int32_t *row = nbr + p * k;
+        const float *fch = feat + ch;
         float bv[8];
         int32_t bj[8];
         for (int s0 = 0; s0 < k; s0 += 8) {
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
             for (int u = 0; u < 8; ++u) jj[u] = __ldg(row + min(s0 + u, k - 1));
 #pragma unroll
-            for (int u = 0; u < 8; ++u) ldg8f(feat + (base + jj[u]) * c + ch, vv[u]);
+            for (int u = 0; u < 8; ++u) ldg8f(fch + (int64_t)(base + jj[u]) * c, vv[u]);
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int s = s0 + u;
@@ -774,8 +775,12 @@ int launch_pool_fwd(int64_t total, int64_t n, int c, int k, const T *feat, const
         }();
         if constexpr (sizeof(T) == 4) {
             if (!v4 && c % 8 == 0 && reinterpret_cast<uintptr_t>(feat) % 32 == 0) {
-                pool_fwd_w8_kernel<<<grid_1d(total * (c / 8)), 256, 0, st>>>(total, n, c, k, (const float *)feat, nbr,
-                                                                              (float *)out, argmax);
+                static const int bs = [] {  // (FC_POOL_FWD_BLOCK for A/B)
+                    const char *e = getenv("FC_POOL_FWD_BLOCK");
+                    return e ? atoi(e) : 256;
+                }();
+                pool_fwd_w8_kernel<<<grid_1d(total * (c / 8), bs), bs, 0, st>>>(total, n, c, k, (const float *)feat, nbr,
+                                                                                (float *)out, argmax);
                 count_launch();
                 return check_launch("pool_fwd_w8_kernel");
             }
