@@ -327,7 +327,7 @@ __device__ __forceinline__ void ldvec(const T *p, T (&v)[V]) {
 
 // out row r pools fine row p = rows ? rows[r] : r; neighbour j's value is
 // owner ? (owner[j] >= 0 ? feat[owner[j]] : 0) : feat[j]; winners hold the fine index j.
-// B slots in flight per batch (fp32 x 8 channels: 4, so that the loaded rows stay within
+// B slots in flight per batch (fp32 x 8 channels: 4 in the forward, 2 in the backward -- 78 registers, three 256-thread blocks per SM -- so that the loaded rows stay within
 // ~128 registers and two or more 256-thread blocks fit an SM: these are latency-bound)
 template <typename T, int V, int B = (V == 8 ? 4 : 8)>
 __global__ void __launch_bounds__(256)
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(256)
 // (i, s) ascending, each i once, with q = owner ? owner[i] : i (skipped when < 0) and
 // winners[q, ch] == j -- the additions of _native.pyx:165-168 restricted to the rows that can
 // be non-zero (dropping additions of +0.0 cannot change an accumulator that starts at +0.0).
-template <typename T, int V, int B = (V == 8 ? 4 : 8)>
+template <typename T, int V, int B = (V == 8 ? 2 : 8)>
 __global__ void __launch_bounds__(256)
     pool_select_bwd_kernel(int64_t m, int c, int k, const T *__restrict__ g, const int32_t *__restrict__ winners,
                            Csr csr, const int32_t *__restrict__ rows, const int32_t *__restrict__ owner,
