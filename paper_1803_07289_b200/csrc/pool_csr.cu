@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// fp32 backward, 8 channels per thread, 4 reverse entries in flight (32-byte argmax and
+// fp32 backward, 8 channels per thread, 2 reverse entries in flight (32-byte argmax and
 // upstream loads); same additions in the same order as pool_bwd_vec_kernel.
 __device__ __forceinline__ void ldg8i(const int32_t *p, int32_t (&v)[8]) {
     asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
@@ -256,6 +256,7 @@ __device__ __forceinline__ void ldg8i(const int32_t *p, int32_t (&v)[8]) {
                  : "l"(p));
 }
 
+constexpr int kPB = 2;  // reverse entries in flight per thread
 __global__ void __launch_bounds__(256)
     pool_bwd_w8_kernel(int64_t total, int64_t n, int c, int k, const float *__restrict__ g,
                        const int32_t *__restrict__ argmax, Csr csr, float *__restrict__ df) {
@@ -271,19 +272,19 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[e] = 0.f;
         int64_t prev = -1;
-        for (int32_t qb = q0; qb < q1; qb += 4) {
-            int32_t ii[4];
-            int32_t am[4][8];
-            float gv[4][8];
+        for (int32_t qb = q0; qb < q1; qb += kPB) {
+            int32_t ii[kPB];
+            int32_t am[kPB][8];
+            float gv[kPB][8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) ii[u] = __ldg(csr.ent + min(qb + u, q1 - 1)) / k;
+            for (int u = 0; u < kPB; ++u) ii[u] = __ldg(csr.ent + min(qb + u, q1 - 1)) / k;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kPB; ++u) {
                 ldg8i(argmax + (int64_t)ii[u] * c + ch, am[u]);
                 ldg8f(g + (int64_t)ii[u] * c + ch, gv[u]);
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kPB; ++u) {
                 if (qb + u < q1 && ii[u] != prev) {  // row i lists j twice: routed once
                     prev = ii[u];
 #pragma unroll
@@ -803,11 +804,12 @@ int launch_pool_bwd(int64_t total, int64_t n, int c, int k, const T *g, const in
         }();
         if (!v4 && c % 8 == 0 && reinterpret_cast<uintptr_t>(g) % 32 == 0 &&
             reinterpret_cast<uintptr_t>(argmax) % 32 == 0 && reinterpret_cast<uintptr_t>(df) % 16 == 0) {
-            // 128-thread blocks: at 92 registers five fit an SM (20 warps) against two of 256
-            // (16 warps); latency-bound, 7 M x 64 ch: 2.97 -> 2.76 ms (FC_POOL_BWD_BLOCK for A/B)
+            // latency-bound: with 2 reverse entries in flight the kernel needs 58 registers, so
+            // four 256-thread blocks fill an SM (32 warps); 7 M x 64 ch 2.76 ms (4 entries, 92
+            // registers, 128-thread blocks) -> 2.29 ms (FC_POOL_BWD_BLOCK for A/B)
             static const int bs = [] {
                 const char *e = getenv("FC_POOL_BWD_BLOCK");
-                return e ? atoi(e) : 128;
+                return e ? atoi(e) : 256;
             }();
             pool_bwd_w8_kernel<<<grid_1d(total * (c / 8), bs), bs, 0, st>>>(total, n, c, k, (const float *)g, argmax, csr,
                                                                           (float *)df);
