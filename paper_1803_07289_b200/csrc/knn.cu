@@ -308,6 +308,30 @@ __device__ __forceinline__ double cell_gap2(const GridParams &gp, double x, int 
     return g * g;
 }
 
+// candidates of a contiguous bucket range (a forced-inline function, not a lambda: the
+// lambda was outlined as a call, which put the top-k arrays in local memory)
+template <int KK>
+__device__ __forceinline__ void knn_scan(int32_t s0, int32_t s1, const double4 *__restrict__ sp, int32_t i,
+                                         const double4 &pi, int d, double (&bd)[KK], int32_t (&bi)[KK]) {
+    for (int32_t s = s0; s < s1; ++s) {
+        const double4 pj = sp[s];
+        const int32_t j = __double2loint(pj.w);
+        if (j == i) continue;
+        double dist = 0.0, dv;
+        dv = __dsub_rn(pi.x, pj.x);
+        dist = __dadd_rn(dist, __dmul_rn(dv, dv));
+        if (d > 1) {
+            dv = __dsub_rn(pi.y, pj.y);
+            dist = __dadd_rn(dist, __dmul_rn(dv, dv));
+        }
+        if (d > 2) {
+            dv = __dsub_rn(pi.z, pj.z);
+            dist = __dadd_rn(dist, __dmul_rn(dv, dv));
+        }
+        topk_insert<KK>(bd, bi, dist, j);
+    }
+}
+
 template <int KK>
 __global__ void __launch_bounds__(128)
     knn_grid_query_kernel(int64_t n, int k, const double4 *__restrict__ sp,
@@ -332,25 +356,6 @@ __global__ void __launch_bounds__(128)
     const int rmax = max(gp.G[0], max(gp.G[1], gp.G[2]));
     const double margin = gp.h * 1e-7;
     const double prune_margin = gp.h * gp.h * 1e-6;
-    auto scan = [&](int32_t s0, int32_t s1) {  // candidates of a contiguous bucket range
-        for (int32_t s = s0; s < s1; ++s) {
-            const double4 pj = sp[s];
-            const int32_t j = __double2loint(pj.w);
-            if (j == i) continue;
-            double dist = 0.0, dv;
-            dv = __dsub_rn(pi.x, pj.x);
-            dist = __dadd_rn(dist, __dmul_rn(dv, dv));
-            if (gp.d > 1) {
-                dv = __dsub_rn(pi.y, pj.y);
-                dist = __dadd_rn(dist, __dmul_rn(dv, dv));
-            }
-            if (gp.d > 2) {
-                dv = __dsub_rn(pi.z, pj.z);
-                dist = __dadd_rn(dist, __dmul_rn(dv, dv));
-            }
-            topk_insert<KK>(bd, bi, dist, j);
-        }
-    };
     for (int r = 0;; ++r) {
         for (int dz = -r; dz <= r; ++dz) {
             const int z = c[2] + dz;
@@ -362,10 +367,11 @@ __global__ void __launch_bounds__(128)
                 // lower bound of the squared distance to any point of a cell of row (y, z):
                 // cells farther than the current k-1-th distance cannot contribute (exact:
                 // boundary cells are unbounded outward, and a small margin covers rounding)
-                double worst = DBL_MAX;
+                // the k-1-th distance, by register selects (an index by the runtime kk would put
+                // the top-k arrays in local memory)
+                double worst = bd[0];
 #pragma unroll
-                for (int a = 0; a < KK; ++a)
-                    if (a == kk - 1) worst = bd[a];
+                for (int a = 1; a < KK; ++a) worst = a <= kk - 1 ? bd[a] : worst;
                 const double gyz = cell_gap2(gp, px[1], y, 1) + cell_gap2(gp, px[2], z, 2);
                 if (worst < DBL_MAX && gyz - prune_margin > worst) continue;  // the whole row
                 const int64_t rb = ((int64_t)z * gp.G[1] + y) * gp.G[0];
@@ -376,13 +382,13 @@ __global__ void __launch_bounds__(128)
                         while (x0 <= x1 && gyz + cell_gap2(gp, px[0], x0, 0) - prune_margin > worst) ++x0;
                         while (x1 >= x0 && gyz + cell_gap2(gp, px[0], x1, 0) - prune_margin > worst) --x1;
                     }
-                    if (x0 <= x1) scan(off[rb + x0], off[rb + x1 + 1]);
+                    if (x0 <= x1) knn_scan<KK>(off[rb + x0], off[rb + x1 + 1], sp, i, pi, gp.d, bd, bi);
                 } else {
                     for (int dx = -r; dx <= r; dx += 2 * r) {
                         const int x = c[0] + dx;
                         if (x < 0 || x >= gp.G[0]) continue;
                         if (worst < DBL_MAX && gyz + cell_gap2(gp, px[0], x, 0) - prune_margin > worst) continue;
-                        scan(off[rb + x], off[rb + x + 1]);
+                        knn_scan<KK>(off[rb + x], off[rb + x + 1], sp, i, pi, gp.d, bd, bi);
                     }
                 }
             }
@@ -397,10 +403,9 @@ __global__ void __launch_bounds__(128)
         }
         if (dmin == DBL_MAX) break;  // the block covers the whole grid
         dmin -= margin;
-        double worst = DBL_MAX;
+        double worst = bd[0];
 #pragma unroll
-        for (int a = 0; a < KK; ++a)
-            if (a == kk - 1) worst = bd[a];
+        for (int a = 1; a < KK; ++a) worst = a <= kk - 1 ? bd[a] : worst;
         if (dmin > 0.0 && worst < dmin * dmin) break;
     }
     int32_t *row = out + (int64_t)i * k;
