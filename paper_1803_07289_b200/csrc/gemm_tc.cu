@@ -110,7 +110,9 @@ __global__ void pack_b_kernel(PackArgs a) {
         const int n = ch * a.nc + rr;
         float v = 0.f;
         if (n < a.nrows) {
-            for (int s = 0; s < a.nseg; ++s) {
+#pragma unroll
+            for (int s = 0; s < kMaxOps; ++s) {  // (compile-time indices: the segment table stays in registers)
+                if (s >= a.nseg) break;
                 const int kl = (kb - a.seg_kb0[s]) * 32 + kk;
                 if (kb >= a.seg_kb0[s] && kl < a.seg_k[s]) {
                     const int kc = a.seg_src[s] + kl;
